@@ -1,0 +1,180 @@
+/*
+ * include/tsw.h — C ABI of the B200-native leapfrog solver for the regularised tsunami equation
+ * (arXiv 2005.11931, "Tsunami propagation for singular topographies").
+ *
+ * The hot path (BASELINE.json north_star): explicit second-order leapfrog time stepping of
+ *     u_tt = Σ_j ∂_j( h_{j,ε}(x) ∂_j u )                    PAPER.md §2, eq. (Equation)
+ * with u(0) = u0, u_t(0) = u1, homogeneous Dirichlet boundary (§3.3), on a
+ * 1D or 2D uniform grid, where the singular depth is replaced by the mollified family
+ * h_ε = h * φ_ε, φ_ε(x) = ε⁻¹ φ(x/ε), φ(x) = c·exp(1/(x²−1)) on |x| < 1,
+ * δ ↦ φ_ε, δ² ↦ φ_ε².  Readings of the paper: DESIGN.md §3 (R1–R25).
+ *
+ * Conventions (all calls):
+ *  - Every function returns tsw_status; no C++ exception or longjmp crosses this ABI.  On error
+ *    the ctx is unchanged (arguments are validated before any device work) and
+ *    tsw_last_error(ctx) returns a message (thread-local; ctx may be NULL after tsw_create).
+ *  - Grid (R9): nx, ny count GLOBAL nodes including the Dirichlet boundary nodes.  Node i of an
+ *    n-node axis is at ((2i + 1 − n)·d)/2 (a centred grid), face i+1/2 at ((2i + 2 − n)·d)/2.
+ *  - Field layout seen by the caller: [batch][ny_local][nx] row-major, x fastest, in the ctx
+ *    dtype (float or double), where ny_local is this rank's slab height (ny if nranks == 1;
+ *    1 if dim == 1).  Internally rows are padded and carry one ghost row above and below.
+ *  - Host buffers are only read/written during the call (copied); device buffers passed with
+ *    on_device = 1 must be valid device pointers of the ctx's device and are read during the
+ *    call (stream-ordered on the ctx stream).  The ctx owns all of its device memory.
+ *  - Asynchrony: tsw_step is asynchronous on the ctx stream.  tsw_energy, tsw_wave2, tsw_read
+ *    (to host), tsw_info and tsw_sync synchronise the ctx stream.
+ *  - Threads: one ctx per host thread at a time.  Different ctxs are independent.
+ *  - There is no CPU fallback: without a CUDA device tsw_create fails with TSW_ERR_CUDA.
+ */
+#ifndef TSW_H
+#define TSW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tsw_ctx tsw_ctx; /* opaque */
+
+typedef enum {
+    TSW_OK = 0,
+    TSW_ERR_ARG = 1,      /* invalid argument (sizes, ε ∉ (0,1], h < c0, dt ≤ 0, …) */
+    TSW_ERR_CFL = 2,      /* dt above the Gershgorin leapfrog bound (R16) */
+    TSW_ERR_STATE = 3,    /* call out of order (e.g. step before set_initial, energy at n = 0) */
+    TSW_ERR_CUDA = 4,     /* CUDA runtime error or no device */
+    TSW_ERR_NCCL = 5,     /* NCCL unavailable or failed */
+    TSW_ERR_OOM = 6,      /* device allocation failed */
+    TSW_ERR_UNSTABLE = 7  /* reserved: non-finite energy */
+} tsw_status;
+
+typedef enum { TSW_F32 = 0, TSW_F64 = 1 } tsw_dtype;
+
+/* Depth kinds (§3.1 Cases; R5–R8). */
+typedef enum {
+    TSW_H_CONST = 0,        /* h1 = h2 = h_b */
+    TSW_H_DELTA_LINE_X = 1, /* h1 = h_b + A·φ_ε(x − xs)^order, h2 = h_b  (δ-line along x = xs; 1D: δ-point) */
+    TSW_H_DELTA_POINT = 2,  /* h1 = h2 = h_b + A·(φ_ε(x − xs)·φ_ε(y − ys))^order  (tensor mollifier, R3) */
+    TSW_H_FACES = 3         /* dense caller-given faces (tsw_set_coeff_faces) */
+} tsw_hkind;
+
+/* tsw_set_initial flags */
+#define TSW_ALLOW_UNSTABLE 1u /* skip the CFL check */
+#define TSW_INIT_SHARED 2u    /* u0/u1 are ONE [ny_local][nx] field used by every member */
+
+typedef struct {
+    int32_t dim;          /* 1 or 2 */
+    int64_t nx, ny;       /* global node counts incl. boundary; nx ≥ 3; ny ≥ 3 (2D) or 1 (1D) */
+    double dx, dy;        /* grid steps > 0 (dy ignored in 1D) */
+    int32_t batch;        /* B ≥ 1 members (an ε-family, §2 very weak solution net P:385–403) */
+    int32_t dtype;        /* tsw_dtype: working precision T of the fields and prescaled coefficients */
+    int32_t rank, nranks; /* row-slab decomposition along y (2D only); nranks = 1 ⇒ single GPU */
+    int32_t device;       /* CUDA device ordinal; −1 ⇒ the calling thread's current device */
+    void* stream;         /* cudaStream_t to run on, or NULL ⇒ the ctx creates its own stream */
+} tsw_grid_desc;
+
+typedef struct {
+    int32_t kind;                 /* tsw_hkind (not TSW_H_FACES) */
+    int32_t order;                /* 1: φ_ε (δ) ; 2: φ_ε² (δ²) */
+    double h_background;          /* h_b ≥ c0 > 0 (positivity) */
+    double amp;                   /* A ≥ 0 (A = 0 ⇒ background member) */
+    double xs, ys;                /* singular point / line location */
+    const double* eps;            /* [batch] host array, each ε ∈ (0, 1] */
+    const double* amp_per_member; /* optional [batch] host array overriding amp, or NULL */
+} tsw_coeff_desc;
+
+/* Create a solver context: validates the grid, allocates the two time levels on the device.
+ * Errors: TSW_ERR_ARG (bad sizes / rank), TSW_ERR_CUDA (no device), TSW_ERR_OOM. */
+tsw_status tsw_create(const tsw_grid_desc* grid, tsw_ctx** out);
+
+/* Free all device memory and the NCCL communicator owned by ctx.  NULL is a no-op. */
+void tsw_destroy(tsw_ctx* ctx);
+
+/* S1 coefficient builder (§2 h_{i,ε} = h_i * ψ_ε; §3.1): evaluates
+ * h_ε in fp64 on the device at every half-grid face of this rank's slab (R2).  Validates
+ * h_b > 0, A ≥ 0, ε ∈ (0, 1], order ∈ {1, 2}.  Prescaling to T happens in tsw_set_initial. */
+tsw_status tsw_set_coeff(tsw_ctx* ctx, const tsw_coeff_desc* h);
+
+/* Dense override of the fp64 faces (kind TSW_H_FACES), host (on_device = 0) or device pointers:
+ *   h1 [batch][ny_local][nx−1]   face (i+1/2, j) of local row j
+ *   h2 [batch][ny_local+1][nx]   row k = face (i, g+1/2) with g = (first global row of the slab) + k − 1;
+ *                                rows outside the global grid are ignored (2D only; NULL in 1D).
+ * Values must be > 0 where used. */
+tsw_status tsw_set_coeff_faces(tsw_ctx* ctx, const double* h1, const double* h2, int on_device);
+
+/* Copy the fp64 faces h_ε the stepper uses (after tsw_set_coeff or tsw_set_coeff_faces) to host
+ * arrays in the tsw_set_coeff_faces layout (h1 [batch][ny_local][nx−1]; h2 [batch][ny_local+1][nx],
+ * rows outside the global grid written as 0; h2 may be NULL; 1D: h1 [batch][nx−1]).  Synchronises. */
+tsw_status tsw_read_faces(tsw_ctx* ctx, double* h1, double* h2);
+
+/* Set u(0) = u0 and u_t(0) = u1, the time step dt, and reset n = 0.
+ *   u0, u1: [batch][ny_local][nx] in the ctx dtype (or [ny_local][nx] with TSW_INIT_SHARED);
+ *           u1 may be NULL (⇒ 0).  Boundary entries are ignored and forced to +0 (R10).
+ * Prescales c = fl_T((dt²/d²)·h) (R19) and checks dt ≤ 2/√ρ_G (R16) unless TSW_ALLOW_UNSTABLE.
+ * Errors: TSW_ERR_STATE (no coefficients), TSW_ERR_ARG (dt ≤ 0), TSW_ERR_CFL. */
+tsw_status tsw_set_initial(tsw_ctx* ctx, const void* u0, const void* u1, double dt, int on_device,
+                           uint32_t flags);
+
+/* Advance nsteps ≥ 0 time levels (asynchronous).  From n = 0 the first level is the Taylor start
+ * u¹ = (u⁰ + dt·u₁) + ½L(u⁰) (R11); every later level is leapfrog
+ * u^{n+1} = (2u^n − u^{n−1}) + L(u^n) with the canonical contraction-free operator of DESIGN.md §2.
+ * With nranks > 1 each level is followed by the ghost-row exchange.  Errors: TSW_ERR_STATE. */
+tsw_status tsw_step(tsw_ctx* ctx, int64_t nsteps);
+
+/* Loopback slabs on ONE device: advance ctxs[0..n−1] (ranks 0..n−1 of one decomposition, same
+ * device and stream, no NCCL) by nsteps, exchanging ghost rows with device copies.  Test and
+ * emulation path for the multi-GPU decomposition. */
+tsw_status tsw_group_step(tsw_ctx** ctxs, int32_t n, int64_t nsteps);
+
+/* S5 discrete energy E^{n−1/2} of the current levels (R17; discrete form of CL-01):
+ *   E = (dx·dy/dt²)·[Σ_interior (u^n − u^{n−1})² + Σ_faces c·(Δu^n)(Δu^{n−1})]   (1D: dx/dt²)
+ * accumulated in fp64 with the stepper's own rounded c; summed over ranks (NCCL) when nranks > 1.
+ *   out_B: host double[batch].  Errors: TSW_ERR_STATE if n < 1. */
+tsw_status tsw_energy(tsw_ctx* ctx, double* out_B);
+
+/* S6 second-wave amplitude (R18; §3.2.3, qualitative): for every member b
+ *   A₂⁺ = max, A₂⁻ = min over nodes with x_i ≤ xs − ε_b of fl_T(u_b − u_{bg_member})
+ * with the global row-major index (g·nx + i) of the first extremum; empty region ⇒ 0 and −1.
+ *   out_B2: host double[batch][2]; argidx_B2: host int64[batch][2] (may be NULL). */
+tsw_status tsw_wave2(tsw_ctx* ctx, int32_t bg_member, double* out_B2, int64_t* argidx_B2);
+
+/* Copy a level of this rank's slab out: which = 0 ⇒ u^n, 1 ⇒ u^{n−1}; dst is [batch][ny_local][nx]
+ * in the ctx dtype, host (to_device = 0, synchronous) or device (to_device = 1, stream-ordered). */
+tsw_status tsw_read(tsw_ctx* ctx, int32_t which, void* dst, int32_t to_device);
+
+/* Resume from a saved state: un = u^n, unm1 = u^{n−1} (layout as tsw_read), level n ≥ 1 and dt.
+ * Coefficients must be set; they are prescaled with this dt.  Boundary entries forced to +0. */
+tsw_status tsw_set_state(tsw_ctx* ctx, const void* un, const void* unm1, int64_t n, double dt,
+                         int32_t on_device, uint32_t flags);
+
+/* Current level n, time t = n·dt, and the Gershgorin bound 2/√ρ_G of the current coefficients
+ * (0 if unknown).  Any pointer may be NULL.  Synchronises. */
+tsw_status tsw_info(tsw_ctx* ctx, int64_t* n, double* t, double* dt_max);
+
+/* Block until the ctx stream is idle. */
+tsw_status tsw_sync(tsw_ctx* ctx);
+
+/* Number of kernels this ctx has launched so far (the bench's gpu_launches evidence). */
+int64_t tsw_launch_count(const tsw_ctx* ctx);
+
+/* Tuning knob: TSW_OPT_ROWS_PER_ITEM (rows per warp work item of the 2D stencil, ≥ 1; 0 = auto). */
+#define TSW_OPT_ROWS_PER_ITEM 1
+tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
+
+/* NCCL row-slab plumbing.  tsw_nccl_unique_id writes a 128-byte ncclUniqueId
+ * (call on rank 0, broadcast it, e.g. with torch.distributed); tsw_nccl_init creates the ctx's
+ * communicator over grid.nranks ranks.  libnccl.so.2 is resolved at run time. */
+tsw_status tsw_nccl_unique_id(void* out_128B);
+tsw_status tsw_nccl_init(tsw_ctx* ctx, const void* unique_id_128B);
+
+/* Message of the last failing call on this thread (never NULL). */
+const char* tsw_last_error(const tsw_ctx* ctx);
+
+/* Library version string. */
+const char* tsw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSW_H */

@@ -1,0 +1,596 @@
+// tsw_kernels.cuh — sm_100a kernels of the leapfrog hot path (DESIGN.md §1 rows S1–S6).
+//
+// Written from PAPER.md and DESIGN.md's readings; shares nothing with oracle/.
+// Arithmetic of the stepper uses the __d*_rn / __f*_rn intrinsics (never contracted into FMA)
+// in the canonical tree of DESIGN.md §2, so every node's value is the same IEEE operation
+// sequence as any other implementation of that tree (R19).  The library is also built with
+// --fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tsw {
+
+// PAPER.md §3.1, "c ≃ 2.2523 to get ∫φ = 1" (R4: 1/∫_{-1}^{1} e^{1/(x²−1)} dx).
+constexpr double TSW_MOLLIFIER_C = 2.252283621043581;
+
+enum CoeffMode { MODE_LINE = 0, MODE_DENSE = 1 };
+
+// ------------------------------------------------------------------------------------------
+// rounding-explicit arithmetic (no contraction)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ double r_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double r_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float r_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float r_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b); }
+
+template <typename T> struct Vec16;
+template <> struct Vec16<double> { using type = double2; static constexpr int N = 2; };
+template <> struct Vec16<float> { using type = float4; static constexpr int N = 4; };
+
+template <typename T>
+__device__ __forceinline__ void vload(const T* __restrict__ p, T (&v)[Vec16<T>::N]) {
+    using VT = typename Vec16<T>::type;
+    VT x = __ldg(reinterpret_cast<const VT*>(p));
+    const T* e = reinterpret_cast<const T*>(&x);
+#pragma unroll
+    for (int k = 0; k < Vec16<T>::N; ++k) v[k] = e[k];
+}
+
+// streaming load (read once: u^{n-1})
+template <typename T>
+__device__ __forceinline__ void vload_cs(const T* p, T (&v)[Vec16<T>::N]) {
+    using VT = typename Vec16<T>::type;
+    VT x = __ldcs(reinterpret_cast<const VT*>(p));
+    const T* e = reinterpret_cast<const T*>(&x);
+#pragma unroll
+    for (int k = 0; k < Vec16<T>::N; ++k) v[k] = e[k];
+}
+
+template <typename T>
+__device__ __forceinline__ void vstore(T* p, const T (&v)[Vec16<T>::N]) {
+    using VT = typename Vec16<T>::type;
+    VT x;
+    T* e = reinterpret_cast<T*>(&x);
+#pragma unroll
+    for (int k = 0; k < Vec16<T>::N; ++k) e[k] = v[k];
+    __stcs(reinterpret_cast<VT*>(p), x);
+}
+
+// One node of S2/S3 (DESIGN.md §2 canonical tree):
+//   lap = (c1r·(u_{i+1}−u_i) − c1l·(u_i−u_{i−1})) + (c2u·(u_{j+1}−u_j) − c2d·(u_j−u_{j−1}))
+//   START: u¹ = (u⁰ + dt·v) + ½·lap        else: u^{n+1} = (2u^n − u^{n−1}) + lap
+template <typename T, bool START, bool TWO_D>
+__device__ __forceinline__ T node_update(T u, T ul, T ur, T ud, T uu, T p, T c1l, T c1r, T c2d, T c2u,
+                                         T dtT) {
+    T dxp = r_sub(ur, u);
+    T dxm = r_sub(u, ul);
+    T lap = r_sub(r_mul(c1r, dxp), r_mul(c1l, dxm));
+    if (TWO_D) {
+        T dyp = r_sub(uu, u);
+        T dym = r_sub(u, ud);
+        lap = r_add(lap, r_sub(r_mul(c2u, dyp), r_mul(c2d, dym)));
+    }
+    if (START) return r_add(r_add(u, r_mul(dtT, p)), r_mul((T)0.5, lap));
+    return r_add(r_sub(r_mul((T)2, u), p), lap);
+}
+
+// ------------------------------------------------------------------------------------------
+// S2/S3: 2D stencil, warp column strips marching in y (register-rotated u^{n}[j−1..j+1])
+// ------------------------------------------------------------------------------------------
+// Storage: fields [B][rows_alloc][pitch]; storage row s ↔ global row g = r0 + s − 1 (s = 0 and
+// s = ny_local + 1 are ghost rows).  pitch is a multiple of 32·V elements.
+// Coefficients: LINE  c1[b][cpitch] (face i+1/2), c2[b] scalar;
+//               DENSE c1[b][rows_alloc][pitch] (face (i+1/2, s)), c2[b][rows_alloc][pitch]
+//               where c2 row s = face between storage rows s−1 and s.
+template <typename T>
+struct StepArgs {
+    const T* __restrict__ ucur;  // u^n
+    T* __restrict__ uprev;       // u^{n−1} in, u^{n+1} out (in place; START: u1 in, u¹ out)
+    const T* __restrict__ c1;
+    const T* __restrict__ c2;
+    int64_t pitch;         // elements per stored row
+    int64_t mstride;       // elements per member (rows_alloc·pitch)
+    int64_t cstride1;      // elements per member of c1
+    int64_t cstride2;      // elements per member of c2
+    int64_t nx;            // global nodes per row
+    int32_t s_lo, s_hi;    // storage rows updated: [s_lo, s_hi)
+    int32_t rows_per_item; // R
+    int32_t chunks;        // ceil((s_hi − s_lo)/R)
+    int64_t strips;        // pitch / (32·V)
+    int64_t items;         // strips · chunks · B
+    T dtT;
+};
+
+template <typename T, int MODE, bool START>
+__global__ void __launch_bounds__(256) k_step2d(const StepArgs<T> a) {
+    constexpr int V = Vec16<T>::N;
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+
+    for (int64_t item = gwarp; item < a.items; item += nwarps) {
+        const int64_t strip = item % a.strips;
+        const int64_t rest = item / a.strips;
+        const int chunk = int(rest % a.chunks);
+        const int b = int(rest / a.chunks);
+        const int64_t cs = strip * 32 * V;       // first column of the strip
+        const int64_t col = cs + int64_t(lane) * V;
+        const int s0 = a.s_lo + chunk * a.rows_per_item;
+        const int s1 = min(s0 + a.rows_per_item, a.s_hi);
+        const T* __restrict__ ub = a.ucur + b * a.mstride;
+        T* __restrict__ pb = a.uprev + b * a.mstride;
+        const bool has_l = (lane == 0) && (cs > 0);
+        const bool has_r = (lane == 31) && (cs + 32 * V < a.pitch);
+
+        bool interior[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) interior[k] = (col + k >= 1) && (col + k <= a.nx - 2);
+
+        // LINE coefficients are row-invariant: load once per item.
+        T c1r[V], c1l[V];
+        T c2s = (T)0;
+        if (MODE == MODE_LINE) {
+            const T* c1b = a.c1 + b * a.cstride1;
+            vload(c1b + col, c1r);
+            T left = __shfl_up_sync(0xffffffffu, c1r[V - 1], 1);
+            if (lane == 0) left = has_l ? c1b[cs - 1] : (T)0;
+            c1l[0] = left;
+#pragma unroll
+            for (int k = 1; k < V; ++k) c1l[k] = c1r[k - 1];
+            c2s = a.c2[b];
+        }
+
+        // register window: up = row s−1, cu = row s, dn = row s+1 ; pv = u^{n−1} row s
+        T up[V], cu[V], dn[V], pv[V];
+        T hl_c = 0, hr_c = 0, hl_d = 0, hr_d = 0;
+        vload(ub + (s0 - 1) * a.pitch + col, up);
+        vload(ub + s0 * a.pitch + col, cu);
+        if (has_l) hl_c = ub[s0 * a.pitch + cs - 1];
+        if (has_r) hr_c = ub[s0 * a.pitch + cs + 32 * V];
+        if (s0 < s1) {
+            vload(ub + (s0 + 1) * a.pitch + col, dn);
+            vload_cs(pb + s0 * a.pitch + col, pv);
+            if (has_l) hl_d = ub[(s0 + 1) * a.pitch + cs - 1];
+            if (has_r) hr_d = ub[(s0 + 1) * a.pitch + cs + 32 * V];
+        }
+        // DENSE: c2 face below row s (= c2 row s) carried between iterations
+        T c2lo[V];
+        if (MODE == MODE_DENSE) vload(a.c2 + b * a.cstride2 + s0 * a.pitch + col, c2lo);
+
+        for (int s = s0; s < s1; ++s) {
+            // prefetch row s+2 of u^n and row s+1 of u^{n−1}
+            T dn2[V], pv2[V];
+            T hl_d2 = 0, hr_d2 = 0;
+            const bool more = (s + 1 < s1);
+            if (more) {
+                vload(ub + (s + 2) * a.pitch + col, dn2);
+                vload_cs(pb + (s + 1) * a.pitch + col, pv2);
+                if (has_l) hl_d2 = ub[(s + 2) * a.pitch + cs - 1];
+                if (has_r) hr_d2 = ub[(s + 2) * a.pitch + cs + 32 * V];
+            }
+            T c1r_d[V], c1l_d[V], c2hi[V];
+            if (MODE == MODE_DENSE) {
+                const T* c1row = a.c1 + b * a.cstride1 + s * a.pitch;
+                vload(c1row + col, c1r_d);
+                T left = __shfl_up_sync(0xffffffffu, c1r_d[V - 1], 1);
+                if (lane == 0) left = has_l ? c1row[cs - 1] : (T)0;
+                c1l_d[0] = left;
+#pragma unroll
+                for (int k = 1; k < V; ++k) c1l_d[k] = c1r_d[k - 1];
+                vload(a.c2 + b * a.cstride2 + (s + 1) * a.pitch + col, c2hi);
+            }
+            // x neighbours across lanes
+            T left = __shfl_up_sync(0xffffffffu, cu[V - 1], 1);
+            T right = __shfl_down_sync(0xffffffffu, cu[0], 1);
+            if (lane == 0) left = hl_c;
+            if (lane == 31) right = hr_c;
+            T out[V];
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                T ul = (k == 0) ? left : cu[k - 1];
+                T ur = (k == V - 1) ? right : cu[k + 1];
+                T l1 = (MODE == MODE_LINE) ? c1l[k] : c1l_d[k];
+                T r1 = (MODE == MODE_LINE) ? c1r[k] : c1r_d[k];
+                T d2 = (MODE == MODE_LINE) ? c2s : c2lo[k];
+                T u2 = (MODE == MODE_LINE) ? c2s : c2hi[k];
+                T v = node_update<T, START, true>(cu[k], ul, ur, up[k], dn[k], pv[k], l1, r1, d2, u2, a.dtT);
+                out[k] = interior[k] ? v : (T)0;
+            }
+            vstore(pb + s * a.pitch + col, out);
+            // rotate
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                up[k] = cu[k];
+                cu[k] = dn[k];
+                if (more) {
+                    dn[k] = dn2[k];
+                    pv[k] = pv2[k];
+                }
+                if (MODE == MODE_DENSE) c2lo[k] = c2hi[k];
+            }
+            hl_c = hl_d;
+            hr_c = hr_d;
+            hl_d = hl_d2;
+            hr_d = hr_d2;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// S2/S3: 1D, persistent — one CTA per member, both levels resident in shared memory, all
+// steps in one launch (config 1: 2000 fp64 nodes × 3 arrays = 48 KB).
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(1024) k_step1d_smem(T* __restrict__ ucur, T* __restrict__ uprev,
+                                                      const T* __restrict__ c1, int64_t nx, int64_t pitch,
+                                                      int64_t cpitch, int64_t nsteps, int start, T dtT) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* A = reinterpret_cast<T*>(smem_raw);  // u^n
+    T* P = A + pitch;                       // u^{n−1} → u^{n+1}
+    T* C = P + pitch;                       // c1
+    const int b = blockIdx.x;
+    T* ug = ucur + b * pitch;
+    T* pg = uprev + b * pitch;
+    const T* cg = c1 + b * cpitch;
+    for (int64_t i = threadIdx.x; i < nx; i += blockDim.x) {
+        A[i] = ug[i];
+        P[i] = pg[i];
+        if (i < nx - 1) C[i] = cg[i];
+    }
+    __syncthreads();
+    int64_t k = 0;
+    if (start && nsteps > 0) {
+        for (int64_t i = 1 + threadIdx.x; i < nx - 1; i += blockDim.x)
+            P[i] = node_update<T, true, false>(A[i], A[i - 1], A[i + 1], (T)0, (T)0, P[i], C[i - 1], C[i], (T)0,
+                                               (T)0, dtT);
+        __syncthreads();
+        T* t = A; A = P; P = t;
+        k = 1;
+    }
+    for (; k < nsteps; ++k) {
+        for (int64_t i = 1 + threadIdx.x; i < nx - 1; i += blockDim.x)
+            P[i] = node_update<T, false, false>(A[i], A[i - 1], A[i + 1], (T)0, (T)0, P[i], C[i - 1], C[i],
+                                                (T)0, (T)0, dtT);
+        __syncthreads();
+        T* t = A; A = P; P = t;
+    }
+    for (int64_t i = threadIdx.x; i < nx; i += blockDim.x) {
+        ug[i] = A[i];
+        pg[i] = P[i];
+    }
+}
+
+// 1D fallback when the row does not fit in shared memory: one launch per step.
+template <typename T, bool START>
+__global__ void k_step1d_global(const T* __restrict__ ucur, T* __restrict__ uprev, const T* __restrict__ c1,
+                                int64_t nx, int64_t pitch, int64_t cpitch, T dtT) {
+    const int b = blockIdx.y;
+    const T* u = ucur + b * pitch;
+    T* p = uprev + b * pitch;
+    const T* c = c1 + b * cpitch;
+    for (int64_t i = 1 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nx - 1;
+         i += int64_t(gridDim.x) * blockDim.x)
+        p[i] = node_update<T, START, false>(u[i], u[i - 1], u[i + 1], (T)0, (T)0, p[i], c[i - 1], c[i], (T)0, (T)0,
+                                            dtT);
+}
+
+// ------------------------------------------------------------------------------------------
+// S1: coefficient builder — h_ε at half-grid faces in fp64
+// ------------------------------------------------------------------------------------------
+// φ_ε(d) = (c/ε)·exp(1/(t² − 1)), t = d/ε, for |t| < 1; exactly 0 otherwise (R25).
+__device__ __forceinline__ double phi_eps(double d, double eps) {
+    double t = d / eps;
+    if (!(fabs(t) < 1.0)) return 0.0;
+    return (TSW_MOLLIFIER_C / eps) * exp(1.0 / (t * t - 1.0));
+}
+// R9: node i at ((2i+1−n)·d)/2, face i+1/2 at ((2i+2−n)·d)/2.
+__device__ __forceinline__ double grid_node(int64_t i, int64_t n, double d) { return (double(2 * i + 1 - n) * d) / 2.0; }
+__device__ __forceinline__ double grid_face(int64_t i, int64_t n, double d) { return (double(2 * i + 2 - n) * d) / 2.0; }
+
+struct CoeffArgs {
+    int kind, order;
+    double hb, xs, ys, dx, dy;
+    const double* eps;  // [B] device
+    const double* amp;  // [B] device
+    int64_t nx, ny;
+    int64_t r0;         // first global row of the slab
+    int64_t rows_alloc, pitch, cpitch;
+    int B;
+};
+
+// LINE (and CONST): h1[b][i], i < nx−1 (pad 0), h2[b] = h_b.
+__global__ void k_coeff_line(CoeffArgs a, double* __restrict__ h1, double* __restrict__ h2) {
+    const int b = blockIdx.y;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.cpitch; i += int64_t(gridDim.x) * blockDim.x) {
+        double h = 0.0;
+        if (i < a.nx - 1) {
+            if (a.kind == 0) {
+                h = a.hb;
+            } else {
+                double bump = phi_eps(grid_face(i, a.nx, a.dx) - a.xs, a.eps[b]);
+                if (a.order == 2) bump = bump * bump;
+                h = a.hb + a.amp[b] * bump;
+            }
+        }
+        h1[b * a.cpitch + i] = h;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) h2[b] = a.hb;
+}
+
+// POINT, dense storage layout: h1[b][s][i] = face (i+1/2, g), h2[b][s][i] = face (i, g−1/2),
+// g = r0 + s − 1; entries outside the global grid are 0.
+__global__ void k_coeff_point(CoeffArgs a, double* __restrict__ h1, double* __restrict__ h2) {
+    const int b = blockIdx.z;
+    const int64_t s = blockIdx.y;
+    const int64_t g = a.r0 + s - 1;
+    const double eps = a.eps[b], amp = a.amp[b];
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.pitch; i += int64_t(gridDim.x) * blockDim.x) {
+        double v1 = 0.0, v2 = 0.0;
+        if (g >= 0 && g < a.ny && i < a.nx - 1) {
+            double bump = phi_eps(grid_face(i, a.nx, a.dx) - a.xs, eps) * phi_eps(grid_node(g, a.ny, a.dy) - a.ys, eps);
+            if (a.order == 2) bump = bump * bump;
+            v1 = a.hb + amp * bump;
+        }
+        if (g >= 1 && g < a.ny && i < a.nx) {
+            double bump = phi_eps(grid_node(i, a.nx, a.dx) - a.xs, eps) * phi_eps(grid_face(g - 1, a.ny, a.dy) - a.ys, eps);
+            if (a.order == 2) bump = bump * bump;
+            v2 = a.hb + amp * bump;
+        }
+        const int64_t o = (b * a.rows_alloc + s) * a.pitch + i;
+        h1[o] = v1;
+        h2[o] = v2;
+    }
+}
+
+// O3-equivalent prescale: c = fl_T(r·h), r = (dt·dt)/(d·d) computed on the device in fp64.
+template <typename T>
+__global__ void k_prescale(const double* __restrict__ h, T* __restrict__ c, int64_t n, double dt, double d) {
+    const double r = (dt * dt) / (d * d);
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+        c[k] = (T)(r * h[k]);
+}
+
+// S1b: Gershgorin ρ_G = max over updated nodes of 2·(Σ h_x/dx² + Σ h_y/dy²) (R16); atomicMax on
+// the bit pattern (non-negative doubles order like their int64 bits).
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* addr, double v) {
+    if (v >= 0.0) atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+struct CflArgs {
+    int dim, mode;
+    const double* h1;
+    const double* h2;
+    int64_t nx, pitch, cpitch, rows_alloc;
+    int32_t s_lo, s_hi;  // storage rows of updated nodes
+    double dx, dy;
+    int B;
+};
+
+__global__ void k_cfl(CflArgs a, unsigned long long* __restrict__ out) {
+    const int b = blockIdx.z;
+    double m = 0.0;
+    const int64_t rows = (a.dim == 1) ? 1 : (a.s_hi - a.s_lo);
+    const int64_t total = rows * (a.nx - 2);
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = 1 + k % (a.nx - 2);
+        double r;
+        if (a.dim == 1) {
+            const double* h = a.h1 + b * a.cpitch;
+            r = 2.0 * ((h[i - 1] + h[i]) / (a.dx * a.dx));
+        } else if (a.mode == MODE_LINE) {
+            const double* h = a.h1 + b * a.cpitch;
+            const double hy = a.h2[b];
+            r = 2.0 * ((h[i - 1] + h[i]) / (a.dx * a.dx) + (hy + hy) / (a.dy * a.dy));
+        } else {
+            const int64_t s = a.s_lo + k / (a.nx - 2);
+            const double* h1r = a.h1 + (b * a.rows_alloc + s) * a.pitch;
+            const double* h2b = a.h2 + b * a.rows_alloc * a.pitch;
+            r = 2.0 * ((h1r[i - 1] + h1r[i]) / (a.dx * a.dx) + (h2b[s * a.pitch + i] + h2b[(s + 1) * a.pitch + i]) / (a.dy * a.dy));
+        }
+        m = fmax(m, r);
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomic_max_pos(out, m);
+}
+
+// Minimum over faces (positivity check).
+__global__ void k_min_pos(const double* __restrict__ h, int64_t n, unsigned long long* __restrict__ out_neg_count) {
+    unsigned long long c = 0;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+        c += (h[k] <= 0.0 || !(h[k] == h[k])) ? 1ull : 0ull;
+    if (c) atomicAdd(out_neg_count, c);
+}
+
+// ------------------------------------------------------------------------------------------
+// S5: discrete energy E^{n+1/2} partials (R17), fp64, warp-shuffle then block reduction.
+// Terms owned by node (s, i) of the slab: its kinetic term (interior node), its x face
+// (i+1/2) if its row is interior, and its y face (g+1/2) if g ≤ ny−2 and i interior.
+// ------------------------------------------------------------------------------------------
+struct EnergyArgs {
+    int dim, mode;
+    const void* unp1;  // u^{n}   of the ctx (the newer level)
+    const void* un;    // u^{n−1}
+    const void* c1;
+    const void* c2;
+    int64_t nx, ny, r0, pitch, mstride, cstride1, cstride2, ny_local;
+    int nblk;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_energy(EnergyArgs a, double* __restrict__ partial) {
+    const int b = blockIdx.y;
+    const T* A = static_cast<const T*>(a.unp1) + b * a.mstride;
+    const T* Bv = static_cast<const T*>(a.un) + b * a.mstride;
+    const T* C1 = static_cast<const T*>(a.c1) + b * a.cstride1;
+    const T* C2 = static_cast<const T*>(a.c2) + b * a.cstride2;
+    const int64_t rows = (a.dim == 1) ? 1 : a.ny_local;
+    const int64_t total = rows * a.nx;
+    double acc = 0.0;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k % a.nx;
+        const int64_t s = (a.dim == 1) ? 0 : 1 + k / a.nx;
+        const int64_t g = (a.dim == 1) ? 0 : a.r0 + s - 1;
+        const bool row_int = (a.dim == 1) || (g >= 1 && g <= a.ny - 2);
+        const bool col_int = (i >= 1 && i <= a.nx - 2);
+        const int64_t o = s * a.pitch + i;
+        const double a0 = (double)A[o], b0 = (double)Bv[o];
+        if (row_int && col_int) {
+            const double d = a0 - b0;
+            acc += d * d;
+        }
+        if (row_int && i <= a.nx - 2) {
+            const double c = (a.dim == 1 || a.mode == MODE_LINE) ? (double)C1[i] : (double)C1[s * a.pitch + i];
+            acc += (c * ((double)A[o + 1] - a0)) * ((double)Bv[o + 1] - b0);
+        }
+        if (a.dim == 2 && col_int && g <= a.ny - 2) {
+            const double c = (a.mode == MODE_LINE) ? (double)C2[0] : (double)C2[(s + 1) * a.pitch + i];
+            acc += (c * ((double)A[o + a.pitch] - a0)) * ((double)Bv[o + a.pitch] - b0);
+        }
+    }
+    __shared__ double red[32];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) partial[b * a.nblk + blockIdx.x] = v;
+    }
+}
+
+// Final pass: one warp per member sums its partials in a fixed order (deterministic) and scales.
+__global__ void k_energy_final(const double* __restrict__ partial, int nblk, double w, double* __restrict__ out) {
+    const int b = blockIdx.x;
+    double v = 0.0;
+    for (int k = threadIdx.x; k < nblk; k += 32) v += partial[b * nblk + k];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[b] = w * v;
+}
+
+// ------------------------------------------------------------------------------------------
+// S6: second-wave amplitude (R18) — max/min of fl_T(u_b − u_bg) over x_i ≤ xs − ε_b with the
+// first (smallest global row-major index) extremum; warp shuffle arg-reductions.
+// ------------------------------------------------------------------------------------------
+struct Wave2Args {
+    int dim;
+    const void* u;
+    int64_t nx, ny, r0, pitch, mstride, ny_local;
+    int bg;
+    double dx, xs;
+    const double* eps;  // [B] device
+    int nblk;
+};
+
+struct ArgVal {
+    double v;
+    long long i;
+};
+__device__ __forceinline__ void arg_better_max(double& v, long long& i, double v2, long long i2) {
+    if (i2 >= 0 && (i < 0 || v2 > v || (v2 == v && i2 < i))) { v = v2; i = i2; }
+}
+__device__ __forceinline__ void arg_better_min(double& v, long long& i, double v2, long long i2) {
+    if (i2 >= 0 && (i < 0 || v2 < v || (v2 == v && i2 < i))) { v = v2; i = i2; }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_wave2(Wave2Args a, ArgVal* __restrict__ partial) {
+    const int b = blockIdx.y;
+    const T* U = static_cast<const T*>(a.u) + b * a.mstride;
+    const T* G = static_cast<const T*>(a.u) + a.bg * a.mstride;
+    const double xlim = a.xs - a.eps[b];
+    const int64_t rows = (a.dim == 1) ? 1 : a.ny_local;
+    const int64_t total = rows * a.nx;
+    double vmax = 0.0, vmin = 0.0;
+    long long imax = -1, imin = -1;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k % a.nx;
+        if (!(grid_node(i, a.nx, a.dx) <= xlim)) continue;
+        const int64_t s = (a.dim == 1) ? 0 : 1 + k / a.nx;
+        const int64_t g = (a.dim == 1) ? 0 : a.r0 + s - 1;
+        const T d = r_sub(U[s * a.pitch + i], G[s * a.pitch + i]);
+        const long long gi = (long long)(g * a.nx + i);
+        arg_better_max(vmax, imax, (double)d, gi);
+        arg_better_min(vmin, imin, (double)d, gi);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, vmax, o);
+        long long i2 = __shfl_xor_sync(0xffffffffu, imax, o);
+        arg_better_max(vmax, imax, v2, i2);
+        v2 = __shfl_xor_sync(0xffffffffu, vmin, o);
+        i2 = __shfl_xor_sync(0xffffffffu, imin, o);
+        arg_better_min(vmin, imin, v2, i2);
+    }
+    __shared__ ArgVal smax[32], smin[32];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        smax[w] = {vmax, imax};
+        smin[w] = {vmin, imin};
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bv = 0.0, cv = 0.0;
+        long long bi = -1, ci = -1;
+        for (int k = 0; k < int(blockDim.x >> 5); ++k) {
+            arg_better_max(bv, bi, smax[k].v, smax[k].i);
+            arg_better_min(cv, ci, smin[k].v, smin[k].i);
+        }
+        partial[(b * a.nblk + blockIdx.x) * 2 + 0] = {bv, bi};
+        partial[(b * a.nblk + blockIdx.x) * 2 + 1] = {cv, ci};
+    }
+}
+
+__global__ void k_wave2_final(const ArgVal* __restrict__ partial, int nblk, double* __restrict__ out,
+                              long long* __restrict__ idx) {
+    const int b = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    double bv = 0.0, cv = 0.0;
+    long long bi = -1, ci = -1;
+    for (int k = 0; k < nblk; ++k) {
+        arg_better_max(bv, bi, partial[(b * nblk + k) * 2].v, partial[(b * nblk + k) * 2].i);
+        arg_better_min(cv, ci, partial[(b * nblk + k) * 2 + 1].v, partial[(b * nblk + k) * 2 + 1].i);
+    }
+    out[2 * b] = (bi >= 0) ? bv : 0.0;
+    out[2 * b + 1] = (ci >= 0) ? cv : 0.0;
+    idx[2 * b] = bi;
+    idx[2 * b + 1] = ci;
+}
+
+// ------------------------------------------------------------------------------------------
+// plumbing kernels
+// ------------------------------------------------------------------------------------------
+// Force the Dirichlet nodes of the slab (global rows 0 / ny−1, columns 0 / nx−1) and the padding
+// columns to +0 (R10).
+template <typename T>
+__global__ void k_zero_boundary(T* __restrict__ u, int dim, int64_t nx, int64_t ny, int64_t r0, int64_t ny_local,
+                                int64_t pitch, int64_t mstride) {
+    const int b = blockIdx.y;
+    T* ub = u + b * mstride;
+    const int64_t rows = (dim == 1) ? 1 : ny_local;
+    const int64_t total = rows * pitch;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k % pitch;
+        const int64_t s = (dim == 1) ? 0 : 1 + k / pitch;
+        const int64_t g = (dim == 1) ? 0 : r0 + s - 1;
+        const bool bnd = (i == 0) || (i >= nx - 1) || (dim == 2 && (g == 0 || g == ny - 1));
+        if (bnd) ub[s * pitch + i] = (T)0;
+    }
+}
+
+}  // namespace tsw

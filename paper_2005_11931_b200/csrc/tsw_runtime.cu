@@ -1,0 +1,983 @@
+// tsw_runtime.cu — the C ABI of include/tsw.h: context, device memory, launch configuration,
+// ghost-row exchange (NCCL or loopback) and the diagnostics' reductions.  Kernels are in
+// tsw_kernels.cuh.  No C++ exception crosses the ABI; every CUDA/NCCL error becomes a status.
+#include "tsw.h"
+#include "tsw_kernels.cuh"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace tsw;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+tsw_status fail(tsw_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(e_ == cudaErrorMemoryAllocation ? TSW_ERR_OOM : TSW_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+    } while (0)
+
+#define CKL()                                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = cudaGetLastError();                                                       \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(TSW_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+// ---- NCCL, resolved at run time (the process usually already holds torch's libnccl.so.2) ----
+struct NcclId {
+    char internal[128];
+};
+struct Nccl {
+    bool ok = false;
+    void* h = nullptr;
+    int (*GetUniqueId)(NcclId*) = nullptr;
+    int (*CommInitRank)(void**, int, NcclId, int) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+enum { NCCL_INT64 = 4, NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0, NCCL_MAX = 2, NCCL_MIN = 3 };
+
+Nccl& nccl() {
+    static Nccl n;
+    static bool tried = false;
+    if (tried) return n;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return n;
+    n.h = h;
+#define NSYM(f, name) n.f = reinterpret_cast<decltype(n.f)>(dlsym(h, name))
+    NSYM(GetUniqueId, "ncclGetUniqueId");
+    NSYM(CommInitRank, "ncclCommInitRank");
+    NSYM(CommDestroy, "ncclCommDestroy");
+    NSYM(Send, "ncclSend");
+    NSYM(Recv, "ncclRecv");
+    NSYM(AllReduce, "ncclAllReduce");
+    NSYM(GroupStart, "ncclGroupStart");
+    NSYM(GroupEnd, "ncclGroupEnd");
+    NSYM(GetErrorString, "ncclGetErrorString");
+#undef NSYM
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Send && n.Recv && n.AllReduce && n.GroupStart &&
+           n.GroupEnd && n.GetErrorString;
+    return n;
+}
+
+#define NK(call)                                                                                   \
+    do {                                                                                           \
+        int r_ = (call);                                                                           \
+        if (r_ != 0) return fail(TSW_ERR_NCCL, "%s: %s", #call, nccl().GetErrorString(r_));       \
+    } while (0)
+
+int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
+
+}  // namespace
+
+struct tsw_ctx {
+    tsw_grid_desc g{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+    size_t esz = 8;
+    int V = 2;
+    // slab geometry
+    int64_t r0 = 0, r1 = 0, ny_local = 1, rows_alloc = 1, pitch = 0, mstride = 0;
+    int32_t s_lo = 0, s_hi = 0;  // storage rows of updated nodes (2D)
+    // time levels: buf[cur] = u^n, buf[cur ^ 1] = u^{n−1}
+    void* buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    // coefficients (fp64 faces h, prescaled T faces c)
+    bool have_coeff = false;
+    int mode = MODE_LINE;
+    int kind = TSW_H_CONST;
+    double* h1 = nullptr;
+    double* h2 = nullptr;
+    void* c1 = nullptr;
+    void* c2 = nullptr;
+    int64_t cstride1 = 0, cstride2 = 0;  // per-member elements
+    double* d_eps = nullptr;
+    double* d_amp = nullptr;
+    double xs = 0.0, ys = 0.0;
+    bool have_eps = false;
+    double dt_max = 0.0;
+    // state
+    bool have_init = false;
+    int64_t n = 0;
+    double dt = 0.0;
+    // scratch
+    double* d_partial = nullptr;
+    int nblk_red = 0;
+    double* d_out = nullptr;
+    ArgVal* d_argpart = nullptr;
+    long long* d_idx = nullptr;
+    unsigned long long* d_u64 = nullptr;
+    // launch bookkeeping
+    int64_t launches = 0;
+    int rows_per_item_opt = 0;
+    int step_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};  // [mode][start]
+    // NCCL
+    void* comm = nullptr;
+};
+
+namespace {
+
+bool is_f64(const tsw_ctx* c) { return c->g.dtype == TSW_F64; }
+
+tsw_status set_dev(tsw_ctx* c) {
+    CK(cudaSetDevice(c->device));
+    return TSW_OK;
+}
+
+int grid_for(int64_t n, int threads, int cap) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return int(b);
+}
+
+// ---- 2D stencil launch ---------------------------------------------------------------------
+template <typename T, int MODE, bool START>
+tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
+    if (s_hi <= s_lo) return TSW_OK;
+    StepArgs<T> a;
+    a.ucur = static_cast<const T*>(c->buf[c->cur]);
+    a.uprev = static_cast<T*>(c->buf[c->cur ^ 1]);
+    a.c1 = static_cast<const T*>(c->c1);
+    a.c2 = static_cast<const T*>(c->c2);
+    a.pitch = c->pitch;
+    a.mstride = c->mstride;
+    a.cstride1 = c->cstride1;
+    a.cstride2 = c->cstride2;
+    a.nx = c->g.nx;
+    a.s_lo = s_lo;
+    a.s_hi = s_hi;
+    a.strips = c->pitch / (32 * Vec16<T>::N);
+    a.dtT = (T)c->dt;
+    int& occ = c->step_blocks_per_sm[MODE][START ? 1 : 0];
+    if (occ == 0) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d<T, MODE, START>, 256, 0));
+        if (occ < 1) occ = 1;
+    }
+    const int64_t resident_warps = int64_t(occ) * c->sm_count * 8;
+    const int64_t rows = s_hi - s_lo;
+    int R = c->rows_per_item_opt;
+    if (R <= 0) {
+        // ≈ 8 work items per resident warp, but at least 16 rows per item (halo re-read ≤ 2/R)
+        int64_t want_chunks = (8 * resident_warps + a.strips * c->g.batch - 1) / (a.strips * c->g.batch);
+        if (want_chunks < 1) want_chunks = 1;
+        R = int((rows + want_chunks - 1) / want_chunks);
+        if (R < 16) R = 16;
+    }
+    if (R > rows) R = int(rows);
+    a.rows_per_item = R;
+    a.chunks = int((rows + R - 1) / R);
+    a.items = a.strips * a.chunks * c->g.batch;
+    int64_t blocks = (a.items + 7) / 8;
+    blocks = std::min<int64_t>(blocks, int64_t(occ) * c->sm_count);
+    k_step2d<T, MODE, START><<<unsigned(blocks), 256, 0, c->stream>>>(a);
+    CKL();
+    c->launches++;
+    return TSW_OK;
+}
+
+tsw_status launch_step2d(tsw_ctx* c, bool start, int32_t s_lo, int32_t s_hi) {
+    if (is_f64(c)) {
+        if (c->mode == MODE_LINE)
+            return start ? launch_step2d_t<double, MODE_LINE, true>(c, s_lo, s_hi)
+                         : launch_step2d_t<double, MODE_LINE, false>(c, s_lo, s_hi);
+        return start ? launch_step2d_t<double, MODE_DENSE, true>(c, s_lo, s_hi)
+                     : launch_step2d_t<double, MODE_DENSE, false>(c, s_lo, s_hi);
+    }
+    if (c->mode == MODE_LINE)
+        return start ? launch_step2d_t<float, MODE_LINE, true>(c, s_lo, s_hi)
+                     : launch_step2d_t<float, MODE_LINE, false>(c, s_lo, s_hi);
+    return start ? launch_step2d_t<float, MODE_DENSE, true>(c, s_lo, s_hi)
+                 : launch_step2d_t<float, MODE_DENSE, false>(c, s_lo, s_hi);
+}
+
+// ---- 1D ---------------------------------------------------------------------------------------
+template <typename T>
+tsw_status step1d_t(tsw_ctx* c, int64_t k) {
+    const bool start = (c->n == 0);
+    const size_t smem = size_t(3) * c->pitch * sizeof(T);
+    T* u = static_cast<T*>(c->buf[c->cur]);
+    T* p = static_cast<T*>(c->buf[c->cur ^ 1]);
+    const T* c1 = static_cast<const T*>(c->c1);
+    if (smem <= 200 * 1024) {
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_step1d_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int threads = int(std::min<int64_t>(1024, round_up(c->g.nx, 32)));
+        k_step1d_smem<T><<<c->g.batch, threads, smem, c->stream>>>(u, p, c1, c->g.nx, c->pitch, c->cstride1, k,
+                                                                   start ? 1 : 0, (T)c->dt);
+        CKL();
+        c->launches++;
+        c->n += k;  // the kernel writes the newest level back into buf[cur]
+        return TSW_OK;
+    }
+    const dim3 grid(unsigned(grid_for(c->g.nx, 256, 4 * c->sm_count)), unsigned(c->g.batch));
+    for (int64_t s = 0; s < k; ++s) {
+        const T* uc = static_cast<const T*>(c->buf[c->cur]);
+        T* up = static_cast<T*>(c->buf[c->cur ^ 1]);
+        if (c->n == 0)
+            k_step1d_global<T, true><<<grid, 256, 0, c->stream>>>(uc, up, c1, c->g.nx, c->pitch, c->cstride1, (T)c->dt);
+        else
+            k_step1d_global<T, false><<<grid, 256, 0, c->stream>>>(uc, up, c1, c->g.nx, c->pitch, c->cstride1, (T)c->dt);
+        CKL();
+        c->launches++;
+        c->cur ^= 1;
+        c->n++;
+    }
+    return TSW_OK;
+}
+
+// ---- ghost rows -------------------------------------------------------------------------------
+// NCCL: send my first owned row up to rank−1 and my last owned row down to rank+1; receive their
+// rows into my ghost rows (storage rows 0 and ny_local+1).  Rows are contiguous: no packing.
+tsw_status exchange_nccl(tsw_ctx* c, void* field) {
+    if (c->g.nranks <= 1) return TSW_OK;
+    if (!c->comm) return fail(TSW_ERR_STATE, "nranks > 1 but tsw_nccl_init was not called");
+    Nccl& N = nccl();
+    const int dt = is_f64(c) ? NCCL_F64 : NCCL_F32;
+    char* base = static_cast<char*>(field);
+    const size_t row = size_t(c->pitch) * c->esz;
+    NK(N.GroupStart());
+    for (int b = 0; b < c->g.batch; ++b) {
+        char* m = base + size_t(b) * c->mstride * c->esz;
+        if (c->g.rank > 0) {
+            NK(N.Send(m + 1 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, c->stream));
+            NK(N.Recv(m + 0 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, c->stream));
+        }
+        if (c->g.rank < c->g.nranks - 1) {
+            NK(N.Send(m + size_t(c->ny_local) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, c->stream));
+            NK(N.Recv(m + size_t(c->ny_local + 1) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, c->stream));
+        }
+    }
+    NK(N.GroupEnd());
+    return TSW_OK;
+}
+
+// Loopback: ranks are ctxs on one device and stream; copy rows device-to-device.
+tsw_status exchange_loopback(tsw_ctx** cs, int n) {
+    for (int r = 0; r + 1 < n; ++r) {
+        tsw_ctx* a = cs[r];      // upper slab (smaller rows)
+        tsw_ctx* b = cs[r + 1];  // lower slab
+        const size_t row_a = size_t(a->pitch) * a->esz;
+        const size_t row_b = size_t(b->pitch) * b->esz;
+        for (int m = 0; m < a->g.batch; ++m) {
+            char* ma = static_cast<char*>(a->buf[a->cur]) + size_t(m) * a->mstride * a->esz;
+            char* mb = static_cast<char*>(b->buf[b->cur]) + size_t(m) * b->mstride * b->esz;
+            // a's last owned row → b's ghost row 0 ; b's first owned row → a's ghost row ny_local+1
+            CK(cudaMemcpyAsync(mb, ma + size_t(a->ny_local) * row_a, size_t(a->g.nx) * a->esz, cudaMemcpyDeviceToDevice,
+                               a->stream));
+            CK(cudaMemcpyAsync(ma + size_t(a->ny_local + 1) * row_a, mb + row_b, size_t(b->g.nx) * b->esz,
+                               cudaMemcpyDeviceToDevice, a->stream));
+        }
+    }
+    return TSW_OK;
+}
+
+tsw_status prescale_all(tsw_ctx* c) {
+    const int threads = 256;
+    const int64_t n1 = c->cstride1 * c->g.batch;
+    const int64_t n2 = c->cstride2 * c->g.batch;
+    const int cap = 8 * c->sm_count;
+    if (is_f64(c)) {
+        k_prescale<double><<<grid_for(n1, threads, cap), threads, 0, c->stream>>>(c->h1, static_cast<double*>(c->c1), n1, c->dt, c->g.dx);
+        CKL();
+        if (c->g.dim == 2) {
+            k_prescale<double><<<grid_for(n2, threads, cap), threads, 0, c->stream>>>(c->h2, static_cast<double*>(c->c2), n2, c->dt, c->g.dy);
+            CKL();
+        }
+    } else {
+        k_prescale<float><<<grid_for(n1, threads, cap), threads, 0, c->stream>>>(c->h1, static_cast<float*>(c->c1), n1, c->dt, c->g.dx);
+        CKL();
+        if (c->g.dim == 2) {
+            k_prescale<float><<<grid_for(n2, threads, cap), threads, 0, c->stream>>>(c->h2, static_cast<float*>(c->c2), n2, c->dt, c->g.dy);
+            CKL();
+        }
+    }
+    c->launches += (c->g.dim == 2) ? 2 : 1;
+    return TSW_OK;
+}
+
+tsw_status alloc_coeff(tsw_ctx* c, int mode) {
+    if (c->have_coeff && c->mode == mode) return TSW_OK;
+    cudaFree(c->h1);
+    cudaFree(c->h2);
+    cudaFree(c->c1);
+    cudaFree(c->c2);
+    c->h1 = c->h2 = nullptr;
+    c->c1 = c->c2 = nullptr;
+    c->have_coeff = false;
+    c->mode = mode;
+    if (mode == MODE_LINE) {
+        c->cstride1 = c->pitch;
+        c->cstride2 = 1;
+    } else {
+        c->cstride1 = c->mstride;
+        c->cstride2 = c->mstride;
+    }
+    const size_t B = size_t(c->g.batch);
+    CK(cudaMalloc(&c->h1, B * c->cstride1 * sizeof(double)));
+    CK(cudaMalloc(&c->h2, B * c->cstride2 * sizeof(double)));
+    CK(cudaMalloc(&c->c1, B * c->cstride1 * c->esz));
+    CK(cudaMalloc(&c->c2, B * c->cstride2 * c->esz));
+    CK(cudaMemsetAsync(c->h1, 0, B * c->cstride1 * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(c->h2, 0, B * c->cstride2 * sizeof(double), c->stream));
+    return TSW_OK;
+}
+
+// Gershgorin bound and positivity of the current faces; all-reduced over ranks.
+tsw_status check_faces(tsw_ctx* c) {
+    CK(cudaMemsetAsync(c->d_u64, 0, 2 * sizeof(unsigned long long), c->stream));
+    CflArgs a;
+    a.dim = c->g.dim;
+    a.mode = c->mode;
+    a.h1 = c->h1;
+    a.h2 = c->h2;
+    a.nx = c->g.nx;
+    a.pitch = c->pitch;
+    a.cpitch = c->cstride1;
+    a.rows_alloc = c->rows_alloc;
+    a.s_lo = c->s_lo;
+    a.s_hi = c->s_hi;
+    a.dx = c->g.dx;
+    a.dy = c->g.dy;
+    a.B = c->g.batch;
+    const int64_t rows = (c->g.dim == 1) ? 1 : (c->s_hi - c->s_lo);
+    dim3 grid(unsigned(grid_for(rows * (c->g.nx - 2), 256, 2 * c->sm_count)), 1, unsigned(c->g.batch));
+    if (rows > 0) {
+        k_cfl<<<grid, 256, 0, c->stream>>>(a, c->d_u64);
+        CKL();
+        c->launches++;
+    }
+    unsigned long long rho_bits = 0;
+    CK(cudaMemcpyAsync(&rho_bits, c->d_u64, sizeof(rho_bits), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    double rho;
+    memcpy(&rho, &rho_bits, sizeof(rho));
+    if (c->g.nranks > 1 && c->comm) {
+        double* d = reinterpret_cast<double*>(c->d_u64);
+        CK(cudaMemcpyAsync(d, &rho, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        NK(nccl().AllReduce(d, d, 1, NCCL_F64, NCCL_MAX, c->comm, c->stream));
+        CK(cudaMemcpyAsync(&rho, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (!(rho > 0.0) || !std::isfinite(rho)) return fail(TSW_ERR_ARG, "non-finite or zero Gershgorin radius (%g)", rho);
+    c->dt_max = 2.0 / std::sqrt(rho);
+    return TSW_OK;
+}
+
+tsw_status load_field(tsw_ctx* c, void* dst_buf, const void* src, bool shared, int on_device) {
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const size_t w = size_t(c->g.nx) * c->esz;
+    const size_t rows = size_t(c->ny_local);
+    for (int b = 0; b < c->g.batch; ++b) {
+        const char* s = static_cast<const char*>(src) + (shared ? 0 : size_t(b) * rows * w);
+        char* d = static_cast<char*>(dst_buf) + size_t(b) * c->mstride * c->esz +
+                  (c->g.dim == 2 ? size_t(c->pitch) * c->esz : 0);
+        CK(cudaMemcpy2DAsync(d, size_t(c->pitch) * c->esz, s, w, w, rows, kind, c->stream));
+    }
+    return TSW_OK;
+}
+
+tsw_status zero_boundary(tsw_ctx* c, void* field) {
+    const int64_t rows = (c->g.dim == 1) ? 1 : c->ny_local;
+    dim3 grid(unsigned(grid_for(rows * c->pitch, 256, 4 * c->sm_count)), unsigned(c->g.batch));
+    if (is_f64(c))
+        k_zero_boundary<double><<<grid, 256, 0, c->stream>>>(static_cast<double*>(field), c->g.dim, c->g.nx, c->g.ny,
+                                                             c->r0, c->ny_local, c->pitch, c->mstride);
+    else
+        k_zero_boundary<float><<<grid, 256, 0, c->stream>>>(static_cast<float*>(field), c->g.dim, c->g.nx, c->g.ny,
+                                                            c->r0, c->ny_local, c->pitch, c->mstride);
+    CKL();
+    c->launches++;
+    return TSW_OK;
+}
+
+tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int on_device, uint32_t flags,
+                      int64_t n) {
+    if (!c->have_coeff) return fail(TSW_ERR_STATE, "set coefficients (tsw_set_coeff / tsw_set_coeff_faces) first");
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(TSW_ERR_ARG, "dt must be finite and > 0 (got %g)", dt);
+    if (!a) return fail(TSW_ERR_ARG, "u0 / un is NULL");
+    if (!(flags & TSW_ALLOW_UNSTABLE) && !(dt <= c->dt_max))
+        return fail(TSW_ERR_CFL, "dt = %.17g exceeds the Gershgorin leapfrog bound 2/sqrt(rho_G) = %.17g (R16)", dt,
+                    c->dt_max);
+    const bool shared = (flags & TSW_INIT_SHARED) != 0;
+    const size_t bytes = size_t(c->g.batch) * c->mstride * c->esz;
+    c->cur = 0;
+    CK(cudaMemsetAsync(c->buf[0], 0, bytes, c->stream));
+    CK(cudaMemsetAsync(c->buf[1], 0, bytes, c->stream));
+    tsw_status st = load_field(c, c->buf[0], a, shared, on_device);
+    if (st) return st;
+    if (b) {
+        st = load_field(c, c->buf[1], b, shared, on_device);
+        if (st) return st;
+    }
+    if ((st = zero_boundary(c, c->buf[0]))) return st;
+    if ((st = zero_boundary(c, c->buf[1]))) return st;
+    c->dt = dt;
+    if ((st = prescale_all(c))) return st;
+    if (c->g.dim == 2 && c->g.nranks > 1) {
+        if ((st = exchange_nccl(c, c->buf[0]))) return st;
+    }
+    c->n = n;
+    c->have_init = true;
+    return TSW_OK;
+}
+
+tsw_status do_steps(tsw_ctx* c, int64_t k) {
+    if (k <= 0) return TSW_OK;
+    if (c->g.dim == 1) return is_f64(c) ? step1d_t<double>(c, k) : step1d_t<float>(c, k);
+    for (int64_t s = 0; s < k; ++s) {
+        tsw_status st = launch_step2d(c, c->n == 0, c->s_lo, c->s_hi);
+        if (st) return st;
+        c->cur ^= 1;
+        c->n++;
+        if (c->g.nranks > 1) {
+            if ((st = exchange_nccl(c, c->buf[c->cur]))) return st;
+        }
+    }
+    return TSW_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+// ABI
+// =============================================================================================
+extern "C" {
+
+const char* tsw_version(void) { return "tsw 0.1 (sm_100a)"; }
+
+const char* tsw_last_error(const tsw_ctx*) { return g_err.c_str(); }
+
+tsw_status tsw_create(const tsw_grid_desc* gd, tsw_ctx** out) {
+    if (!gd || !out) return fail(TSW_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    const tsw_grid_desc g = *gd;
+    if (g.dim != 1 && g.dim != 2) return fail(TSW_ERR_ARG, "dim must be 1 or 2");
+    if (g.nx < 3) return fail(TSW_ERR_ARG, "nx must be >= 3");
+    if (g.dim == 2 && g.ny < 3) return fail(TSW_ERR_ARG, "ny must be >= 3 in 2D");
+    if (g.dim == 1 && g.ny != 1) return fail(TSW_ERR_ARG, "ny must be 1 in 1D");
+    if (!(g.dx > 0) || (g.dim == 2 && !(g.dy > 0))) return fail(TSW_ERR_ARG, "dx, dy must be > 0");
+    if (g.batch < 1) return fail(TSW_ERR_ARG, "batch must be >= 1");
+    if (g.dtype != TSW_F32 && g.dtype != TSW_F64) return fail(TSW_ERR_ARG, "dtype must be TSW_F32 or TSW_F64");
+    if (g.nranks < 1 || g.rank < 0 || g.rank >= g.nranks) return fail(TSW_ERR_ARG, "bad rank/nranks");
+    if (g.dim == 1 && g.nranks != 1) return fail(TSW_ERR_ARG, "1D grids are not slab-decomposed");
+    if (g.dim == 2 && g.ny < 2 * int64_t(g.nranks)) return fail(TSW_ERR_ARG, "need >= 2 rows per rank");
+    if (g.nx > (int64_t(1) << 31) || g.ny > (int64_t(1) << 31)) return fail(TSW_ERR_ARG, "grid too large");
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(TSW_ERR_CUDA, "no CUDA device (%s); this library has no CPU fallback", cudaGetErrorString(e));
+    tsw_ctx* c = new tsw_ctx();
+    c->g = g;
+    if (g.device >= 0) {
+        c->device = g.device;
+    } else if (cudaGetDevice(&c->device) != cudaSuccess) {
+        delete c;
+        return fail(TSW_ERR_CUDA, "cudaGetDevice failed");
+    }
+    auto bail = [&](tsw_status s) {
+        tsw_destroy(c);
+        return s;
+    };
+    if (cudaSetDevice(c->device) != cudaSuccess) return bail(fail(TSW_ERR_CUDA, "cudaSetDevice(%d) failed", c->device));
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
+    c->esz = (g.dtype == TSW_F64) ? 8 : 4;
+    c->V = int(16 / c->esz);
+    if (g.dim == 1) {
+        c->r0 = 0;
+        c->r1 = 1;
+        c->ny_local = 1;
+        c->rows_alloc = 1;
+        c->pitch = round_up(g.nx, 32);
+    } else {
+        const int64_t base = g.ny / g.nranks, rem = g.ny % g.nranks;
+        c->r0 = g.rank * base + std::min<int64_t>(g.rank, rem);
+        c->r1 = c->r0 + base + (g.rank < rem ? 1 : 0);
+        c->ny_local = c->r1 - c->r0;
+        c->rows_alloc = c->ny_local + 2;
+        c->pitch = round_up(g.nx, 32 * c->V);
+        c->s_lo = (c->r0 == 0) ? 2 : 1;
+        c->s_hi = int32_t((c->r1 == g.ny) ? c->ny_local : c->ny_local + 1);
+    }
+    c->mstride = c->rows_alloc * c->pitch;
+    if (g.stream) {
+        c->stream = static_cast<cudaStream_t>(g.stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(TSW_ERR_CUDA, "cudaStreamCreate failed"));
+        c->own_stream = true;
+    }
+    const size_t bytes = size_t(g.batch) * c->mstride * c->esz;
+    for (int k = 0; k < 2; ++k) {
+        e = cudaMalloc(&c->buf[k], bytes);
+        if (e != cudaSuccess)
+            return bail(fail(e == cudaErrorMemoryAllocation ? TSW_ERR_OOM : TSW_ERR_CUDA, "cudaMalloc(%zu): %s", bytes,
+                             cudaGetErrorString(e)));
+        cudaMemsetAsync(c->buf[k], 0, bytes, c->stream);
+    }
+    c->nblk_red = std::max(1, std::min(4 * c->sm_count, 65535 / std::max(1, g.batch)));
+    if (cudaMalloc(&c->d_partial, sizeof(double) * size_t(g.batch) * c->nblk_red) != cudaSuccess ||
+        cudaMalloc(&c->d_out, sizeof(double) * 4 * size_t(g.batch)) != cudaSuccess ||
+        cudaMalloc(&c->d_argpart, sizeof(ArgVal) * 2 * size_t(g.batch) * c->nblk_red) != cudaSuccess ||
+        cudaMalloc(&c->d_idx, sizeof(long long) * 4 * size_t(g.batch)) != cudaSuccess ||
+        cudaMalloc(&c->d_u64, sizeof(unsigned long long) * 4) != cudaSuccess ||
+        cudaMalloc(&c->d_eps, sizeof(double) * size_t(g.batch)) != cudaSuccess ||
+        cudaMalloc(&c->d_amp, sizeof(double) * size_t(g.batch)) != cudaSuccess)
+        return bail(fail(TSW_ERR_OOM, "scratch allocation failed"));
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(TSW_ERR_CUDA, "stream sync failed"));
+    *out = c;
+    return TSW_OK;
+}
+
+void tsw_destroy(tsw_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    void* ptrs[] = {c->buf[0], c->buf[1], c->h1, c->h2, c->c1, c->c2, c->d_eps, c->d_amp,
+                    c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+tsw_status tsw_set_coeff(tsw_ctx* c, const tsw_coeff_desc* h) {
+    if (!c || !h) return fail(TSW_ERR_ARG, "NULL argument");
+    if (h->kind != TSW_H_CONST && h->kind != TSW_H_DELTA_LINE_X && h->kind != TSW_H_DELTA_POINT)
+        return fail(TSW_ERR_ARG, "kind must be CONST, DELTA_LINE_X or DELTA_POINT (FACES: tsw_set_coeff_faces)");
+    if (h->kind == TSW_H_DELTA_POINT && c->g.dim != 2) return fail(TSW_ERR_ARG, "DELTA_POINT needs dim == 2");
+    if (h->order != 1 && h->order != 2) return fail(TSW_ERR_ARG, "order must be 1 or 2");
+    if (!(h->h_background > 0.0) || !std::isfinite(h->h_background))
+        return fail(TSW_ERR_ARG, "h_background must be > 0 (positivity 0 < c0 <= h, P:165)");
+    if (!std::isfinite(h->xs) || !std::isfinite(h->ys)) return fail(TSW_ERR_ARG, "xs, ys must be finite");
+    if (!h->eps) return fail(TSW_ERR_ARG, "eps[batch] is required");
+    std::vector<double> eps(h->eps, h->eps + c->g.batch), amp(size_t(c->g.batch), h->amp);
+    if (h->amp_per_member) amp.assign(h->amp_per_member, h->amp_per_member + c->g.batch);
+    for (int b = 0; b < c->g.batch; ++b) {
+        if (!(eps[b] > 0.0 && eps[b] <= 1.0)) return fail(TSW_ERR_ARG, "eps[%d] = %g outside (0, 1] (P:335)", b, eps[b]);
+        if (!(amp[b] >= 0.0) || !std::isfinite(amp[b])) return fail(TSW_ERR_ARG, "amp[%d] = %g must be >= 0", b, amp[b]);
+    }
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    const int mode = (h->kind == TSW_H_DELTA_POINT) ? MODE_DENSE : MODE_LINE;
+    if ((st = alloc_coeff(c, mode))) return st;
+    CK(cudaMemcpyAsync(c->d_eps, eps.data(), sizeof(double) * eps.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_amp, amp.data(), sizeof(double) * amp.size(), cudaMemcpyHostToDevice, c->stream));
+    CoeffArgs a;
+    a.kind = h->kind;
+    a.order = h->order;
+    a.hb = h->h_background;
+    a.xs = h->xs;
+    a.ys = h->ys;
+    a.dx = c->g.dx;
+    a.dy = c->g.dy;
+    a.eps = c->d_eps;
+    a.amp = c->d_amp;
+    a.nx = c->g.nx;
+    a.ny = c->g.ny;
+    a.r0 = c->r0;
+    a.rows_alloc = c->rows_alloc;
+    a.pitch = c->pitch;
+    a.cpitch = c->cstride1;
+    a.B = c->g.batch;
+    if (mode == MODE_LINE) {
+        dim3 grid(unsigned(grid_for(c->cstride1, 256, 4 * c->sm_count)), unsigned(c->g.batch));
+        k_coeff_line<<<grid, 256, 0, c->stream>>>(a, c->h1, c->h2);
+    } else {
+        dim3 grid(unsigned(grid_for(c->pitch, 256, 64)), unsigned(c->rows_alloc), unsigned(c->g.batch));
+        k_coeff_point<<<grid, 256, 0, c->stream>>>(a, c->h1, c->h2);
+    }
+    CKL();
+    c->launches++;
+    c->kind = h->kind;
+    c->xs = h->xs;
+    c->ys = h->ys;
+    c->have_eps = true;
+    if ((st = check_faces(c))) return st;
+    c->have_coeff = true;
+    c->have_init = false;
+    return TSW_OK;
+}
+
+tsw_status tsw_set_coeff_faces(tsw_ctx* c, const double* h1, const double* h2, int on_device) {
+    if (!c || !h1) return fail(TSW_ERR_ARG, "NULL argument");
+    if (c->g.dim == 2 && !h2) return fail(TSW_ERR_ARG, "h2 is required in 2D");
+    if (!on_device) {
+        // positivity 0 < c0 <= h on every face the stepper can use
+        const size_t n1 = size_t(c->g.batch) * size_t(c->ny_local) * size_t(c->g.nx - 1);
+        for (size_t k = 0; k < n1; ++k)
+            if (!(h1[k] > 0.0) || !std::isfinite(h1[k])) return fail(TSW_ERR_ARG, "h1[%zu] = %g is not > 0", k, h1[k]);
+        if (c->g.dim == 2) {
+            const size_t rows = size_t(c->ny_local) + 1;
+            for (size_t b = 0; b < size_t(c->g.batch); ++b)
+                for (size_t k = 0; k < rows; ++k) {
+                    const int64_t g = c->r0 + int64_t(k) - 1;  // face g + 1/2
+                    if (g < 0 || g > c->g.ny - 2) continue;
+                    for (size_t i = 0; i < size_t(c->g.nx); ++i) {
+                        const double v = h2[(b * rows + k) * size_t(c->g.nx) + i];
+                        if (!(v > 0.0) || !std::isfinite(v)) return fail(TSW_ERR_ARG, "h2 face (%zu, %lld+1/2) = %g is not > 0", i, (long long)g, v);
+                    }
+                }
+        }
+    }
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    const int mode = (c->g.dim == 1) ? MODE_LINE : MODE_DENSE;
+    if ((st = alloc_coeff(c, mode))) return st;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const size_t B = size_t(c->g.batch);
+    const size_t nx = size_t(c->g.nx);
+    if (c->g.dim == 1) {
+        CK(cudaMemcpy2DAsync(c->h1, c->cstride1 * sizeof(double), h1, (nx - 1) * sizeof(double), (nx - 1) * sizeof(double),
+                             B, kind, c->stream));
+        std::vector<double> hb(B, 1.0);
+        CK(cudaMemcpyAsync(c->h2, hb.data(), B * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    } else {
+        CK(cudaMemsetAsync(c->h1, 0, B * c->cstride1 * sizeof(double), c->stream));
+        CK(cudaMemsetAsync(c->h2, 0, B * c->cstride2 * sizeof(double), c->stream));
+        const size_t rows = size_t(c->ny_local);
+        for (size_t b = 0; b < B; ++b) {
+            // h1 local row j → storage row j+1 ; h2 row k (face between global rows r0+k−1 and
+            // r0+k, i.e. storage rows k and k+1) → storage row k+1 (c2 storage row s = face
+            // between storage rows s−1 and s).
+            CK(cudaMemcpy2DAsync(c->h1 + b * c->mstride + c->pitch, c->pitch * sizeof(double),
+                                 h1 + b * rows * (nx - 1), (nx - 1) * sizeof(double), (nx - 1) * sizeof(double), rows, kind,
+                                 c->stream));
+            CK(cudaMemcpy2DAsync(c->h2 + b * c->mstride + c->pitch, c->pitch * sizeof(double), h2 + b * (rows + 1) * nx,
+                                 nx * sizeof(double), nx * sizeof(double), rows + 1, kind, c->stream));
+        }
+    }
+    c->kind = TSW_H_FACES;
+    if ((st = check_faces(c))) return st;
+    c->have_coeff = true;
+    c->have_init = false;
+    return TSW_OK;
+}
+
+tsw_status tsw_read_faces(tsw_ctx* c, double* h1, double* h2) {
+    if (!c || !h1) return fail(TSW_ERR_ARG, "NULL argument");
+    if (!c->have_coeff) return fail(TSW_ERR_STATE, "no coefficients");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    const size_t B = size_t(c->g.batch), nx = size_t(c->g.nx), rows = size_t(c->ny_local);
+    if (c->mode == MODE_LINE) {
+        std::vector<double> line(B * c->cstride1), hy(B);
+        CK(cudaMemcpyAsync(line.data(), c->h1, line.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hy.data(), c->h2, B * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const size_t nrow = (c->g.dim == 1) ? 1 : rows;
+        for (size_t b = 0; b < B; ++b)
+            for (size_t j = 0; j < nrow; ++j)
+                memcpy(h1 + (b * nrow + j) * (nx - 1), line.data() + b * c->cstride1, (nx - 1) * sizeof(double));
+        if (h2 && c->g.dim == 2)
+            for (size_t b = 0; b < B; ++b)
+                for (size_t k = 0; k <= rows; ++k) {
+                    const int64_t g = c->r0 + int64_t(k) - 1;
+                    for (size_t i = 0; i < nx; ++i)
+                        h2[(b * (rows + 1) + k) * nx + i] = (g >= 0 && g <= c->g.ny - 2) ? hy[b] : 0.0;
+                }
+        return TSW_OK;
+    }
+    for (size_t b = 0; b < B; ++b) {
+        CK(cudaMemcpy2DAsync(h1 + b * rows * (nx - 1), (nx - 1) * sizeof(double), c->h1 + b * c->mstride + c->pitch,
+                             c->pitch * sizeof(double), (nx - 1) * sizeof(double), rows, cudaMemcpyDeviceToHost, c->stream));
+        if (h2)
+            CK(cudaMemcpy2DAsync(h2 + b * (rows + 1) * nx, nx * sizeof(double), c->h2 + b * c->mstride + c->pitch,
+                                 c->pitch * sizeof(double), nx * sizeof(double), rows + 1, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    if (h2) {
+        // storage row s = face (g−1)+1/2 between storage rows s−1 and s; layout row k ↔ storage row k+1
+        for (size_t b = 0; b < B; ++b)
+            for (size_t k = 0; k <= rows; ++k) {
+                const int64_t g = c->r0 + int64_t(k) - 1;
+                if (g < 0 || g > c->g.ny - 2)
+                    for (size_t i = 0; i < nx; ++i) h2[(b * (rows + 1) + k) * nx + i] = 0.0;
+            }
+    }
+    return TSW_OK;
+}
+
+tsw_status tsw_set_initial(tsw_ctx* c, const void* u0, const void* u1, double dt, int on_device, uint32_t flags) {
+    if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    return set_levels(c, u0, u1, dt, on_device, flags, 0);
+}
+
+tsw_status tsw_set_state(tsw_ctx* c, const void* un, const void* unm1, int64_t n, double dt, int32_t on_device,
+                         uint32_t flags) {
+    if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    if (n < 1) return fail(TSW_ERR_ARG, "n must be >= 1 for a saved state (u^n, u^{n-1})");
+    if (!unm1) return fail(TSW_ERR_ARG, "unm1 is NULL");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    return set_levels(c, un, unm1, dt, on_device, flags & ~TSW_INIT_SHARED, n);
+}
+
+tsw_status tsw_step(tsw_ctx* c, int64_t nsteps) {
+    if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    if (nsteps < 0) return fail(TSW_ERR_ARG, "nsteps must be >= 0");
+    if (!c->have_init) return fail(TSW_ERR_STATE, "tsw_set_initial / tsw_set_state first");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    return do_steps(c, nsteps);
+}
+
+tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
+    if (!cs || n < 1) return fail(TSW_ERR_ARG, "bad ctx group");
+    for (int r = 0; r < n; ++r) {
+        if (!cs[r] || !cs[r]->have_init) return fail(TSW_ERR_STATE, "group member %d not initialised", r);
+        if (cs[r]->g.dim != 2 || cs[r]->g.nranks != n || cs[r]->g.rank != r)
+            return fail(TSW_ERR_ARG, "group member %d must be rank %d of %d (2D)", r, r, n);
+        if (cs[r]->stream != cs[0]->stream || cs[r]->device != cs[0]->device)
+            return fail(TSW_ERR_ARG, "loopback group members must share one device and stream");
+        if (cs[r]->n != cs[0]->n) return fail(TSW_ERR_STATE, "group members are at different levels");
+    }
+    tsw_status st = set_dev(cs[0]);
+    if (st) return st;
+    if (cs[0]->n == 0) {
+        // initial ghost rows of u^0 (set_initial could not exchange without NCCL)
+        if ((st = exchange_loopback(cs, n))) return st;
+    }
+    for (int64_t s = 0; s < nsteps; ++s) {
+        for (int r = 0; r < n; ++r) {
+            tsw_ctx* c = cs[r];
+            if ((st = launch_step2d(c, c->n == 0, c->s_lo, c->s_hi))) return st;
+            c->cur ^= 1;
+            c->n++;
+        }
+        if ((st = exchange_loopback(cs, n))) return st;
+    }
+    return TSW_OK;
+}
+
+tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
+    if (!c || !out_B) return fail(TSW_ERR_ARG, "NULL argument");
+    if (!c->have_init || c->n < 1) return fail(TSW_ERR_STATE, "energy E^{n-1/2} needs n >= 1");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    EnergyArgs a;
+    a.dim = c->g.dim;
+    a.mode = c->mode;
+    a.unp1 = c->buf[c->cur];
+    a.un = c->buf[c->cur ^ 1];
+    a.c1 = c->c1;
+    a.c2 = c->c2;
+    a.nx = c->g.nx;
+    a.ny = c->g.ny;
+    a.r0 = c->r0;
+    a.pitch = c->pitch;
+    a.mstride = c->mstride;
+    a.cstride1 = c->cstride1;
+    a.cstride2 = c->cstride2;
+    a.ny_local = c->ny_local;
+    const int64_t total = ((c->g.dim == 1) ? 1 : c->ny_local) * c->g.nx;
+    a.nblk = grid_for(total, 256, c->nblk_red);
+    dim3 grid(unsigned(a.nblk), unsigned(c->g.batch));
+    if (is_f64(c))
+        k_energy<double><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+    else
+        k_energy<float><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+    CKL();
+    const double w = ((c->g.dim == 1) ? c->g.dx : c->g.dx * c->g.dy) / (c->dt * c->dt);
+    k_energy_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_partial, a.nblk, w, c->d_out);
+    CKL();
+    c->launches += 2;
+    if (c->g.nranks > 1) {
+        if (!c->comm) return fail(TSW_ERR_STATE, "nranks > 1 but tsw_nccl_init was not called");
+        NK(nccl().AllReduce(c->d_out, c->d_out, size_t(c->g.batch), NCCL_F64, NCCL_SUM, c->comm, c->stream));
+    }
+    CK(cudaMemcpyAsync(out_B, c->d_out, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return TSW_OK;
+}
+
+tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
+    if (!c || !out_B2) return fail(TSW_ERR_ARG, "NULL argument");
+    if (!c->have_init) return fail(TSW_ERR_STATE, "no field");
+    if (!c->have_eps) return fail(TSW_ERR_STATE, "wave2 needs eps/xs from tsw_set_coeff");
+    if (bg < 0 || bg >= c->g.batch) return fail(TSW_ERR_ARG, "bg_member out of range");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    Wave2Args a;
+    a.dim = c->g.dim;
+    a.u = c->buf[c->cur];
+    a.nx = c->g.nx;
+    a.ny = c->g.ny;
+    a.r0 = c->r0;
+    a.pitch = c->pitch;
+    a.mstride = c->mstride;
+    a.ny_local = c->ny_local;
+    a.bg = bg;
+    a.dx = c->g.dx;
+    a.xs = c->xs;
+    a.eps = c->d_eps;
+    const int64_t total = ((c->g.dim == 1) ? 1 : c->ny_local) * c->g.nx;
+    a.nblk = grid_for(total, 256, c->nblk_red);
+    dim3 grid(unsigned(a.nblk), unsigned(c->g.batch));
+    if (is_f64(c))
+        k_wave2<double><<<grid, 256, 0, c->stream>>>(a, c->d_argpart);
+    else
+        k_wave2<float><<<grid, 256, 0, c->stream>>>(a, c->d_argpart);
+    CKL();
+    k_wave2_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_argpart, a.nblk, c->d_out, c->d_idx);
+    CKL();
+    c->launches += 2;
+    const int B = c->g.batch;
+    std::vector<double> v(2 * size_t(B));
+    std::vector<long long> ix(2 * size_t(B));
+    CK(cudaMemcpyAsync(v.data(), c->d_out, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(ix.data(), c->d_idx, sizeof(long long) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->g.nranks > 1) {
+        if (!c->comm) return fail(TSW_ERR_STATE, "nranks > 1 but tsw_nccl_init was not called");
+        // values: empty local regions must not win → ±inf; indices: first global extremum
+        std::vector<double> mx(B), mn(B);
+        for (int b = 0; b < B; ++b) {
+            mx[b] = ix[2 * b] >= 0 ? v[2 * b] : -INFINITY;
+            mn[b] = ix[2 * b + 1] >= 0 ? v[2 * b + 1] : INFINITY;
+        }
+        double* d = c->d_out;
+        CK(cudaMemcpyAsync(d, mx.data(), sizeof(double) * B, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(d + B, mn.data(), sizeof(double) * B, cudaMemcpyHostToDevice, c->stream));
+        NK(nccl().AllReduce(d, d, size_t(B), NCCL_F64, NCCL_MAX, c->comm, c->stream));
+        NK(nccl().AllReduce(d + B, d + B, size_t(B), NCCL_F64, NCCL_MIN, c->comm, c->stream));
+        std::vector<double> gmx(B), gmn(B);
+        CK(cudaMemcpyAsync(gmx.data(), d, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(gmn.data(), d + B, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        std::vector<long long> li(2 * size_t(B));
+        for (int b = 0; b < B; ++b) {
+            li[2 * b] = (ix[2 * b] >= 0 && mx[b] == gmx[b]) ? ix[2 * b] : LLONG_MAX;
+            li[2 * b + 1] = (ix[2 * b + 1] >= 0 && mn[b] == gmn[b]) ? ix[2 * b + 1] : LLONG_MAX;
+        }
+        CK(cudaMemcpyAsync(c->d_idx, li.data(), sizeof(long long) * 2 * B, cudaMemcpyHostToDevice, c->stream));
+        NK(nccl().AllReduce(c->d_idx, c->d_idx, size_t(2 * B), NCCL_INT64, NCCL_MIN, c->comm, c->stream));
+        CK(cudaMemcpyAsync(li.data(), c->d_idx, sizeof(long long) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int b = 0; b < B; ++b) {
+            const bool e1 = li[2 * b] == LLONG_MAX, e2 = li[2 * b + 1] == LLONG_MAX;
+            v[2 * b] = e1 ? 0.0 : gmx[b];
+            v[2 * b + 1] = e2 ? 0.0 : gmn[b];
+            ix[2 * b] = e1 ? -1 : li[2 * b];
+            ix[2 * b + 1] = e2 ? -1 : li[2 * b + 1];
+        }
+    }
+    for (int k = 0; k < 2 * B; ++k) {
+        out_B2[k] = v[k];
+        if (idx_B2) idx_B2[k] = ix[k];
+    }
+    return TSW_OK;
+}
+
+tsw_status tsw_read(tsw_ctx* c, int32_t which, void* dst, int32_t to_device) {
+    if (!c || !dst) return fail(TSW_ERR_ARG, "NULL argument");
+    if (which != 0 && which != 1) return fail(TSW_ERR_ARG, "which must be 0 (u^n) or 1 (u^{n-1})");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    const void* src = c->buf[c->cur ^ which];
+    const cudaMemcpyKind kind = to_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const size_t w = size_t(c->g.nx) * c->esz;
+    const size_t rows = size_t(c->ny_local);
+    for (int b = 0; b < c->g.batch; ++b) {
+        const char* s = static_cast<const char*>(src) + size_t(b) * c->mstride * c->esz +
+                        (c->g.dim == 2 ? size_t(c->pitch) * c->esz : 0);
+        char* d = static_cast<char*>(dst) + size_t(b) * rows * w;
+        CK(cudaMemcpy2DAsync(d, w, s, size_t(c->pitch) * c->esz, w, rows, kind, c->stream));
+    }
+    if (!to_device) CK(cudaStreamSynchronize(c->stream));
+    return TSW_OK;
+}
+
+tsw_status tsw_info(tsw_ctx* c, int64_t* n, double* t, double* dt_max) {
+    if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    if (n) *n = c->n;
+    if (t) *t = double(c->n) * c->dt;
+    if (dt_max) *dt_max = c->have_coeff ? c->dt_max : 0.0;
+    return TSW_OK;
+}
+
+tsw_status tsw_sync(tsw_ctx* c) {
+    if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    return TSW_OK;
+}
+
+int64_t tsw_launch_count(const tsw_ctx* c) { return c ? c->launches : 0; }
+
+tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
+    if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    if (key == TSW_OPT_ROWS_PER_ITEM) {
+        if (value < 0 || value > (1 << 30)) return fail(TSW_ERR_ARG, "rows per item must be >= 0");
+        c->rows_per_item_opt = int(value);
+        return TSW_OK;
+    }
+    return fail(TSW_ERR_ARG, "unknown option %d", key);
+}
+
+tsw_status tsw_nccl_unique_id(void* out) {
+    if (!out) return fail(TSW_ERR_ARG, "NULL argument");
+    Nccl& N = nccl();
+    if (!N.ok) return fail(TSW_ERR_NCCL, "libnccl.so.2 not found or incomplete");
+    NcclId id;
+    NK(N.GetUniqueId(&id));
+    memcpy(out, &id, sizeof(id));
+    return TSW_OK;
+}
+
+tsw_status tsw_nccl_init(tsw_ctx* c, const void* uid) {
+    if (!c || !uid) return fail(TSW_ERR_ARG, "NULL argument");
+    Nccl& N = nccl();
+    if (!N.ok) return fail(TSW_ERR_NCCL, "libnccl.so.2 not found or incomplete");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    if (c->comm) return fail(TSW_ERR_STATE, "NCCL communicator already initialised");
+    NcclId id;
+    memcpy(&id, uid, sizeof(id));
+    void* comm = nullptr;
+    NK(N.CommInitRank(&comm, c->g.nranks, id, c->g.rank));
+    c->comm = comm;
+    return TSW_OK;
+}
+
+}  // extern "C"
