@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark of the leapfrog hot path (BASELINE.json metric: 2D stencil Gpoint-updates/s and HBM
+GB/s vs the B200 peak, at 1/2/4/8 GPUs).
+
+Workload: config 4's weak-scaling unit (R22) — a 32768 × 4096-row δ-line slab per
+GPU (global grid 32768 × 4096·N, dx = dy = 0.0025, ε = 0.05, dt = 4e−4), dense uniform [−1, 1]
+data (SURVEY §8(d) data-independence guard), fp64 by default.  One "step" = one pass of the
+hot path over the slab: the leapfrog stencil (S3), the NCCL ghost-row exchange at N > 1 (S4),
+and the discrete-energy reduction every `--energy-every` steps (S5).  Inputs (2 × 1.07 GB per
+GPU in fp64) exceed the 126 MB L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f64|f32] [--impl tsw|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2D stencil Gpoint-updates/s & HBM GB/s vs 8 TB/s peak, at 1/2/4/8 B200"
+UNIT = "Gpt/s"
+ESZ = {"f64": 8, "f32": 4}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(dtype: str, workload: str):
+    """dram bytes per stencil launch from the committed ncu --set full summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(dtype)
+        if e and e.get("workload") == workload:
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled in the background (the recipe's clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.samples = []
+        self.proc = None
+        self.t0 = self.t1 = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        win = [s for t, s in self.samples if self.t0 is not None and self.t0 - 0.06 <= t <= (self.t1 or t) + 0.06]
+        if not win and self.samples:
+            # the timed region was shorter than the sampling period: nearest sample
+            mid = 0.5 * ((self.t0 or 0) + (self.t1 or 0))
+            win = [min(self.samples, key=lambda ts: abs(ts[0] - mid))[1]]
+        sm = [float(s[0]) for s in win if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in win if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in win for k in range(4) if len(s) > 4 + k and s[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(win)}
+
+
+def cpu_baseline(cfg, dtype: str, budget_s: float = 15.0, rows: int = 1024):
+    """The oracle as it stands, on this host's cores, over a bounded sample of the same workload:
+    `rows` interior rows × the full 32768-wide row, dense data, the same δ-line faces."""
+    import oracle
+    threads = host_cores()
+    oracle.set_threads(threads)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    j0 = cfg.ny // 2 - rows // 2
+    wny = rows + 2
+    _, _, c1, c2 = oracle.member_coefficients(cfg, 0, npdt, 0, j0, cfg.nx, wny)
+    from paper_2005_11931_b200 import inputs
+    u = inputs.uniform_dense_rows(cfg.nx, cfg.ny, j0, wny).astype(npdt)
+    v = oracle.startup(2, c1, c2, u, None, cfg.dt)
+    t = time.perf_counter()
+    v, u = oracle.leapfrog(2, c1, c2, v, u, 2)
+    t_step = max((time.perf_counter() - t) / 2, 1e-6)
+    steps = int(min(2000, max(2, budget_s / t_step)))
+    t = time.perf_counter()
+    oracle.leapfrog(2, c1, c2, v, u, steps)
+    el = time.perf_counter() - t
+    upd = rows * (cfg.nx - 2) * steps
+    return {"value": upd / el / 1e9, "unit": UNIT, "cores": int(oracle.max_threads()), "kind": "oracle",
+            "sample": f"{rows} rows x {cfg.nx} cols of the per-GPU slab, {steps} leapfrog steps, {dtype}, "
+                      f"OpenMP over rows, {el:.1f} s"}
+
+
+def run_reference(args, cfg, rank: int, world: int):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores, rank 0 only."""
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2005_11931_b200 import inputs
+    threads = host_cores()
+    oracle.set_threads(threads)
+    npdt = np.float64 if args.dtype == "f64" else np.float32
+    rows = args.ref_rows
+    j0 = cfg.ny // 2 - rows // 2
+    _, _, c1, c2 = oracle.member_coefficients(cfg, 0, npdt, 0, j0, cfg.nx, rows + 2)
+    u = inputs.uniform_dense_rows(cfg.nx, cfg.ny, j0, rows + 2).astype(npdt)
+    v = oracle.startup(2, c1, c2, u, None, cfg.dt)
+    if args.warmup:
+        v, u = oracle.leapfrog(2, c1, c2, v, u, args.warmup)
+    t = time.perf_counter()
+    oracle.leapfrog(2, c1, c2, v, u, args.steps)
+    el = time.perf_counter() - t
+    upd = rows * (cfg.nx - 2) * args.steps
+    val = upd / el / 1e9
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "impl": "reference",
+            "data": "synthetic (dense uniform[-1,1], seed 0)",
+            "config": {"workload": workload_name(cfg, world), "sample_rows": rows, "nx": cfg.nx},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": int(oracle.max_threads()), "kind": "oracle",
+                             "sample": f"{rows} rows x {cfg.nx} cols per step of the per-GPU slab"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_name(cfg, world: int) -> str:
+    return f"config4_weak_unit_delta_line_{cfg.nx}x{cfg.ny // world}_per_gpu"
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
+    ap.add_argument("--impl", choices=["tsw", "reference"], default="tsw")
+    ap.add_argument("--rows-per-gpu", type=int, default=4096)
+    ap.add_argument("--nx", type=int, default=32768)
+    ap.add_argument("--energy-every", type=int, default=100)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-also", action="store_true", help="skip the second-precision line item")
+    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--rows-per-item", type=int, default=0)
+    args = ap.parse_args()
+
+    from paper_2005_11931_b200 import inputs, parallel
+    rank, world, local = parallel.env_rank()
+    cfg = inputs.weak_unit(world, rows_per_rank=args.rows_per_gpu, nx=args.nx)
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2005_11931_b200 import tsw
+    torch.cuda.set_device(local)
+    if world > 1:
+        parallel.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+
+    def run(dtype: str, full: bool):
+        npdt = np.float64 if dtype == "f64" else np.float32
+        stream = torch.cuda.Stream(device=dev)
+        s = tsw.Solver.from_config(cfg, dtype, rank=rank, nranks=world, device=local, stream=stream.cuda_stream)
+        if args.rows_per_item:
+            s.set_option(tsw.TSW_OPT_ROWS_PER_ITEM, args.rows_per_item)
+        parallel.nccl_bootstrap(s)
+        r0, r1 = parallel.slab(cfg.ny, rank, world)
+        u0_host = torch.from_numpy(inputs.uniform_dense_rows(cfg.nx, cfg.ny, r0, r1 - r0).astype(npdt)).pin_memory()
+        u0_dev = u0_host.to(dev)
+        torch.cuda.synchronize()
+        s.set_initial(u0_dev, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+        # untimed spin-up (clocks ramp) then the W warm-up steps
+        s.step(max(50, 3 * args.warmup))
+        s.step(args.warmup)
+        s.energy()
+        clocks = ClockSampler(local) if full else None
+        if clocks:
+            time.sleep(0.2)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.set_option(tsw.TSW_OPT_TIME_KERNELS, 1)
+        l0 = s.launches()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.mark(True)
+        ev0.record(stream)
+        done = 0
+        while done < args.steps:
+            k = min(args.energy_every, args.steps - done) if args.energy_every > 0 else args.steps - done
+            s.step(k)
+            done += k
+            if args.energy_every > 0 and done % args.energy_every == 0:
+                s.energy()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.mark(False)
+        if world > 1:
+            dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+        launches = s.launches() - l0
+        kms, klaunch, kupd = s.kernel_stats()
+        s.set_option(tsw.TSW_OPT_TIME_KERNELS, 0)
+        if world > 1:
+            t = torch.tensor([ms, kms / max(klaunch, 1)], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, kavg = float(t[0]), float(t[1])
+        else:
+            kavg = kms / max(klaunch, 1)
+        updates = (cfg.nx - 2) * (cfg.ny - 2) * args.steps
+        res = {"ms": ms, "value": updates / (ms * 1e-3) / 1e9, "launches": launches, "kernel_avg_ms": kavg,
+               "kernel_updates_per_launch": kupd / max(klaunch, 1), "clocks": clocks.stop() if clocks else None}
+        if full and not args.no_e2e:
+            # e2e through the public API with host buffers: H2D of u0 (pinned), K steps (+ energy),
+            # D2H of u^K — all inside the timed region.
+            out_host = torch.empty_like(u0_host).pin_memory()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s.set_initial(u0_host.numpy(), None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+            done = 0
+            while done < args.steps:
+                k = min(args.energy_every, args.steps - done) if args.energy_every > 0 else args.steps - done
+                s.step(k)
+                done += k
+                if args.energy_every > 0 and done % args.energy_every == 0:
+                    s.energy()
+            s.read(0, out_host.numpy().reshape(1, r1 - r0, cfg.nx))
+            el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t[0])
+            nb = u0_host.numel() * u0_host.element_size()
+            res["e2e"] = {"value": updates / el / 1e9, "unit": UNIT, "h2d_bytes_per_step": nb / args.steps,
+                          "d2h_bytes_per_step": nb / args.steps}
+        s.close()
+        del u0_dev
+        torch.cuda.empty_cache()
+        return res
+
+    main_res = run(args.dtype, True)
+    other = "f32" if args.dtype == "f64" else "f64"
+    also = None if args.no_also else run(other, False)
+
+    if rank == 0:
+        peak, peak_src = measured_peak()
+        esz = ESZ[args.dtype]
+        achieved = main_res["kernel_updates_per_launch"] * 3 * esz / (main_res["kernel_avg_ms"] * 1e-3) / 1e9
+        wl = workload_name(cfg, world)
+        traffic = ncu_traffic(args.dtype, wl)
+        line = {
+            "metric": METRIC, "value": main_res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main_res["ms"] / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (dense uniform[-1,1] u0, u1 = 0, seed 0; delta-line h_eps, eps = 0.05)",
+            "config": {"workload": wl, "nx": cfg.nx, "ny_global": cfg.ny, "rows_per_gpu": cfg.ny // world,
+                       "dx": cfg.dx, "dt": cfg.dt, "eps": cfg.eps[0], "energy_every": args.energy_every,
+                       "parallelism": f"row-slab x{world} (NCCL ghost rows)" if world > 1 else "single GPU",
+                       "l2": "inputs exceed L2 (2 levels x %.2f GB per GPU), no flush" %
+                             ((cfg.nx * (cfg.ny // world) * esz) / 1e9)},
+            "hbm_gbs_effective": main_res["value"] * 3 * esz,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_step2d (S3 leapfrog stencil)",
+                         "algorithmic_bytes_per_update": 3 * esz, "peak_source": peak_src,
+                         "kernel_avg_ms": main_res["kernel_avg_ms"]},
+            "gpu_launches": main_res["launches"],
+            "clocks": main_res["clocks"],
+        }
+        if "e2e" in main_res:
+            line["e2e"] = main_res["e2e"]
+        if also:
+            e2 = ESZ[other]
+            ach2 = also["kernel_updates_per_launch"] * 3 * e2 / (also["kernel_avg_ms"] * 1e-3) / 1e9
+            line["also"] = {"dtype": other, "value": also["value"], "unit": UNIT,
+                            "ms_per_step": also["ms"] / args.steps, "hbm_gbs_effective": also["value"] * 3 * e2,
+                            "roofline_frac": ach2 / peak, "achieved_gbs": ach2}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, args.dtype)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

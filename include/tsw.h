@@ -157,9 +157,17 @@ tsw_status tsw_sync(tsw_ctx* ctx);
 /* Number of kernels this ctx has launched so far (the bench's gpu_launches evidence). */
 int64_t tsw_launch_count(const tsw_ctx* ctx);
 
-/* Tuning knob: TSW_OPT_ROWS_PER_ITEM (rows per warp work item of the 2D stencil, ≥ 1; 0 = auto). */
+/* Options: TSW_OPT_ROWS_PER_ITEM — rows per warp work item of the 2D stencil (≥ 1; 0 = auto);
+ *          TSW_OPT_TIME_KERNELS — 1: bracket every stencil launch with CUDA events on the ctx
+ *          stream (for tsw_kernel_stats), 0: off; setting it resets the statistics. */
 #define TSW_OPT_ROWS_PER_ITEM 1
+#define TSW_OPT_TIME_KERNELS 2
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
+
+/* Live per-kernel timing of the stencil (S2/S3) launches recorded since TSW_OPT_TIME_KERNELS was
+ * set: total device milliseconds, number of launches, and interior point-updates they performed.
+ * Synchronises.  Any pointer may be NULL. */
+tsw_status tsw_kernel_stats(tsw_ctx* ctx, double* total_ms, int64_t* launches, int64_t* updates);
 
 /* NCCL row-slab plumbing.  tsw_nccl_unique_id writes a 128-byte ncclUniqueId
  * (call on rank 0, broadcast it, e.g. with torch.distributed); tsw_nccl_init creates the ctx's

@@ -144,6 +144,11 @@ struct tsw_ctx {
     int64_t launches = 0;
     int rows_per_item_opt = 0;
     int step_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};  // [mode][start]
+    // live kernel timing (TSW_OPT_TIME_KERNELS)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    int64_t timed_launches = 0, timed_updates = 0;
     // NCCL
     void* comm = nullptr;
 };
@@ -162,6 +167,19 @@ int grid_for(int64_t n, int threads, int cap) {
     if (b < 1) b = 1;
     if (b > cap) b = cap;
     return int(b);
+}
+
+// ---- live kernel timing ----------------------------------------------------------------------
+tsw_status timing_events(tsw_ctx* c, cudaEvent_t* e0, cudaEvent_t* e1) {
+    while (c->ev_pool.size() < c->ev_used + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->ev_pool.push_back(e);
+    }
+    *e0 = c->ev_pool[c->ev_used];
+    *e1 = c->ev_pool[c->ev_used + 1];
+    c->ev_used += 2;
+    return TSW_OK;
 }
 
 // ---- 2D stencil launch ---------------------------------------------------------------------
@@ -203,8 +221,19 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
     a.items = a.strips * a.chunks * c->g.batch;
     int64_t blocks = (a.items + 7) / 8;
     blocks = std::min<int64_t>(blocks, int64_t(occ) * c->sm_count);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        tsw_status st = timing_events(c, &e0, &e1);
+        if (st) return st;
+        CK(cudaEventRecord(e0, c->stream));
+    }
     k_step2d<T, MODE, START><<<unsigned(blocks), 256, 0, c->stream>>>(a);
     CKL();
+    if (c->timing) {
+        CK(cudaEventRecord(e1, c->stream));
+        c->timed_launches++;
+        c->timed_updates += rows * (c->g.nx - 2) * c->g.batch;
+    }
     c->launches++;
     return TSW_OK;
 }
@@ -235,9 +264,20 @@ tsw_status step1d_t(tsw_ctx* c, int64_t k) {
     if (smem <= 200 * 1024) {
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_step1d_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int threads = int(std::min<int64_t>(1024, round_up(c->g.nx, 32)));
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (c->timing) {
+            tsw_status st = timing_events(c, &e0, &e1);
+            if (st) return st;
+            CK(cudaEventRecord(e0, c->stream));
+        }
         k_step1d_smem<T><<<c->g.batch, threads, smem, c->stream>>>(u, p, c1, c->g.nx, c->pitch, c->cstride1, k,
                                                                    start ? 1 : 0, (T)c->dt);
         CKL();
+        if (c->timing) {
+            CK(cudaEventRecord(e1, c->stream));
+            c->timed_launches++;
+            c->timed_updates += k * (c->g.nx - 2) * c->g.batch;
+        }
         c->launches++;
         c->n += k;  // the kernel writes the newest level back into buf[cur]
         return TSW_OK;
@@ -571,6 +611,7 @@ void tsw_destroy(tsw_ctx* c) {
                     c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -952,7 +993,31 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         c->rows_per_item_opt = int(value);
         return TSW_OK;
     }
+    if (key == TSW_OPT_TIME_KERNELS) {
+        c->timing = value != 0;
+        c->ev_used = 0;
+        c->timed_launches = 0;
+        c->timed_updates = 0;
+        return TSW_OK;
+    }
     return fail(TSW_ERR_ARG, "unknown option %d", key);
+}
+
+tsw_status tsw_kernel_stats(tsw_ctx* c, double* total_ms, int64_t* launches, int64_t* updates) {
+    if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    double ms = 0.0;
+    for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+        float m = 0.f;
+        CK(cudaEventElapsedTime(&m, c->ev_pool[k], c->ev_pool[k + 1]));
+        ms += m;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = c->timed_launches;
+    if (updates) *updates = c->timed_updates;
+    return TSW_OK;
 }
 
 tsw_status tsw_nccl_unique_id(void* out) {

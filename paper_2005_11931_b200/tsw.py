@@ -24,6 +24,7 @@ TSW_H_CONST, TSW_H_DELTA_LINE_X, TSW_H_DELTA_POINT, TSW_H_FACES = range(4)
 TSW_ALLOW_UNSTABLE = 1
 TSW_INIT_SHARED = 2
 TSW_OPT_ROWS_PER_ITEM = 1
+TSW_OPT_TIME_KERNELS = 2
 
 STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STATE", 4: "TSW_ERR_CUDA",
                 5: "TSW_ERR_NCCL", 6: "TSW_ERR_OOM", 7: "TSW_ERR_UNSTABLE"}
@@ -31,7 +32,7 @@ STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STA
 # every symbol include/tsw.h declares (tests check the library exports all of them)
 EXPORTS = ["tsw_create", "tsw_destroy", "tsw_set_coeff", "tsw_set_coeff_faces", "tsw_read_faces", "tsw_set_initial", "tsw_step",
            "tsw_group_step", "tsw_energy", "tsw_wave2", "tsw_read", "tsw_set_state", "tsw_info", "tsw_sync",
-           "tsw_launch_count", "tsw_set_option", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
+           "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
            "tsw_version"]
 
 
@@ -85,6 +86,7 @@ def load(path: Optional[str] = None):
         "tsw_sync": (i32, [vp]),
         "tsw_launch_count": (i64, [vp]),
         "tsw_set_option": (i32, [vp, i32, i64]),
+        "tsw_kernel_stats": (i32, [vp, ctypes.POINTER(d), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "tsw_nccl_unique_id": (i32, [vp]),
         "tsw_nccl_init": (i32, [vp, vp]),
         "tsw_last_error": (ctypes.c_char_p, [vp]),
@@ -234,6 +236,13 @@ def tsw_set_option(ctx, key: int, value: int) -> None:
     _check(load().tsw_set_option(ctx, key, value), ctx)
 
 
+def tsw_kernel_stats(ctx) -> Tuple[float, int, int]:
+    """(total stencil-kernel ms, launches, point-updates) since TSW_OPT_TIME_KERNELS was set."""
+    ms, n, u = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+    _check(load().tsw_kernel_stats(ctx, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(u)), ctx)
+    return ms.value, n.value, u.value
+
+
 def tsw_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load().tsw_nccl_unique_id(buf))
@@ -333,3 +342,6 @@ class Solver:
 
     def set_option(self, key: int, value: int):
         tsw_set_option(self.ctx, key, value)
+
+    def kernel_stats(self):
+        return tsw_kernel_stats(self.ctx)
