@@ -128,13 +128,15 @@ tsw_status tsw_group_step(tsw_ctx** ctxs, int32_t n, int64_t nsteps);
 
 /* S5 discrete energy E^{n−1/2} of the current levels (R17; discrete form of CL-01):
  *   E = (dx·dy/dt²)·[Σ_interior (u^n − u^{n−1})² + Σ_faces c·(Δu^n)(Δu^{n−1})]   (1D: dx/dt²)
- * accumulated in fp64 with the stepper's own rounded c; summed over ranks (NCCL) when nranks > 1.
+ * accumulated in fp64 with the stepper's own rounded c; summed over ranks (NCCL) when nranks > 1
+ * and tsw_nccl_init was called (a loopback-group member returns its slab's share).
  *   out_B: host double[batch].  Errors: TSW_ERR_STATE if n < 1. */
 tsw_status tsw_energy(tsw_ctx* ctx, double* out_B);
 
 /* S6 second-wave amplitude (R18; §3.2.3, qualitative): for every member b
  *   A₂⁺ = max, A₂⁻ = min over nodes with x_i ≤ xs − ε_b of fl_T(u_b − u_{bg_member})
  * with the global row-major index (g·nx + i) of the first extremum; empty region ⇒ 0 and −1.
+ * Reduced over ranks with NCCL when a communicator exists (else this slab's extrema).
  *   out_B2: host double[batch][2]; argidx_B2: host int64[batch][2] (may be NULL). */
 tsw_status tsw_wave2(tsw_ctx* ctx, int32_t bg_member, double* out_B2, int64_t* argidx_B2);
 
@@ -158,10 +160,13 @@ tsw_status tsw_sync(tsw_ctx* ctx);
 int64_t tsw_launch_count(const tsw_ctx* ctx);
 
 /* Options: TSW_OPT_ROWS_PER_ITEM — rows per warp work item of the 2D stencil (≥ 1; 0 = auto);
+ *          TSW_OPT_KERNEL / TSW_OPT_DEPTH — stencil variant and its ring depth;
  *          TSW_OPT_TIME_KERNELS — 1: bracket every stencil launch with CUDA events on the ctx
  *          stream (for tsw_kernel_stats), 0: off; setting it resets the statistics. */
 #define TSW_OPT_ROWS_PER_ITEM 1
 #define TSW_OPT_TIME_KERNELS 2
+#define TSW_OPT_KERNEL 3 /* 0: CTA-wide TMA bulk-copy row pipeline (default); 1: register-prefetch kernel */
+#define TSW_OPT_DEPTH 4  /* TMA ring stages per CTA, 2..32 (default 4) */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
 
 /* Live per-kernel timing of the stencil (S2/S3) launches recorded since TSW_OPT_TIME_KERNELS was

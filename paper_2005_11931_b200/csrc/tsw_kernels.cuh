@@ -221,6 +221,237 @@ __global__ void __launch_bounds__(256) k_step2d(const StepArgs<T> a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// S2/S3: 2D stencil, CTA-wide TMA bulk-copy row pipeline (the production kernel on sm_100a)
+// ------------------------------------------------------------------------------------------
+// Same per-node arithmetic as k_step2d.  A CTA owns a strip of WC = NC·32·V columns (4 KB of a
+// row in either precision) and marches down a chunk of rows.  A dedicated producer warp streams
+// rows into a ring of D shared-memory stages with cp.async.bulk (TMA 1D bulk copies, SASS UBLKCP;
+// one ≈4 KB request per row and field, so the TMA request rate is no limit), completing each
+// stage on a "full" mbarrier (expect_tx bytes); the NC consumer warps arrive on an "empty"
+// mbarrier when a stage can be refilled.  The vertical window u^n[s−1], u^n[s], u^n[s+1] lives
+// in registers; horizontal neighbours come from the centre row's stage (16-byte halo on each
+// side, so every thread reads its left/right neighbour the same way).
+//
+// The CTA walks a STREAM of stages over its items (strip, row chunk, member); item rows [s0, s1)
+// are the stages t = 0 .. (s1 − s0) + 1 and
+//   stage t loads u^n row r = s0 − 1 + t (+ halos)            (DENSE: + c2 row r when t ≥ 1)
+//            and, when t ≥ 2, u^{n−1} row r − 1               (DENSE: + c1 row r − 1 + halos)
+//   and emits output row r − 1.  The producer runs up to D stages ahead, across items.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+constexpr int TMA_NC = 8;  // consumer warps per CTA (+1 producer warp)
+
+template <typename T>
+struct TmaGeom {
+    static constexpr int V = Vec16<T>::N;      // elements per thread
+    static constexpr int H = 16 / sizeof(T);   // halo elements (16 bytes) on each side
+    static constexpr int WC = TMA_NC * 32 * V; // strip width in elements (4 KB)
+    static constexpr int WH = WC + 2 * H;      // strip + halos
+};
+
+template <typename T, int MODE>
+__host__ __device__ constexpr int tma_slot_bytes() {
+    return int(sizeof(T)) * (TmaGeom<T>::WH + TmaGeom<T>::WC + (MODE == MODE_DENSE ? TmaGeom<T>::WH + TmaGeom<T>::WC : 0));
+}
+
+template <typename T>
+__device__ __forceinline__ void lds_vec(const T* p, T (&v)[Vec16<T>::N]) {
+    using VT = typename Vec16<T>::type;
+    VT x = *reinterpret_cast<const VT*>(p);
+    const T* e = reinterpret_cast<const T*>(&x);
+#pragma unroll
+    for (int k = 0; k < Vec16<T>::N; ++k) v[k] = e[k];
+}
+
+// a.strips counts WC-wide strips for this kernel
+template <typename T, int MODE, bool START>
+__global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs<T> a, int depth) {
+    using G = TmaGeom<T>;
+    constexpr int V = G::V, H = G::H, WC = G::WC, WH = G::WH;
+    constexpr int SLOT = tma_slot_bytes<T, MODE>();
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(depth) * SLOT);
+    uint64_t* empty = full + depth;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < depth; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], TMA_NC);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    auto item_geom = [&](int64_t item, int64_t& cs, int& s0, int& s1, int& b) {
+        const int64_t strip = item % a.strips;
+        const int64_t rest = item / a.strips;
+        const int chunk = int(rest % a.chunks);
+        b = int(rest / a.chunks);
+        cs = strip * WC;
+        s0 = a.s_lo + chunk * a.rows_per_item;
+        s1 = min(s0 + a.rows_per_item, a.s_hi);
+    };
+
+    if (warp == TMA_NC) {
+        // ------------------------------ producer warp ------------------------------
+        if (lane != 0) return;
+        int64_t it = 0;
+        for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+            int64_t cs;
+            int s0, s1, b;
+            item_geom(item, cs, s0, s1, b);
+            const int L = s1 - s0 + 2;
+            const T* ub = a.ucur + b * a.mstride;
+            const T* pb = a.uprev + b * a.mstride;
+            for (int t = 0; t < L; ++t, ++it) {
+                const int slot = int(it % depth);
+                if (it >= depth) mbar_wait(&empty[slot], uint32_t(((it / depth) - 1) & 1));
+                T* un_s = reinterpret_cast<T*>(smem + size_t(slot) * SLOT);
+                T* pv_s = un_s + WH;
+                T* c1_s = pv_s + WC;
+                T* c2_s = c1_s + WH;
+                const int r = s0 - 1 + t;
+                uint32_t bytes = WH * sizeof(T);
+                if (t >= 2) bytes += WC * sizeof(T);
+                if (MODE == MODE_DENSE) {
+                    if (t >= 1) bytes += WC * sizeof(T);
+                    if (t >= 2) bytes += WH * sizeof(T);
+                }
+                mbar_arrive_expect_tx(&full[slot], bytes);
+                bulk_g2s(un_s, ub + r * a.pitch + cs - H, WH * sizeof(T), &full[slot]);
+                if (t >= 2) bulk_g2s(pv_s, pb + (r - 1) * a.pitch + cs, WC * sizeof(T), &full[slot]);
+                if (MODE == MODE_DENSE) {
+                    if (t >= 2)
+                        bulk_g2s(c1_s, a.c1 + b * a.cstride1 + (r - 1) * a.pitch + cs - H, WH * sizeof(T), &full[slot]);
+                    if (t >= 1) bulk_g2s(c2_s, a.c2 + b * a.cstride2 + r * a.pitch + cs, WC * sizeof(T), &full[slot]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------ consumer warps ------------------------------
+    const int tid = threadIdx.x;  // 0 .. NC·32 − 1
+    int64_t it = 0;
+    for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+        int64_t cs;
+        int s0, s1, b;
+        item_geom(item, cs, s0, s1, b);
+        const int64_t col = cs + int64_t(tid) * V;
+        T* __restrict__ pb = a.uprev + b * a.mstride;
+        bool interior[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) interior[k] = (col + k >= 1) && (col + k <= a.nx - 2);
+        T c1r[V], c1l[V];
+        T c2s = (T)0;
+        if (MODE == MODE_LINE) {
+            const T* c1b = a.c1 + b * a.cstride1;
+            vload(c1b + col, c1r);
+            c1l[0] = (col > 0) ? __ldg(c1b + col - 1) : (T)0;
+#pragma unroll
+            for (int k = 1; k < V; ++k) c1l[k] = c1r[k - 1];
+            c2s = a.c2[b];
+        }
+        T up[V], cu[V], dn[V], pv[V], c2lo[V], c2hi[V];
+        const int L = s1 - s0 + 2;
+        int prev_slot = 0;
+        for (int t = 0; t < L; ++t, ++it) {
+            const int slot = int(it % depth);
+            mbar_wait(&full[slot], uint32_t((it / depth) & 1));
+            const T* un_s = reinterpret_cast<const T*>(smem + size_t(slot) * SLOT);
+            const T* pv_s = un_s + WH;
+            const T* c1_s = pv_s + WC;
+            const T* c2_s = c1_s + WH;
+            if (t == 0) {
+                lds_vec(un_s + H + tid * V, up);
+            } else if (t == 1) {
+                lds_vec(un_s + H + tid * V, cu);
+                if (MODE == MODE_DENSE) lds_vec(c2_s + tid * V, c2lo);
+            } else {
+                lds_vec(un_s + H + tid * V, dn);
+                lds_vec(pv_s + tid * V, pv);
+                T c1d_r[V], c1d_l[V];
+                if (MODE == MODE_DENSE) {
+                    lds_vec(c2_s + tid * V, c2hi);
+                    lds_vec(c1_s + H + tid * V, c1d_r);
+                    c1d_l[0] = c1_s[H + tid * V - 1];
+#pragma unroll
+                    for (int k = 1; k < V; ++k) c1d_l[k] = c1d_r[k - 1];
+                }
+                // horizontal neighbours of the centre row (loaded at the previous stage)
+                const T* ce = reinterpret_cast<const T*>(smem + size_t(prev_slot) * SLOT);
+                const T left = ce[H + tid * V - 1];
+                const T right = ce[H + tid * V + V];
+                T out[V];
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    T ul = (k == 0) ? left : cu[k - 1];
+                    T ur = (k == V - 1) ? right : cu[k + 1];
+                    T l1 = (MODE == MODE_LINE) ? c1l[k] : c1d_l[k];
+                    T r1 = (MODE == MODE_LINE) ? c1r[k] : c1d_r[k];
+                    T d2 = (MODE == MODE_LINE) ? c2s : c2lo[k];
+                    T u2 = (MODE == MODE_LINE) ? c2s : c2hi[k];
+                    T v = node_update<T, START, true>(cu[k], ul, ur, up[k], dn[k], pv[k], l1, r1, d2, u2, a.dtT);
+                    out[k] = interior[k] ? v : (T)0;
+                }
+                const int s = s0 + t - 2;
+                if (col < a.pitch) vstore(pb + s * a.pitch + col, out);  // ragged last strip
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    up[k] = cu[k];
+                    cu[k] = dn[k];
+                    if (MODE == MODE_DENSE) c2lo[k] = c2hi[k];
+                }
+            }
+            // release the previous stage (its rows are in registers / consumed above); the last
+            // stage of an item releases itself too.
+            __syncwarp();
+            if (lane == 0) {
+                if (t >= 1) mbar_arrive(&empty[prev_slot]);
+                if (t == L - 1) mbar_arrive(&empty[slot]);
+            }
+            prev_slot = slot;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // S2/S3: 1D, persistent — one CTA per member, both levels resident in shared memory, all
 // steps in one launch (config 1: 2000 fp64 nodes × 3 arrays = 48 KB).
 // ------------------------------------------------------------------------------------------

@@ -99,6 +99,23 @@ Nccl& nccl() {
 
 int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
 
+// Field and coefficient arrays carry a 16 KB guard before and after: the TMA stencil reads each
+// 4 KB strip with a 16-byte halo on both sides, and the last strip of a row may run past the
+// row's padding; for the first/last row of the array those bytes lie outside it (their values
+// are never used and never written).
+constexpr size_t GUARD = 16384;
+cudaError_t dmalloc_guarded(void** p, size_t bytes) {
+    void* raw = nullptr;
+    cudaError_t e = cudaMalloc(&raw, bytes + 2 * GUARD);
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(raw, 0, bytes + 2 * GUARD);
+    *p = static_cast<char*>(raw) + GUARD;
+    return e;
+}
+void dfree_guarded(void* p) {
+    if (p) cudaFree(static_cast<char*>(p) - GUARD);
+}
+
 }  // namespace
 
 struct tsw_ctx {
@@ -131,6 +148,7 @@ struct tsw_ctx {
     double dt_max = 0.0;
     // state
     bool have_init = false;
+    bool ghosts_valid = false;  // ghost rows of u^n hold the neighbours' rows
     int64_t n = 0;
     double dt = 0.0;
     // scratch
@@ -143,6 +161,10 @@ struct tsw_ctx {
     // launch bookkeeping
     int64_t launches = 0;
     int rows_per_item_opt = 0;
+    int kernel_opt = 0;   // 0: CTA-wide TMA bulk-copy pipeline (default), 1: register-prefetch kernel
+    int depth_opt = 4;    // TMA ring stages per CTA (sweep: 4 best at 32768-wide rows)
+    int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
+    int bulk_occ_key[2][2] = {{0, 0}, {0, 0}};
     int step_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};  // [mode][start]
     // live kernel timing (TSW_OPT_TIME_KERNELS)
     bool timing = false;
@@ -205,29 +227,61 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d<T, MODE, START>, 256, 0));
         if (occ < 1) occ = 1;
     }
-    const int64_t resident_warps = int64_t(occ) * c->sm_count * 8;
     const int64_t rows = s_hi - s_lo;
     int R = c->rows_per_item_opt;
     if (R <= 0) {
-        // ≈ 8 work items per resident warp, but at least 16 rows per item (halo re-read ≤ 2/R)
-        int64_t want_chunks = (8 * resident_warps + a.strips * c->g.batch - 1) / (a.strips * c->g.batch);
-        if (want_chunks < 1) want_chunks = 1;
-        R = int((rows + want_chunks - 1) / want_chunks);
-        if (R < 16) R = 16;
+        if (c->kernel_opt == 0) {
+            // TMA kernel: ≈ 4 items per resident CTA (≈3 CTAs per SM); ≥ 32 rows per item so the
+            // two extra u^n rows of an item cost ≤ 6% of its u^n reads
+            const int64_t strips = (c->pitch + TmaGeom<T>::WC - 1) / TmaGeom<T>::WC;
+            const int64_t want = int64_t(12) * c->sm_count;
+            int64_t want_chunks = (want + strips * c->g.batch - 1) / (strips * c->g.batch);
+            if (want_chunks < 1) want_chunks = 1;
+            R = int((rows + want_chunks - 1) / want_chunks);
+            if (R < 32) R = 32;
+        } else {
+            // ≈ 8 work items per resident warp, but at least 16 rows per item
+            const int64_t resident_warps = int64_t(occ) * c->sm_count * 8;
+            int64_t want_chunks = (8 * resident_warps + a.strips * c->g.batch - 1) / (a.strips * c->g.batch);
+            if (want_chunks < 1) want_chunks = 1;
+            R = int((rows + want_chunks - 1) / want_chunks);
+            if (R < 16) R = 16;
+        }
     }
     if (R > rows) R = int(rows);
     a.rows_per_item = R;
     a.chunks = int((rows + R - 1) / R);
     a.items = a.strips * a.chunks * c->g.batch;
-    int64_t blocks = (a.items + 7) / 8;
-    blocks = std::min<int64_t>(blocks, int64_t(occ) * c->sm_count);
+    const bool tma = (c->kernel_opt == 0);
+    const int depth = c->depth_opt;
+    const size_t smem = tma ? size_t(depth) * (tma_slot_bytes<T, MODE>() + 2 * sizeof(uint64_t)) : 0;
+    int occ_b = occ;
+    if (tma) {
+        // the TMA kernel's items are 4 KB-wide strips
+        a.strips = (c->pitch + TmaGeom<T>::WC - 1) / TmaGeom<T>::WC;
+        a.items = a.strips * a.chunks * c->g.batch;
+        int& ob = c->bulk_blocks_per_sm[MODE][START ? 1 : 0];
+        int& key = c->bulk_occ_key[MODE][START ? 1 : 0];
+        if (ob == 0 || key != depth) {
+            CK(cudaFuncSetAttribute(k_step2d_tma<T, MODE, START>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_step2d_tma<T, MODE, START>, (TMA_NC + 1) * 32, smem));
+            if (ob < 1) return fail(TSW_ERR_ARG, "TMA stencil does not fit on an SM (depth %d)", depth);
+            key = depth;
+        }
+        occ_b = ob;
+    }
+    int64_t blocks = tma ? a.items : (a.items + 7) / 8;
+    blocks = std::min<int64_t>(blocks, int64_t(occ_b) * c->sm_count);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         tsw_status st = timing_events(c, &e0, &e1);
         if (st) return st;
         CK(cudaEventRecord(e0, c->stream));
     }
-    k_step2d<T, MODE, START><<<unsigned(blocks), 256, 0, c->stream>>>(a);
+    if (tma)
+        k_step2d_tma<T, MODE, START><<<unsigned(blocks), (TMA_NC + 1) * 32, smem, c->stream>>>(a, depth);
+    else
+        k_step2d<T, MODE, START><<<unsigned(blocks), 256, 0, c->stream>>>(a);
     CKL();
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
@@ -370,10 +424,10 @@ tsw_status prescale_all(tsw_ctx* c) {
 
 tsw_status alloc_coeff(tsw_ctx* c, int mode) {
     if (c->have_coeff && c->mode == mode) return TSW_OK;
-    cudaFree(c->h1);
-    cudaFree(c->h2);
-    cudaFree(c->c1);
-    cudaFree(c->c2);
+    dfree_guarded(c->h1);
+    dfree_guarded(c->h2);
+    dfree_guarded(c->c1);
+    dfree_guarded(c->c2);
     c->h1 = c->h2 = nullptr;
     c->c1 = c->c2 = nullptr;
     c->have_coeff = false;
@@ -386,10 +440,10 @@ tsw_status alloc_coeff(tsw_ctx* c, int mode) {
         c->cstride2 = c->mstride;
     }
     const size_t B = size_t(c->g.batch);
-    CK(cudaMalloc(&c->h1, B * c->cstride1 * sizeof(double)));
-    CK(cudaMalloc(&c->h2, B * c->cstride2 * sizeof(double)));
-    CK(cudaMalloc(&c->c1, B * c->cstride1 * c->esz));
-    CK(cudaMalloc(&c->c2, B * c->cstride2 * c->esz));
+    CK(dmalloc_guarded(reinterpret_cast<void**>(&c->h1), B * c->cstride1 * sizeof(double)));  // (guards: see GUARD)
+    CK(dmalloc_guarded(reinterpret_cast<void**>(&c->h2), B * c->cstride2 * sizeof(double)));
+    CK(dmalloc_guarded(&c->c1, B * c->cstride1 * c->esz));
+    CK(dmalloc_guarded(&c->c2, B * c->cstride2 * c->esz));
     CK(cudaMemsetAsync(c->h1, 0, B * c->cstride1 * sizeof(double), c->stream));
     CK(cudaMemsetAsync(c->h2, 0, B * c->cstride2 * sizeof(double), c->stream));
     return TSW_OK;
@@ -486,8 +540,11 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     if ((st = zero_boundary(c, c->buf[1]))) return st;
     c->dt = dt;
     if ((st = prescale_all(c))) return st;
-    if (c->g.dim == 2 && c->g.nranks > 1) {
+    c->ghosts_valid = false;
+    if (c->g.dim == 2 && c->g.nranks > 1 && c->comm) {
+        // ghost rows of u^n (loopback groups exchange in tsw_group_step instead)
         if ((st = exchange_nccl(c, c->buf[0]))) return st;
+        c->ghosts_valid = true;
     }
     c->n = n;
     c->have_init = true;
@@ -582,7 +639,7 @@ tsw_status tsw_create(const tsw_grid_desc* gd, tsw_ctx** out) {
     }
     const size_t bytes = size_t(g.batch) * c->mstride * c->esz;
     for (int k = 0; k < 2; ++k) {
-        e = cudaMalloc(&c->buf[k], bytes);
+        e = dmalloc_guarded(&c->buf[k], bytes);
         if (e != cudaSuccess)
             return bail(fail(e == cudaErrorMemoryAllocation ? TSW_ERR_OOM : TSW_ERR_CUDA, "cudaMalloc(%zu): %s", bytes,
                              cudaGetErrorString(e)));
@@ -607,8 +664,13 @@ void tsw_destroy(tsw_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    void* ptrs[] = {c->buf[0], c->buf[1], c->h1, c->h2, c->c1, c->c2, c->d_eps, c->d_amp,
-                    c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64};
+    dfree_guarded(c->buf[0]);
+    dfree_guarded(c->buf[1]);
+    dfree_guarded(c->h1);
+    dfree_guarded(c->h2);
+    dfree_guarded(c->c1);
+    dfree_guarded(c->c2);
+    void* ptrs[] = {c->d_eps, c->d_amp, c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -794,6 +856,8 @@ tsw_status tsw_step(tsw_ctx* c, int64_t nsteps) {
     if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
     if (nsteps < 0) return fail(TSW_ERR_ARG, "nsteps must be >= 0");
     if (!c->have_init) return fail(TSW_ERR_STATE, "tsw_set_initial / tsw_set_state first");
+    if (c->g.nranks > 1 && !c->comm)
+        return fail(TSW_ERR_STATE, "nranks > 1: call tsw_nccl_init (or step the slabs with tsw_group_step)");
     tsw_status st = set_dev(c);
     if (st) return st;
     return do_steps(c, nsteps);
@@ -811,9 +875,12 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
     }
     tsw_status st = set_dev(cs[0]);
     if (st) return st;
-    if (cs[0]->n == 0) {
-        // initial ghost rows of u^0 (set_initial could not exchange without NCCL)
+    bool need = false;
+    for (int r = 0; r < n; ++r) need = need || !cs[r]->ghosts_valid;
+    if (need) {
+        // ghost rows of the current level (set_initial / set_state cannot exchange without NCCL)
         if ((st = exchange_loopback(cs, n))) return st;
+        for (int r = 0; r < n; ++r) cs[r]->ghosts_valid = true;
     }
     for (int64_t s = 0; s < nsteps; ++s) {
         for (int r = 0; r < n; ++r) {
@@ -859,10 +926,8 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     k_energy_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_partial, a.nblk, w, c->d_out);
     CKL();
     c->launches += 2;
-    if (c->g.nranks > 1) {
-        if (!c->comm) return fail(TSW_ERR_STATE, "nranks > 1 but tsw_nccl_init was not called");
+    if (c->g.nranks > 1 && c->comm)  // without a communicator (loopback group): this slab's share
         NK(nccl().AllReduce(c->d_out, c->d_out, size_t(c->g.batch), NCCL_F64, NCCL_SUM, c->comm, c->stream));
-    }
     CK(cudaMemcpyAsync(out_B, c->d_out, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return TSW_OK;
@@ -905,8 +970,7 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
     CK(cudaMemcpyAsync(v.data(), c->d_out, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(ix.data(), c->d_idx, sizeof(long long) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (c->g.nranks > 1) {
-        if (!c->comm) return fail(TSW_ERR_STATE, "nranks > 1 but tsw_nccl_init was not called");
+    if (c->g.nranks > 1 && c->comm) {  // without a communicator (loopback group): this slab's extrema
         // values: empty local regions must not win → ±inf; indices: first global extremum
         std::vector<double> mx(B), mn(B);
         for (int b = 0; b < B; ++b) {
@@ -991,6 +1055,16 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
     if (key == TSW_OPT_ROWS_PER_ITEM) {
         if (value < 0 || value > (1 << 30)) return fail(TSW_ERR_ARG, "rows per item must be >= 0");
         c->rows_per_item_opt = int(value);
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_KERNEL) {
+        if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "kernel must be 0 (TMA pipeline) or 1 (register)");
+        c->kernel_opt = int(value);
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_DEPTH) {
+        if (value < 2 || value > 32) return fail(TSW_ERR_ARG, "depth must be in [2, 32]");
+        c->depth_opt = int(value);
         return TSW_OK;
     }
     if (key == TSW_OPT_TIME_KERNELS) {

@@ -345,7 +345,7 @@ def test_config5_batched_family():
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("kind", [inputs.H_DELTA_LINE_X, inputs.H_DELTA_POINT])
 def test_loopback_slabs_bitwise(P, dtype, kind):
-    cfg = inputs.config(2, nx=260, ny=151, dx=0.01, dy=0.01, kind=kind, eps=[0.2, 0.3], amp=[1.0, 0.0], dt=3e-3)
+    cfg = inputs.config(2, nx=260, ny=151, dx=0.01, dy=0.01, kind=kind, eps=[0.2, 0.3], amp=[1.0, 0.0], dt=1e-3)
     u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(NP[dtype])
     one = tsw.Solver.from_config(cfg, dtype)
     one.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
