@@ -705,6 +705,107 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a, double* __restrict
     }
 }
 
+// 2D energy, row march: a warp owns 32·V columns of a chunk of rows and reads each of the two
+// levels once, vectorised (the x-face right neighbour of a lane's last element comes from the
+// next lane; lane 31 reads one scalar).  One CTA (8 warps) = one item; partial[b][item].
+struct Energy2Args {
+    int mode;
+    const void* unp1;  // newer level (u^n of the ctx)
+    const void* un;    // older level (u^{n−1})
+    const void* c1;
+    const void* c2;
+    int64_t nx, ny, r0, pitch, mstride, cstride1, cstride2;
+    int32_t rows;          // owned rows: storage rows 1..rows
+    int32_t rows_per_item;
+    int32_t chunks;
+    int64_t cta_strips;    // ceil(pitch / (8·32·V))
+    int64_t items_per_member;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* __restrict__ partial) {
+    constexpr int V = Vec16<T>::N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t item = blockIdx.x;
+    const int b = blockIdx.y;
+    const int64_t cstrip = item % a.cta_strips;
+    const int chunk = int(item / a.cta_strips);
+    const int64_t cs = (cstrip * 8 + warp) * 32 * V;
+    const int64_t col = cs + int64_t(lane) * V;
+    const int s0 = 1 + chunk * a.rows_per_item;
+    const int s1 = min(s0 + a.rows_per_item, a.rows + 1);
+    const T* A = static_cast<const T*>(a.unp1) + b * a.mstride;
+    const T* Bv = static_cast<const T*>(a.un) + b * a.mstride;
+    const T* C1 = static_cast<const T*>(a.c1) + b * a.cstride1;
+    const T* C2 = static_cast<const T*>(a.c2) + b * a.cstride2;
+    double acc = 0.0;
+    if (cs < a.pitch) {
+        bool colint[V], xface[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            colint[k] = (col + k >= 1) && (col + k <= a.nx - 2);
+            xface[k] = (col + k <= a.nx - 2);
+        }
+        T c1l[V];
+        if (a.mode == MODE_LINE) vload(C1 + col, c1l);
+        const double c2s = (a.mode == MODE_LINE) ? (double)C2[0] : 0.0;
+        T ac[V], bc[V], an[V], bn[V];
+        vload(A + s0 * a.pitch + col, ac);
+        vload(Bv + s0 * a.pitch + col, bc);
+        for (int s = s0; s < s1; ++s) {
+            const int64_t g = a.r0 + s - 1;
+            vload(A + (s + 1) * a.pitch + col, an);
+            vload(Bv + (s + 1) * a.pitch + col, bn);
+            T ar = __shfl_down_sync(0xffffffffu, ac[0], 1);
+            T br = __shfl_down_sync(0xffffffffu, bc[0], 1);
+            if (lane == 31) {
+                const bool ok = cs + 32 * V < a.pitch;
+                ar = ok ? A[s * a.pitch + cs + 32 * V] : (T)0;
+                br = ok ? Bv[s * a.pitch + cs + 32 * V] : (T)0;
+            }
+            T c1d[V], c2d[V];
+            if (a.mode == MODE_DENSE) {
+                vload(C1 + s * a.pitch + col, c1d);
+                vload(C2 + (s + 1) * a.pitch + col, c2d);
+            }
+            const bool row_int = (g >= 1) && (g <= a.ny - 2);
+            const bool yface = (g <= a.ny - 2);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const double a0 = (double)ac[k], b0 = (double)bc[k];
+                if (row_int && colint[k]) {
+                    const double d = a0 - b0;
+                    acc += d * d;
+                }
+                if (row_int && xface[k]) {
+                    const double a1 = (double)((k == V - 1) ? ar : ac[k + 1]);
+                    const double b1 = (double)((k == V - 1) ? br : bc[k + 1]);
+                    const double c = (a.mode == MODE_LINE) ? (double)c1l[k] : (double)c1d[k];
+                    acc += (c * (a1 - a0)) * (b1 - b0);
+                }
+                if (yface && colint[k]) {
+                    const double c = (a.mode == MODE_LINE) ? c2s : (double)c2d[k];
+                    acc += (c * ((double)an[k] - a0)) * ((double)bn[k] - b0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                ac[k] = an[k];
+                bc[k] = bn[k];
+            }
+        }
+    }
+    __shared__ double red[8];
+    acc = warp_sum(acc);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = (threadIdx.x < 8) ? red[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) partial[b * a.items_per_member + item] = v;
+    }
+}
+
 // Final pass: one warp per member sums its partials in a fixed order (deterministic) and scales.
 __global__ void k_energy_final(const double* __restrict__ partial, int nblk, double w, double* __restrict__ out) {
     const int b = blockIdx.x;

@@ -204,10 +204,53 @@ tsw_status timing_events(tsw_ctx* c, cudaEvent_t* e0, cudaEvent_t* e1) {
     return TSW_OK;
 }
 
+// Rows per work item: maximise the useful fraction of the last wave of items over the G
+// resident workers, discounted by the halo re-read (two extra u^n rows per item, u^n being a
+// third of the traffic); ties go to longer items.
+int choose_rows_per_item(int64_t rows, int64_t strips, int64_t batch, int64_t G) {
+    double best = -1.0;
+    int bestR = int(rows);
+    const int64_t cmax = std::max<int64_t>(1, rows / 8);
+    for (int64_t cch = 1; cch <= cmax; ++cch) {
+        const int64_t R = (rows + cch - 1) / cch;
+        const int64_t c2 = (rows + R - 1) / R;
+        const int64_t items = strips * c2 * batch;
+        const int64_t waves = (items + G - 1) / G;
+        const double eff = double(items) / double(waves * G);
+        const double score = eff / (1.0 + (2.0 / double(R)) / 3.0);
+        if (score > best + 1e-9) {
+            best = score;
+            bestR = int(R);
+        }
+    }
+    return bestR;
+}
+
+// Resident CTAs per SM of the TMA stencil at the ctx's ring depth (cached; 0 on error).
+template <typename T, int MODE, bool START>
+tsw_status tma_occupancy(tsw_ctx* c, int* occ_out, size_t* smem_out) {
+    const int depth = c->depth_opt;
+    const size_t smem = size_t(depth) * (tma_slot_bytes<T, MODE>() + 2 * sizeof(uint64_t));
+    int& ob = c->bulk_blocks_per_sm[MODE][START ? 1 : 0];
+    int& key = c->bulk_occ_key[MODE][START ? 1 : 0];
+    if (ob == 0 || key != depth) {
+        CK(cudaFuncSetAttribute(k_step2d_tma<T, MODE, START>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_step2d_tma<T, MODE, START>, (TMA_NC + 1) * 32, smem));
+        if (ob < 1) return fail(TSW_ERR_ARG, "TMA stencil does not fit on an SM (depth %d)", depth);
+        key = depth;
+    }
+    *occ_out = ob;
+    *smem_out = smem;
+    return TSW_OK;
+}
+
 // ---- 2D stencil launch ---------------------------------------------------------------------
+// Updates storage rows [s_lo, s_hi) of every member: reads buf[cur] (u^n) and buf[cur^1]
+// (u^{n−1}), writes u^{n+1} in place into buf[cur^1].
 template <typename T, int MODE, bool START>
 tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
     if (s_hi <= s_lo) return TSW_OK;
+    const bool tma = (c->kernel_opt == 0);
     StepArgs<T> a;
     a.ucur = static_cast<const T*>(c->buf[c->cur]);
     a.uprev = static_cast<T*>(c->buf[c->cur ^ 1]);
@@ -220,58 +263,37 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
     a.nx = c->g.nx;
     a.s_lo = s_lo;
     a.s_hi = s_hi;
-    a.strips = c->pitch / (32 * Vec16<T>::N);
     a.dtT = (T)c->dt;
-    int& occ = c->step_blocks_per_sm[MODE][START ? 1 : 0];
-    if (occ == 0) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d<T, MODE, START>, 256, 0));
-        if (occ < 1) occ = 1;
+    // workers: TMA → CTAs (one 4 KB strip each); register kernel → warps (one 32·V strip each)
+    int occ = 0, threads = 0;
+    size_t smem = 0;
+    int64_t workers_per_block = 1;
+    if (tma) {
+        tsw_status st = tma_occupancy<T, MODE, START>(c, &occ, &smem);
+        if (st) return st;
+        a.strips = (c->pitch + TmaGeom<T>::WC - 1) / TmaGeom<T>::WC;
+        threads = (TMA_NC + 1) * 32;
+    } else {
+        int& o = c->step_blocks_per_sm[MODE][START ? 1 : 0];
+        if (o == 0) {
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_step2d<T, MODE, START>, 256, 0));
+            if (o < 1) o = 1;
+        }
+        occ = o;
+        a.strips = c->pitch / (32 * Vec16<T>::N);
+        threads = 256;
+        workers_per_block = 8;
     }
+    const int64_t G = int64_t(occ) * c->sm_count * workers_per_block;
     const int64_t rows = s_hi - s_lo;
     int R = c->rows_per_item_opt;
-    if (R <= 0) {
-        if (c->kernel_opt == 0) {
-            // TMA kernel: ≈ 4 items per resident CTA (≈3 CTAs per SM); ≥ 32 rows per item so the
-            // two extra u^n rows of an item cost ≤ 6% of its u^n reads
-            const int64_t strips = (c->pitch + TmaGeom<T>::WC - 1) / TmaGeom<T>::WC;
-            const int64_t want = int64_t(12) * c->sm_count;
-            int64_t want_chunks = (want + strips * c->g.batch - 1) / (strips * c->g.batch);
-            if (want_chunks < 1) want_chunks = 1;
-            R = int((rows + want_chunks - 1) / want_chunks);
-            if (R < 32) R = 32;
-        } else {
-            // ≈ 8 work items per resident warp, but at least 16 rows per item
-            const int64_t resident_warps = int64_t(occ) * c->sm_count * 8;
-            int64_t want_chunks = (8 * resident_warps + a.strips * c->g.batch - 1) / (a.strips * c->g.batch);
-            if (want_chunks < 1) want_chunks = 1;
-            R = int((rows + want_chunks - 1) / want_chunks);
-            if (R < 16) R = 16;
-        }
-    }
+    if (R <= 0) R = choose_rows_per_item(rows, a.strips, c->g.batch, G);
     if (R > rows) R = int(rows);
     a.rows_per_item = R;
     a.chunks = int((rows + R - 1) / R);
     a.items = a.strips * a.chunks * c->g.batch;
-    const bool tma = (c->kernel_opt == 0);
-    const int depth = c->depth_opt;
-    const size_t smem = tma ? size_t(depth) * (tma_slot_bytes<T, MODE>() + 2 * sizeof(uint64_t)) : 0;
-    int occ_b = occ;
-    if (tma) {
-        // the TMA kernel's items are 4 KB-wide strips
-        a.strips = (c->pitch + TmaGeom<T>::WC - 1) / TmaGeom<T>::WC;
-        a.items = a.strips * a.chunks * c->g.batch;
-        int& ob = c->bulk_blocks_per_sm[MODE][START ? 1 : 0];
-        int& key = c->bulk_occ_key[MODE][START ? 1 : 0];
-        if (ob == 0 || key != depth) {
-            CK(cudaFuncSetAttribute(k_step2d_tma<T, MODE, START>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_step2d_tma<T, MODE, START>, (TMA_NC + 1) * 32, smem));
-            if (ob < 1) return fail(TSW_ERR_ARG, "TMA stencil does not fit on an SM (depth %d)", depth);
-            key = depth;
-        }
-        occ_b = ob;
-    }
-    int64_t blocks = tma ? a.items : (a.items + 7) / 8;
-    blocks = std::min<int64_t>(blocks, int64_t(occ_b) * c->sm_count);
+    int64_t blocks = (a.items + workers_per_block - 1) / workers_per_block;
+    blocks = std::min<int64_t>(blocks, int64_t(occ) * c->sm_count);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         tsw_status st = timing_events(c, &e0, &e1);
@@ -279,9 +301,9 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
         CK(cudaEventRecord(e0, c->stream));
     }
     if (tma)
-        k_step2d_tma<T, MODE, START><<<unsigned(blocks), (TMA_NC + 1) * 32, smem, c->stream>>>(a, depth);
+        k_step2d_tma<T, MODE, START><<<unsigned(blocks), threads, smem, c->stream>>>(a, c->depth_opt);
     else
-        k_step2d<T, MODE, START><<<unsigned(blocks), 256, 0, c->stream>>>(a);
+        k_step2d<T, MODE, START><<<unsigned(blocks), threads, 0, c->stream>>>(a);
     CKL();
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
@@ -379,15 +401,16 @@ tsw_status exchange_nccl(tsw_ctx* c, void* field) {
 }
 
 // Loopback: ranks are ctxs on one device and stream; copy rows device-to-device.
-tsw_status exchange_loopback(tsw_ctx** cs, int n) {
+// level 0 = u^n (buf[cur]), 1 = u^{n−1} (buf[cur^1]).
+tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0) {
     for (int r = 0; r + 1 < n; ++r) {
         tsw_ctx* a = cs[r];      // upper slab (smaller rows)
         tsw_ctx* b = cs[r + 1];  // lower slab
         const size_t row_a = size_t(a->pitch) * a->esz;
         const size_t row_b = size_t(b->pitch) * b->esz;
         for (int m = 0; m < a->g.batch; ++m) {
-            char* ma = static_cast<char*>(a->buf[a->cur]) + size_t(m) * a->mstride * a->esz;
-            char* mb = static_cast<char*>(b->buf[b->cur]) + size_t(m) * b->mstride * b->esz;
+            char* ma = static_cast<char*>(a->buf[a->cur ^ level]) + size_t(m) * a->mstride * a->esz;
+            char* mb = static_cast<char*>(b->buf[b->cur ^ level]) + size_t(m) * b->mstride * b->esz;
             // a's last owned row → b's ghost row 0 ; b's first owned row → a's ghost row ny_local+1
             CK(cudaMemcpyAsync(mb, ma + size_t(a->ny_local) * row_a, size_t(a->g.nx) * a->esz, cudaMemcpyDeviceToDevice,
                                a->stream));
@@ -542,8 +565,10 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     if ((st = prescale_all(c))) return st;
     c->ghosts_valid = false;
     if (c->g.dim == 2 && c->g.nranks > 1 && c->comm) {
-        // ghost rows of u^n (loopback groups exchange in tsw_group_step instead)
+        // ghost rows of both levels (the energy of (u^n, u^{n−1}) reads both; loopback groups
+        // exchange in tsw_group_step instead)
         if ((st = exchange_nccl(c, c->buf[0]))) return st;
+        if ((st = exchange_nccl(c, c->buf[1]))) return st;
         c->ghosts_valid = true;
     }
     c->n = n;
@@ -645,7 +670,7 @@ tsw_status tsw_create(const tsw_grid_desc* gd, tsw_ctx** out) {
                              cudaGetErrorString(e)));
         cudaMemsetAsync(c->buf[k], 0, bytes, c->stream);
     }
-    c->nblk_red = std::max(1, std::min(4 * c->sm_count, 65535 / std::max(1, g.batch)));
+    c->nblk_red = 4096;  // partials per member (energy / wave2 reductions)
     if (cudaMalloc(&c->d_partial, sizeof(double) * size_t(g.batch) * c->nblk_red) != cudaSuccess ||
         cudaMalloc(&c->d_out, sizeof(double) * 4 * size_t(g.batch)) != cudaSuccess ||
         cudaMalloc(&c->d_argpart, sizeof(ArgVal) * 2 * size_t(g.batch) * c->nblk_red) != cudaSuccess ||
@@ -878,8 +903,9 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
     bool need = false;
     for (int r = 0; r < n; ++r) need = need || !cs[r]->ghosts_valid;
     if (need) {
-        // ghost rows of the current level (set_initial / set_state cannot exchange without NCCL)
-        if ((st = exchange_loopback(cs, n))) return st;
+        // ghost rows of both levels (set_initial / set_state cannot exchange without NCCL)
+        if ((st = exchange_loopback(cs, n, 0))) return st;
+        if ((st = exchange_loopback(cs, n, 1))) return st;
         for (int r = 0; r < n; ++r) cs[r]->ghosts_valid = true;
     }
     for (int64_t s = 0; s < nsteps; ++s) {
@@ -899,31 +925,66 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     if (!c->have_init || c->n < 1) return fail(TSW_ERR_STATE, "energy E^{n-1/2} needs n >= 1");
     tsw_status st = set_dev(c);
     if (st) return st;
-    EnergyArgs a;
-    a.dim = c->g.dim;
-    a.mode = c->mode;
-    a.unp1 = c->buf[c->cur];
-    a.un = c->buf[c->cur ^ 1];
-    a.c1 = c->c1;
-    a.c2 = c->c2;
-    a.nx = c->g.nx;
-    a.ny = c->g.ny;
-    a.r0 = c->r0;
-    a.pitch = c->pitch;
-    a.mstride = c->mstride;
-    a.cstride1 = c->cstride1;
-    a.cstride2 = c->cstride2;
-    a.ny_local = c->ny_local;
-    const int64_t total = ((c->g.dim == 1) ? 1 : c->ny_local) * c->g.nx;
-    a.nblk = grid_for(total, 256, c->nblk_red);
-    dim3 grid(unsigned(a.nblk), unsigned(c->g.batch));
-    if (is_f64(c))
-        k_energy<double><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
-    else
-        k_energy<float><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
-    CKL();
+    int nparts = 0;
+    if (c->g.dim == 2) {
+        Energy2Args a;
+        a.mode = c->mode;
+        a.unp1 = c->buf[c->cur];
+        a.un = c->buf[c->cur ^ 1];
+        a.c1 = c->c1;
+        a.c2 = c->c2;
+        a.nx = c->g.nx;
+        a.ny = c->g.ny;
+        a.r0 = c->r0;
+        a.pitch = c->pitch;
+        a.mstride = c->mstride;
+        a.cstride1 = c->cstride1;
+        a.cstride2 = c->cstride2;
+        a.rows = int32_t(c->ny_local);
+        const int64_t cta_w = 8 * 32 * int64_t(16 / c->esz);
+        a.cta_strips = (c->pitch + cta_w - 1) / cta_w;
+        // ≈ 4 CTAs per SM over the batch, ≤ nblk_red partials per member
+        int64_t chunks = (int64_t(4) * c->sm_count + a.cta_strips * c->g.batch - 1) / (a.cta_strips * c->g.batch);
+        chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, std::max<int64_t>(1, c->nblk_red / a.cta_strips)));
+        chunks = std::min<int64_t>(chunks, c->ny_local);
+        a.rows_per_item = int32_t((c->ny_local + chunks - 1) / chunks);
+        a.chunks = int32_t((c->ny_local + a.rows_per_item - 1) / a.rows_per_item);
+        a.items_per_member = a.cta_strips * a.chunks;
+        if (a.items_per_member > c->nblk_red) return fail(TSW_ERR_ARG, "energy: too many partials (pitch too wide)");
+        nparts = int(a.items_per_member);
+        dim3 grid(unsigned(a.items_per_member), unsigned(c->g.batch));
+        if (is_f64(c))
+            k_energy2d<double><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+        else
+            k_energy2d<float><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+        CKL();
+    } else {
+        EnergyArgs a;
+        a.dim = c->g.dim;
+        a.mode = c->mode;
+        a.unp1 = c->buf[c->cur];
+        a.un = c->buf[c->cur ^ 1];
+        a.c1 = c->c1;
+        a.c2 = c->c2;
+        a.nx = c->g.nx;
+        a.ny = c->g.ny;
+        a.r0 = c->r0;
+        a.pitch = c->pitch;
+        a.mstride = c->mstride;
+        a.cstride1 = c->cstride1;
+        a.cstride2 = c->cstride2;
+        a.ny_local = c->ny_local;
+        a.nblk = grid_for(c->g.nx, 256, c->nblk_red);
+        nparts = a.nblk;
+        dim3 grid(unsigned(a.nblk), unsigned(c->g.batch));
+        if (is_f64(c))
+            k_energy<double><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+        else
+            k_energy<float><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+        CKL();
+    }
     const double w = ((c->g.dim == 1) ? c->g.dx : c->g.dx * c->g.dy) / (c->dt * c->dt);
-    k_energy_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_partial, a.nblk, w, c->d_out);
+    k_energy_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_partial, nparts, w, c->d_out);
     CKL();
     c->launches += 2;
     if (c->g.nranks > 1 && c->comm)  // without a communicator (loopback group): this slab's share
