@@ -126,14 +126,15 @@ def cpu_baseline(cfg, dtype: str, budget_s: float = 15.0, rows: int = 1024):
     from paper_2005_11931_b200 import inputs
     u = inputs.uniform_dense_rows(cfg.nx, cfg.ny, j0, wny).astype(npdt)
     v = oracle.startup(2, c1, c2, u, None, cfg.dt)
-    oracle.leapfrog(2, c1, c2, v, u, 2)                  # page in
-    t = time.perf_counter()
-    v, u = oracle.leapfrog(2, c1, c2, v, u, 8)
-    t_step = max((time.perf_counter() - t) / 8, 1e-6)
-    steps = int(min(4000, max(8, budget_s / t_step)))
-    t = time.perf_counter()
-    oracle.leapfrog(2, c1, c2, v, u, steps)
-    el = time.perf_counter() - t
+    # doubling chunks of leapfrog steps until the budget is spent (each call also copies the slab)
+    oracle.leapfrog(2, c1, c2, v, u, 1)
+    steps, el, k = 0, 0.0, 8
+    while el < budget_s and steps < 20000:
+        t = time.perf_counter()
+        v, u = oracle.leapfrog(2, c1, c2, v, u, k)
+        el += time.perf_counter() - t
+        steps += k
+        k *= 2
     upd = rows * (cfg.nx - 2) * steps
     return {"value": upd / el / 1e9, "unit": UNIT, "cores": int(oracle.max_threads()), "kind": "oracle",
             "sample": f"{rows} rows x {cfg.nx} cols of the per-GPU slab, {steps} leapfrog steps, {dtype}, "

@@ -1,9 +1,9 @@
 mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$?
+tail -4 gpurun_out/pytest_gpu.log
+timeout 600 python tools/sweep.py --dtype f64 --depths 3,4,5 --rows 0,37,54,111,147 > gpurun_out/sweep_f64.log 2>&1
+cat gpurun_out/sweep_f64.log
+timeout 600 python tools/sweep.py --dtype f32 --depths 3,4,5 --rows 0,37,111 > gpurun_out/sweep_f32.log 2>&1
+cat gpurun_out/sweep_f32.log
 timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench_exit=$?
-cat gpurun_out/bench_default.json; tail -3 gpurun_out/bench_default.err
-timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-also > gpurun_out/plain.log 2>&1 && \
-timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-also --dtype f32 > gpurun_out/plain32.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_f64.csv python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-also > gpurun_out/ncu_launches.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step2d_tma -s 60 -c 1 -o gpurun_out/prof_tma_f64 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-also > gpurun_out/ncu_full.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step2d_tma -s 60 -c 1 -o gpurun_out/prof_tma_f32 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-also --dtype f32 > gpurun_out/ncu_full32.log 2>&1; echo ncu_exit=$?
-ls gpurun_out
+cat gpurun_out/bench_default.json
