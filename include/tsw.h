@@ -167,6 +167,7 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
 #define TSW_OPT_TIME_KERNELS 2
 #define TSW_OPT_KERNEL 3 /* 0: CTA-wide TMA bulk-copy row pipeline (default); 1: register-prefetch kernel */
 #define TSW_OPT_DEPTH 4  /* TMA ring stages per CTA, 2..32 (default 4) */
+#define TSW_OPT_GRAPHS 5 /* 1 (default): single-rank steps replay a CUDA graph of two levels; 0: plain launches */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
 
 /* Live per-kernel timing of the stencil (S2/S3) launches recorded since TSW_OPT_TIME_KERNELS was

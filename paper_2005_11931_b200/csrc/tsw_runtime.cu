@@ -171,6 +171,12 @@ struct tsw_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     int64_t timed_launches = 0, timed_updates = 0;
+    // slabs: exchange stream + events (boundary rows → exchange ∥ interior rows)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
+    // CUDA graphs of two leapfrog levels (single rank), one per buffer parity
+    bool use_graphs = true;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     // NCCL
     void* comm = nullptr;
 };
@@ -189,6 +195,14 @@ int grid_for(int64_t n, int threads, int cap) {
     if (b < 1) b = 1;
     if (b > cap) b = cap;
     return int(b);
+}
+
+void drop_graphs(tsw_ctx* c) {
+    for (int k = 0; k < 2; ++k)
+        if (c->gexec[k]) {
+            cudaGraphExecDestroy(c->gexec[k]);
+            c->gexec[k] = nullptr;
+        }
 }
 
 // ---- live kernel timing ----------------------------------------------------------------------
@@ -377,7 +391,8 @@ tsw_status step1d_t(tsw_ctx* c, int64_t k) {
 // ---- ghost rows -------------------------------------------------------------------------------
 // NCCL: send my first owned row up to rank−1 and my last owned row down to rank+1; receive their
 // rows into my ghost rows (storage rows 0 and ny_local+1).  Rows are contiguous: no packing.
-tsw_status exchange_nccl(tsw_ctx* c, void* field) {
+tsw_status exchange_nccl(tsw_ctx* c, void* field, cudaStream_t stream = nullptr) {
+    if (!stream) stream = c->stream;
     if (c->g.nranks <= 1) return TSW_OK;
     if (!c->comm) return fail(TSW_ERR_STATE, "nranks > 1 but tsw_nccl_init was not called");
     Nccl& N = nccl();
@@ -388,12 +403,12 @@ tsw_status exchange_nccl(tsw_ctx* c, void* field) {
     for (int b = 0; b < c->g.batch; ++b) {
         char* m = base + size_t(b) * c->mstride * c->esz;
         if (c->g.rank > 0) {
-            NK(N.Send(m + 1 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, c->stream));
-            NK(N.Recv(m + 0 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, c->stream));
+            NK(N.Send(m + 1 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, stream));
+            NK(N.Recv(m + 0 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, stream));
         }
         if (c->g.rank < c->g.nranks - 1) {
-            NK(N.Send(m + size_t(c->ny_local) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, c->stream));
-            NK(N.Recv(m + size_t(c->ny_local + 1) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, c->stream));
+            NK(N.Send(m + size_t(c->ny_local) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, stream));
+            NK(N.Recv(m + size_t(c->ny_local + 1) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, stream));
         }
     }
     NK(N.GroupEnd());
@@ -402,7 +417,8 @@ tsw_status exchange_nccl(tsw_ctx* c, void* field) {
 
 // Loopback: ranks are ctxs on one device and stream; copy rows device-to-device.
 // level 0 = u^n (buf[cur]), 1 = u^{n−1} (buf[cur^1]).
-tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0) {
+tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0, cudaStream_t stream = nullptr) {
+    if (!stream) stream = cs[0]->stream;
     for (int r = 0; r + 1 < n; ++r) {
         tsw_ctx* a = cs[r];      // upper slab (smaller rows)
         tsw_ctx* b = cs[r + 1];  // lower slab
@@ -413,9 +429,9 @@ tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0) {
             char* mb = static_cast<char*>(b->buf[b->cur ^ level]) + size_t(m) * b->mstride * b->esz;
             // a's last owned row → b's ghost row 0 ; b's first owned row → a's ghost row ny_local+1
             CK(cudaMemcpyAsync(mb, ma + size_t(a->ny_local) * row_a, size_t(a->g.nx) * a->esz, cudaMemcpyDeviceToDevice,
-                               a->stream));
+                               stream));
             CK(cudaMemcpyAsync(ma + size_t(a->ny_local + 1) * row_a, mb + row_b, size_t(b->g.nx) * b->esz,
-                               cudaMemcpyDeviceToDevice, a->stream));
+                               cudaMemcpyDeviceToDevice, stream));
         }
     }
     return TSW_OK;
@@ -550,6 +566,7 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
                     c->dt_max);
     const bool shared = (flags & TSW_INIT_SHARED) != 0;
     const size_t bytes = size_t(c->g.batch) * c->mstride * c->esz;
+    drop_graphs(c);  // captured launches bake in dt
     c->cur = 0;
     CK(cudaMemsetAsync(c->buf[0], 0, bytes, c->stream));
     CK(cudaMemsetAsync(c->buf[1], 0, bytes, c->stream));
@@ -576,17 +593,116 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     return TSW_OK;
 }
 
+// Rows of a slab step: the boundary rows other ranks need (first owned row if rank > 0, last
+// owned row if rank < P−1) and the interior rest of [s_lo, s_hi).
+struct SlabSplit {
+    int32_t top = -1, bot = -1, ilo = 0, ihi = 0;
+};
+SlabSplit slab_split(const tsw_ctx* c) {
+    SlabSplit p;
+    p.ilo = c->s_lo;
+    p.ihi = c->s_hi;
+    if (c->g.rank > 0) {
+        p.top = 1;  // == s_lo
+        p.ilo = 2;
+    }
+    if (c->g.rank < c->g.nranks - 1) {
+        p.bot = int32_t(c->ny_local);  // == s_hi − 1
+        p.ihi = int32_t(c->ny_local);
+        if (p.bot == p.top) p.bot = -1;
+    }
+    if (p.ihi < p.ilo) p.ihi = p.ilo;
+    return p;
+}
+
+tsw_status launch_boundary_rows(tsw_ctx* c, bool start) {
+    const SlabSplit p = slab_split(c);
+    tsw_status st;
+    if (p.top >= 0 && (st = launch_step2d(c, start, p.top, p.top + 1))) return st;
+    if (p.bot >= 0 && (st = launch_step2d(c, start, p.bot, p.bot + 1))) return st;
+    return TSW_OK;
+}
+
+tsw_status launch_interior_rows(tsw_ctx* c, bool start) {
+    const SlabSplit p = slab_split(c);
+    return launch_step2d(c, start, p.ilo, p.ihi);
+}
+
+// One slab level with overlap: boundary rows on the ctx stream, then the NCCL
+// ghost-row exchange of the new level on the aux stream, concurrently with the interior rows;
+// the ctx stream waits for the exchange before the next level reads the ghost rows.
+tsw_status step_slab_overlapped(tsw_ctx* c) {
+    const bool start = (c->n == 0);
+    tsw_status st;
+    if ((st = launch_boundary_rows(c, start))) return st;
+    CK(cudaEventRecord(c->ev_bnd, c->stream));
+    CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
+    if ((st = exchange_nccl(c, c->buf[c->cur ^ 1], c->aux))) return st;
+    CK(cudaEventRecord(c->ev_comm, c->aux));
+    if ((st = launch_interior_rows(c, start))) return st;
+    CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+    c->cur ^= 1;
+    c->n++;
+    return TSW_OK;
+}
+
+// Two leapfrog levels captured once per buffer parity and replayed (single rank, n ≥ 1).
+tsw_status step_pair_graph(tsw_ctx* c) {
+    cudaGraphExec_t& ge = c->gexec[c->cur];
+    if (!ge) {
+        const int cur0 = c->cur;
+        const int64_t launches0 = c->launches;
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+        tsw_status st = launch_step2d(c, false, c->s_lo, c->s_hi);
+        if (!st) {
+            c->cur ^= 1;
+            st = launch_step2d(c, false, c->s_lo, c->s_hi);
+        }
+        cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+        c->cur = cur0;
+        c->launches = launches0;
+        if (st) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) return fail(TSW_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&ge, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            ge = nullptr;
+            return fail(TSW_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+        }
+    }
+    CK(cudaGraphLaunch(ge, c->stream));
+    c->launches += 2;
+    c->n += 2;  // two levels: the buffer parity is unchanged
+    return TSW_OK;
+}
+
 tsw_status do_steps(tsw_ctx* c, int64_t k) {
     if (k <= 0) return TSW_OK;
     if (c->g.dim == 1) return is_f64(c) ? step1d_t<double>(c, k) : step1d_t<float>(c, k);
-    for (int64_t s = 0; s < k; ++s) {
-        tsw_status st = launch_step2d(c, c->n == 0, c->s_lo, c->s_hi);
-        if (st) return st;
+    tsw_status st;
+    if (c->g.nranks > 1) {
+        for (int64_t s = 0; s < k; ++s)
+            if ((st = step_slab_overlapped(c))) return st;
+        return TSW_OK;
+    }
+    int64_t s = 0;
+    if (c->n == 0) {  // the start-up level
+        if ((st = launch_step2d(c, true, c->s_lo, c->s_hi))) return st;
         c->cur ^= 1;
         c->n++;
-        if (c->g.nranks > 1) {
-            if ((st = exchange_nccl(c, c->buf[c->cur]))) return st;
-        }
+        s = 1;
+    }
+    const bool graphs = c->use_graphs && !c->timing;
+    for (; s + 1 < k && graphs; s += 2)
+        if ((st = step_pair_graph(c))) return st;
+    for (; s < k; ++s) {
+        if ((st = launch_step2d(c, false, c->s_lo, c->s_hi))) return st;
+        c->cur ^= 1;
+        c->n++;
     }
     return TSW_OK;
 }
@@ -662,6 +778,14 @@ tsw_status tsw_create(const tsw_grid_desc* gd, tsw_ctx** out) {
             return bail(fail(TSW_ERR_CUDA, "cudaStreamCreate failed"));
         c->own_stream = true;
     }
+    if (g.dim == 2 && g.nranks > 1) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(TSW_ERR_CUDA, "exchange stream/events"));
+    }
     const size_t bytes = size_t(g.batch) * c->mstride * c->esz;
     for (int k = 0; k < 2; ++k) {
         e = dmalloc_guarded(&c->buf[k], bytes);
@@ -699,6 +823,10 @@ void tsw_destroy(tsw_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    drop_graphs(c);
+    if (c->ev_bnd) cudaEventDestroy(c->ev_bnd);
+    if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+    if (c->aux) cudaStreamDestroy(c->aux);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -908,14 +1036,23 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
         if ((st = exchange_loopback(cs, n, 1))) return st;
         for (int r = 0; r < n; ++r) cs[r]->ghosts_valid = true;
     }
+    // the slab schedule of step_slab_overlapped, with device copies on the aux stream
+    tsw_ctx* c0 = cs[0];
     for (int64_t s = 0; s < nsteps; ++s) {
+        const bool start = (c0->n == 0);
+        for (int r = 0; r < n; ++r)
+            if ((st = launch_boundary_rows(cs[r], start))) return st;
+        CK(cudaEventRecord(c0->ev_bnd, c0->stream));
+        CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
+        if ((st = exchange_loopback(cs, n, 1, c0->aux))) return st;
+        CK(cudaEventRecord(c0->ev_comm, c0->aux));
+        for (int r = 0; r < n; ++r)
+            if ((st = launch_interior_rows(cs[r], start))) return st;
+        CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
         for (int r = 0; r < n; ++r) {
-            tsw_ctx* c = cs[r];
-            if ((st = launch_step2d(c, c->n == 0, c->s_lo, c->s_hi))) return st;
-            c->cur ^= 1;
-            c->n++;
+            cs[r]->cur ^= 1;
+            cs[r]->n++;
         }
-        if ((st = exchange_loopback(cs, n))) return st;
     }
     return TSW_OK;
 }
@@ -1113,6 +1250,11 @@ int64_t tsw_launch_count(const tsw_ctx* c) { return c ? c->launches : 0; }
 
 tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
     if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
+    drop_graphs(c);  // captured launches bake in the kernel variant and its shape
+    if (key == TSW_OPT_GRAPHS) {
+        c->use_graphs = value != 0;
+        return TSW_OK;
+    }
     if (key == TSW_OPT_ROWS_PER_ITEM) {
         if (value < 0 || value > (1 << 30)) return fail(TSW_ERR_ARG, "rows per item must be >= 0");
         c->rows_per_item_opt = int(value);
