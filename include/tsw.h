@@ -55,7 +55,8 @@ typedef enum {
     TSW_H_CONST = 0,        /* h1 = h2 = h_b */
     TSW_H_DELTA_LINE_X = 1, /* h1 = h_b + A·φ_ε(x − xs)^order, h2 = h_b  (δ-line along x = xs; 1D: δ-point) */
     TSW_H_DELTA_POINT = 2,  /* h1 = h2 = h_b + A·(φ_ε(x − xs)·φ_ε(y − ys))^order  (tensor mollifier, R3) */
-    TSW_H_FACES = 3         /* dense caller-given faces (tsw_set_coeff_faces) */
+    TSW_H_FACES = 3,        /* dense caller-given faces (tsw_set_coeff_faces) */
+    TSW_H_PROFILE_X = 4     /* x-only profile: segments + singular terms (tsw_set_coeff_profile) */
 } tsw_hkind;
 
 /* tsw_set_initial flags */
@@ -94,6 +95,31 @@ void tsw_destroy(tsw_ctx* ctx);
  * h_ε in fp64 on the device at every half-grid face of this rank's slab (R2).  Validates
  * h_b > 0, A ≥ 0, ε ∈ (0, 1], order ∈ {1, 2}.  Prescaling to T happens in tsw_set_initial. */
 tsw_status tsw_set_coeff(tsw_ctx* ctx, const tsw_coeff_desc* h);
+
+/* Piecewise-constant depth in x with singular terms — the paper's own scenarios (§3.1
+ * Case 1 eq. (h2case): h_0 = 100 on [0,75), 10 on [75,100]; Cases 2–3 P:773–789:
+ * h_0 + δ(x−70), h_0 + δ²(x−70); §3.2.3: 100δ, 100δ²; 2D H(x,y) = h_0(x)):
+ *   h_ε(x) = v_0 + Σ_k (v_k − v_{k−1})·Φ((x − b_k)/ε) + Σ_j s_b·A_j·φ_ε(x − x_j)^{o_j}
+ * with Φ(t) = ∫_{−1}^{t} φ, the mollifier's primitive (convolution of a step with φ_ε).  h1 is
+ * evaluated at the x faces; h2 (2D) at the node columns, including the singular terms when
+ * isotropic (scalar depth H) and the segments only otherwise.  Coordinates follow the centred
+ * grid of R9 (the paper's [0, 100] is x + 50 there). */
+typedef struct {
+    int32_t nseg;              /* 1..64 constant segments */
+    const double* seg_value;   /* [nseg] depths v_k > 0 */
+    const double* seg_break;   /* [nseg−1] increasing breaks b_1 < …; segment k = [b_k, b_{k+1}) */
+    int32_t nsing;             /* 0..64 singular terms */
+    const double* sing_loc;    /* [nsing] x_j */
+    const double* sing_amp;    /* [nsing] A_j ≥ 0 */
+    const int32_t* sing_order; /* [nsing] 1 (δ ↦ φ_ε) or 2 (δ² ↦ φ_ε²) */
+    int32_t isotropic;         /* 2D: 1 ⇒ scalar depth (h2 = h1 profile); 0 ⇒ h2 = segments only */
+} tsw_profile_desc;
+
+/* Builds the faces of an x-only profile for every member b with ε = eps[b] (host [batch], each in
+ * (0, 1]) and singular amplitudes scaled by scale[b] (host [batch] ≥ 0, NULL ⇒ 1; 0 gives the
+ * background member of A₂).  A₂'s reference point xs becomes the first singular location (else
+ * the first break).  Errors: TSW_ERR_ARG. */
+tsw_status tsw_set_coeff_profile(tsw_ctx* ctx, const tsw_profile_desc* p, const double* eps, const double* scale);
 
 /* Dense override of the fp64 faces (kind TSW_H_FACES), host (on_device = 0) or device pointers:
  *   h1 [batch][ny_local][nx−1]   face (i+1/2, j) of local row j

@@ -49,6 +49,12 @@ def _L():
         lib.tswo_set_threads.argtypes = [i32]
         lib.tswo_max_threads.restype = i32
         lib.tswo_build_faces.argtypes = [i32, i32, i32, d, d, d, d, d, i64, i64, d, d, i64, i64, i64, i64, vp, vp]
+        lib.tswo_mollifier_primitive.restype = d
+        lib.tswo_mollifier_primitive.argtypes = [d]
+        lib.tswo_profile_eval.restype = d
+        lib.tswo_profile_eval.argtypes = [d, d, i32, vp, vp, i32, i32, vp, vp, vp, d]
+        lib.tswo_build_faces_profile.argtypes = [i32, i32, vp, vp, i32, vp, vp, vp, d, i32, d, i64, i64, d,
+                                                 i64, i64, i64, i64, vp, vp]
         lib.tswo_gershgorin_dt_max.restype = d
         lib.tswo_gershgorin_dt_max.argtypes = [i32, i64, i64, vp, vp, d, d]
         for s in ("f64", "f32"):
@@ -120,6 +126,53 @@ def build_faces(dim: int, kind: int, order: int, hb: float, amp: float, xs: floa
     h1 = np.empty((wny, wnx - 1), dtype=np.float64)
     h2 = np.empty((wny - 1, wnx), dtype=np.float64)
     _L().tswo_build_faces(2, kind, order, hb, amp, xs, ys, eps, nx, ny, dx, dy, i0, j0, wnx, wny, _p(h1), _p(h2))
+    return h1, h2
+
+
+def mollifier_primitive(t) -> np.ndarray:
+    """Φ(t) = ∫_{−1}^{t} φ (adaptive Simpson), elementwise."""
+    t = np.atleast_1d(np.asarray(t, dtype=np.float64))
+    return np.array([_L().tswo_mollifier_primitive(float(v)) for v in t.ravel()]).reshape(t.shape)
+
+
+class Profile:
+    """Piecewise-constant depth + singular terms (§3.1 Cases 1–3, §3.2.3; NEXT 1)."""
+
+    def __init__(self, seg_value, seg_break=(), sing_loc=(), sing_amp=(), sing_order=(), isotropic=False):
+        self.seg_value = np.ascontiguousarray(seg_value, dtype=np.float64)
+        self.seg_break = np.ascontiguousarray(seg_break if len(seg_break) else [0.0], dtype=np.float64)
+        self.nseg = len(seg_value)
+        self.sing_loc = np.ascontiguousarray(sing_loc if len(sing_loc) else [0.0], dtype=np.float64)
+        self.sing_amp = np.ascontiguousarray(sing_amp if len(sing_amp) else [0.0], dtype=np.float64)
+        self.sing_order = np.ascontiguousarray(sing_order if len(sing_order) else [1], dtype=np.int32)
+        self.nsing = len(sing_loc)
+        self.isotropic = bool(isotropic)
+
+    def eval(self, x, eps: float, with_sing: bool = True, sing_scale: float = 1.0) -> np.ndarray:
+        """h_ε(x) = (h_0 * φ_ε)(x) + Σ A φ_ε(x − x_k)^{o_k}."""
+        x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+        f = _L().tswo_profile_eval
+        return np.array([f(float(v), eps, self.nseg, _p(self.seg_value), _p(self.seg_break), int(with_sing),
+                           self.nsing, _p(self.sing_loc), _p(self.sing_amp), _p(self.sing_order), sing_scale)
+                         for v in x.ravel()]).reshape(x.shape)
+
+
+def build_faces_profile(dim: int, prof: "Profile", eps: float, nx: int, ny: int, dx: float, sing_scale: float = 1.0,
+                        i0: int = 0, j0: int = 0, wnx: Optional[int] = None, wny: Optional[int] = None):
+    """Faces of an x-only profile (h1 at x faces; h2 at y faces from node x_i)."""
+    wnx = nx - i0 if wnx is None else wnx
+    if dim == 1:
+        h1 = np.empty(wnx - 1)
+        _L().tswo_build_faces_profile(1, prof.nseg, _p(prof.seg_value), _p(prof.seg_break), prof.nsing,
+                                      _p(prof.sing_loc), _p(prof.sing_amp), _p(prof.sing_order), sing_scale,
+                                      int(prof.isotropic), eps, nx, 1, dx, i0, 0, wnx, 1, _p(h1), None)
+        return h1, None
+    wny = ny - j0 if wny is None else wny
+    h1 = np.empty((wny, wnx - 1))
+    h2 = np.empty((wny - 1, wnx))
+    _L().tswo_build_faces_profile(2, prof.nseg, _p(prof.seg_value), _p(prof.seg_break), prof.nsing,
+                                  _p(prof.sing_loc), _p(prof.sing_amp), _p(prof.sing_order), sing_scale,
+                                  int(prof.isotropic), eps, nx, ny, dx, i0, j0, wnx, wny, _p(h1), _p(h2))
     return h1, h2
 
 

@@ -140,6 +140,81 @@ double tswo_gershgorin_dt_max(int dim, int64_t nx, int64_t ny, const double* h1,
 }
 
 /* ---------------------------------------------------------------------------
+ * Piecewise-constant depth with singular terms (§3.1 Case 1
+ * eq. (h2case), Cases 2–3 P:773–789, §3.2.3, 2D H(x,y) = h_0(x)
+ * P:1145–1149).  h = Σ segments + Σ A_k δ^{o_k}(x − x_k), regularised as
+ *   h_ε(x) = (h_0 * φ_ε)(x) + Σ A_k φ_ε(x − x_k)^{o_k}
+ * and for the piecewise-constant part, with values v_0 … v_{m−1} and breaks b_1 < … < b_{m−1},
+ * h_0 = v_0 + Σ_k (v_k − v_{k−1}) H(x − b_k), so (H(· − b) * φ_ε)(x) = Φ((x − b)/ε) with the
+ * primitive Φ(t) = ∫_{−1}^{t} φ.  Φ has no closed form: the oracle integrates
+ * it by adaptive Simpson to 1e−15 (pinned against 40-digit mpmath quadrature).
+ * ------------------------------------------------------------------------- */
+static double phi_unit(double x) {
+    if (!(fabs(x) < 1.0)) return 0.0;
+    return ORACLE_MOLLIFIER_C * exp(1.0 / (x * x - 1.0));
+}
+
+static double simpson_rec(double a, double b, double eps, double whole, double fa, double fb, double fm,
+                          int depth) {
+    double m = 0.5 * (a + b), lm = 0.5 * (a + m), rm = 0.5 * (m + b);
+    double flm = phi_unit(lm), frm = phi_unit(rm);
+    double left = (m - a) / 6.0 * (fa + 4.0 * flm + fm);
+    double right = (b - m) / 6.0 * (fm + 4.0 * frm + fb);
+    if (depth <= 0 || fabs(left + right - whole) <= 15.0 * eps) return left + right + (left + right - whole) / 15.0;
+    return simpson_rec(a, m, 0.5 * eps, left, fa, fm, flm, depth - 1) +
+           simpson_rec(m, b, 0.5 * eps, right, fm, fb, frm, depth - 1);
+}
+
+/* Φ(t) = ∫_{−1}^{t} φ(x) dx; 0 for t ≤ −1, 1 for t ≥ 1. */
+double tswo_mollifier_primitive(double t) {
+    if (t <= -1.0) return 0.0;
+    if (t >= 1.0) return 1.0;
+    double a = -1.0, b = t;
+    double fa = phi_unit(a), fb = phi_unit(b), fm = phi_unit(0.5 * (a + b));
+    return simpson_rec(a, b, 1e-16, (b - a) / 6.0 * (fa + 4.0 * fm + fb), fa, fb, fm, 60);
+}
+
+/* h_ε at x: segments (nseg values, nseg−1 breaks) + (with_sing) the singular terms, each
+ * amplitude multiplied by sing_scale. */
+double tswo_profile_eval(double x, double eps, int nseg, const double* seg_value, const double* seg_break,
+                         int with_sing, int nsing, const double* sing_loc, const double* sing_amp,
+                         const int* sing_order, double sing_scale) {
+    double h = seg_value[0];
+    for (int k = 1; k < nseg; ++k) h += (seg_value[k] - seg_value[k - 1]) * tswo_mollifier_primitive((x - seg_break[k - 1]) / eps);
+    if (with_sing)
+        for (int k = 0; k < nsing; ++k) {
+            double p = tswo_phi_eps(x - sing_loc[k], eps);
+            if (sing_order[k] == 2) p = p * p;
+            h += (sing_scale * sing_amp[k]) * p;
+        }
+    return h;
+}
+
+/* Faces of a window (as tswo_build_faces) for an x-only profile: h1 at x faces (i+1/2) with the
+ * singular terms; h2 at y faces (i, j+1/2) evaluated at node x_i — with the singular terms when
+ * isotropic (scalar depth H(x)), segments only otherwise (vector depth, R6). */
+int tswo_build_faces_profile(int dim, int nseg, const double* seg_value, const double* seg_break, int nsing,
+                             const double* sing_loc, const double* sing_amp, const int* sing_order,
+                             double sing_scale, int isotropic, double eps, int64_t nx, int64_t ny, double dx,
+                             int64_t i0, int64_t j0, int64_t wnx, int64_t wny, double* h1, double* h2) {
+    (void)ny;
+    (void)j0;
+    if (dim == 1) wny = 1;
+    for (int64_t ii = 0; ii < wnx - 1; ++ii) {
+        double v = tswo_profile_eval(face_x(i0 + ii, nx, dx), eps, nseg, seg_value, seg_break, 1, nsing, sing_loc,
+                                     sing_amp, sing_order, sing_scale);
+        for (int64_t jj = 0; jj < wny; ++jj) h1[jj * (wnx - 1) + ii] = v;
+    }
+    if (dim == 2 && h2)
+        for (int64_t ii = 0; ii < wnx; ++ii) {
+            double v = tswo_profile_eval(node_x(i0 + ii, nx, dx), eps, nseg, seg_value, seg_break, isotropic, nsing,
+                                         sing_loc, sing_amp, sing_order, sing_scale);
+            for (int64_t jj = 0; jj < wny - 1; ++jj) h2[jj * wnx + ii] = v;
+        }
+    return 0;
+}
+
+/* ---------------------------------------------------------------------------
  * Everything below exists once per working precision T (R19): float and
  * double, generated from one macro so both are the same text.
  * ------------------------------------------------------------------------- */

@@ -130,9 +130,8 @@ __global__ void __launch_bounds__(256) k_step2d(const StepArgs<T> a) {
 #pragma unroll
         for (int k = 0; k < V; ++k) interior[k] = (col + k >= 1) && (col + k <= a.nx - 2);
 
-        // LINE coefficients are row-invariant: load once per item.
-        T c1r[V], c1l[V];
-        T c2s = (T)0;
+        // LINE coefficients are row-invariant: load once per item (c2 per node column).
+        T c1r[V], c1l[V], c2v[V];
         if (MODE == MODE_LINE) {
             const T* c1b = a.c1 + b * a.cstride1;
             vload(c1b + col, c1r);
@@ -141,7 +140,7 @@ __global__ void __launch_bounds__(256) k_step2d(const StepArgs<T> a) {
             c1l[0] = left;
 #pragma unroll
             for (int k = 1; k < V; ++k) c1l[k] = c1r[k - 1];
-            c2s = a.c2[b];
+            vload(a.c2 + b * a.cstride2 + col, c2v);
         }
 
         // register window: up = row s−1, cu = row s, dn = row s+1 ; pv = u^{n−1} row s
@@ -195,8 +194,8 @@ __global__ void __launch_bounds__(256) k_step2d(const StepArgs<T> a) {
                 T ur = (k == V - 1) ? right : cu[k + 1];
                 T l1 = (MODE == MODE_LINE) ? c1l[k] : c1l_d[k];
                 T r1 = (MODE == MODE_LINE) ? c1r[k] : c1r_d[k];
-                T d2 = (MODE == MODE_LINE) ? c2s : c2lo[k];
-                T u2 = (MODE == MODE_LINE) ? c2s : c2hi[k];
+                T d2 = (MODE == MODE_LINE) ? c2v[k] : c2lo[k];
+                T u2 = (MODE == MODE_LINE) ? c2v[k] : c2hi[k];
                 T v = node_update<T, START, true>(cu[k], ul, ur, up[k], dn[k], pv[k], l1, r1, d2, u2, a.dtT);
                 out[k] = interior[k] ? v : (T)0;
             }
@@ -378,15 +377,14 @@ __global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs
         bool interior[V];
 #pragma unroll
         for (int k = 0; k < V; ++k) interior[k] = (col + k >= 1) && (col + k <= a.nx - 2);
-        T c1r[V], c1l[V];
-        T c2s = (T)0;
-        if (MODE == MODE_LINE) {
+        T c1r[V], c1l[V], c2v[V];
+        if (MODE == MODE_LINE) {  // row-invariant: c1 per x face, c2 per node column
             const T* c1b = a.c1 + b * a.cstride1;
             vload(c1b + col, c1r);
             c1l[0] = (col > 0) ? __ldg(c1b + col - 1) : (T)0;
 #pragma unroll
             for (int k = 1; k < V; ++k) c1l[k] = c1r[k - 1];
-            c2s = a.c2[b];
+            vload(a.c2 + b * a.cstride2 + col, c2v);
         }
         T up[V], cu[V], dn[V], pv[V], c2lo[V], c2hi[V];
         const int L = s1 - s0 + 2;
@@ -425,8 +423,8 @@ __global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs
                     T ur = (k == V - 1) ? right : cu[k + 1];
                     T l1 = (MODE == MODE_LINE) ? c1l[k] : c1d_l[k];
                     T r1 = (MODE == MODE_LINE) ? c1r[k] : c1d_r[k];
-                    T d2 = (MODE == MODE_LINE) ? c2s : c2lo[k];
-                    T u2 = (MODE == MODE_LINE) ? c2s : c2hi[k];
+                    T d2 = (MODE == MODE_LINE) ? c2v[k] : c2lo[k];
+                    T u2 = (MODE == MODE_LINE) ? c2v[k] : c2hi[k];
                     T v = node_update<T, START, true>(cu[k], ul, ur, up[k], dn[k], pv[k], l1, r1, d2, u2, a.dtT);
                     out[k] = interior[k] ? v : (T)0;
                 }
@@ -548,8 +546,67 @@ __global__ void k_coeff_line(CoeffArgs a, double* __restrict__ h1, double* __res
             }
         }
         h1[b * a.cpitch + i] = h;
+        h2[b * a.cpitch + i] = (i < a.nx) ? a.hb : 0.0;  // R6: h2 ≡ h_b (per node column)
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) h2[b] = a.hb;
+}
+
+// ---- x-only profiles: piecewise-constant depth + singular terms ----------
+// Φ(t) = ∫_{−1}^{t} φ (the mollifier's primitive; no closed form) by tanh-sinh quadrature:
+// x = m + r·tanh(π/2·sinh u), u = k/32, |k| ≤ 140 (error ≈ 1e−15 absolute).
+__device__ double mollifier_primitive(double t) {
+    if (t <= -1.0) return 0.0;
+    if (t >= 1.0) return 1.0;
+    const double r = 0.5 * (t + 1.0), m = 0.5 * (t - 1.0);
+    const double hstep = 1.0 / 32.0, half_pi = 1.5707963267948966;
+    double acc = 0.0;
+    for (int k = -140; k <= 140; ++k) {
+        const double u = k * hstep;
+        const double sh = half_pi * sinh(u);
+        const double ch = cosh(sh);
+        const double w = half_pi * cosh(u) / (ch * ch);
+        const double x = m + r * tanh(sh);
+        if (fabs(x) < 1.0) acc += w * (TSW_MOLLIFIER_C * exp(1.0 / (x * x - 1.0)));
+    }
+    return r * hstep * acc;
+}
+
+struct ProfileArgs {
+    int nseg, nsing, isotropic;
+    const double* data;  // [nseg values][nseg−1 breaks][nsing loc][nsing amp][nsing order]
+    const double* eps;   // [B]
+    const double* scale; // [B] multiplies every singular amplitude
+    int64_t nx, cpitch;
+    double dx;
+};
+
+// h_ε(x) = v_0 + Σ_k (v_k − v_{k−1}) Φ((x − b_k)/ε) + Σ_j A_j·scale·φ_ε(x − x_j)^{o_j}
+// (h_{1,ε} = h_{0,ε} + φ_ε(x − 70), h_{2,ε} = h_{0,ε} + φ_ε²(x − 70)).
+__device__ double profile_eval(const ProfileArgs& a, double x, double eps, double scale, bool with_sing) {
+    const double* v = a.data;
+    const double* br = v + a.nseg;
+    const double* loc = br + (a.nseg - 1);
+    const double* amp = loc + a.nsing;
+    const double* ord = amp + a.nsing;
+    double h = v[0];
+    for (int k = 1; k < a.nseg; ++k) h += (v[k] - v[k - 1]) * mollifier_primitive((x - br[k - 1]) / eps);
+    if (with_sing)
+        for (int j = 0; j < a.nsing; ++j) {
+            double p = phi_eps(x - loc[j], eps);
+            if (ord[j] == 2.0) p = p * p;
+            h += (scale * amp[j]) * p;
+        }
+    return h;
+}
+
+// LINE storage: h1[b][i] at x faces (with the singular terms), h2[b][i] at node columns
+// (with them when isotropic — scalar depth H(x), P:1145–1149 — else segments only).
+__global__ void k_coeff_profile(ProfileArgs a, double* __restrict__ h1, double* __restrict__ h2) {
+    const int b = blockIdx.y;
+    const double eps = a.eps[b], sc = a.scale[b];
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.cpitch; i += int64_t(gridDim.x) * blockDim.x) {
+        h1[b * a.cpitch + i] = (i < a.nx - 1) ? profile_eval(a, grid_face(i, a.nx, a.dx), eps, sc, true) : 0.0;
+        h2[b * a.cpitch + i] = (i < a.nx) ? profile_eval(a, grid_node(i, a.nx, a.dx), eps, sc, a.isotropic != 0) : 0.0;
+    }
 }
 
 // POINT, dense storage layout: h1[b][s][i] = face (i+1/2, g), h2[b][s][i] = face (i, g−1/2),
@@ -620,7 +677,7 @@ __global__ void k_cfl(CflArgs a, unsigned long long* __restrict__ out) {
             r = 2.0 * ((h[i - 1] + h[i]) / (a.dx * a.dx));
         } else if (a.mode == MODE_LINE) {
             const double* h = a.h1 + b * a.cpitch;
-            const double hy = a.h2[b];
+            const double hy = a.h2[b * a.cpitch + i];
             r = 2.0 * ((h[i - 1] + h[i]) / (a.dx * a.dx) + (hy + hy) / (a.dy * a.dy));
         } else {
             const int64_t s = a.s_lo + k / (a.nx - 2);
@@ -690,7 +747,7 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a, double* __restrict
             acc += (c * ((double)A[o + 1] - a0)) * ((double)Bv[o + 1] - b0);
         }
         if (a.dim == 2 && col_int && g <= a.ny - 2) {
-            const double c = (a.mode == MODE_LINE) ? (double)C2[0] : (double)C2[(s + 1) * a.pitch + i];
+            const double c = (a.mode == MODE_LINE) ? (double)C2[i] : (double)C2[(s + 1) * a.pitch + i];
             acc += (c * ((double)A[o + a.pitch] - a0)) * ((double)Bv[o + a.pitch] - b0);
         }
     }
@@ -746,9 +803,11 @@ __global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* _
             colint[k] = (col + k >= 1) && (col + k <= a.nx - 2);
             xface[k] = (col + k <= a.nx - 2);
         }
-        T c1l[V];
-        if (a.mode == MODE_LINE) vload(C1 + col, c1l);
-        const double c2s = (a.mode == MODE_LINE) ? (double)C2[0] : 0.0;
+        T c1l[V], c2l[V];
+        if (a.mode == MODE_LINE) {
+            vload(C1 + col, c1l);
+            vload(C2 + col, c2l);
+        }
         T ac[V], bc[V], an[V], bn[V];
         vload(A + s0 * a.pitch + col, ac);
         vload(Bv + s0 * a.pitch + col, bc);
@@ -784,7 +843,7 @@ __global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* _
                     acc += (c * (a1 - a0)) * (b1 - b0);
                 }
                 if (yface && colint[k]) {
-                    const double c = (a.mode == MODE_LINE) ? c2s : (double)c2d[k];
+                    const double c = (a.mode == MODE_LINE) ? (double)c2l[k] : (double)c2d[k];
                     acc += (c * ((double)an[k] - a0)) * ((double)bn[k] - b0);
                 }
             }

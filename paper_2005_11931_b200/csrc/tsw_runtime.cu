@@ -471,9 +471,9 @@ tsw_status alloc_coeff(tsw_ctx* c, int mode) {
     c->c1 = c->c2 = nullptr;
     c->have_coeff = false;
     c->mode = mode;
-    if (mode == MODE_LINE) {
+    if (mode == MODE_LINE) {  // row-invariant coefficients: c1 per x face, c2 per node column
         c->cstride1 = c->pitch;
-        c->cstride2 = 1;
+        c->cstride2 = c->pitch;
     } else {
         c->cstride1 = c->mstride;
         c->cstride2 = c->mstride;
@@ -889,6 +889,71 @@ tsw_status tsw_set_coeff(tsw_ctx* c, const tsw_coeff_desc* h) {
     return TSW_OK;
 }
 
+tsw_status tsw_set_coeff_profile(tsw_ctx* c, const tsw_profile_desc* p, const double* eps, const double* scale) {
+    if (!c || !p || !eps) return fail(TSW_ERR_ARG, "NULL argument");
+    if (p->nseg < 1 || !p->seg_value || (p->nseg > 1 && !p->seg_break)) return fail(TSW_ERR_ARG, "need >= 1 segment");
+    if (p->nsing < 0 || (p->nsing > 0 && (!p->sing_loc || !p->sing_amp || !p->sing_order)))
+        return fail(TSW_ERR_ARG, "bad singular terms");
+    if (p->nseg > 64 || p->nsing > 64) return fail(TSW_ERR_ARG, "at most 64 segments / singular terms");
+    for (int k = 0; k < p->nseg; ++k)
+        if (!(p->seg_value[k] > 0.0) || !std::isfinite(p->seg_value[k]))
+            return fail(TSW_ERR_ARG, "segment %d depth %g must be > 0 (P:165)", k, p->seg_value[k]);
+    for (int k = 1; k + 1 < p->nseg; ++k)
+        if (!(p->seg_break[k] > p->seg_break[k - 1])) return fail(TSW_ERR_ARG, "breaks must increase");
+    for (int k = 0; k < p->nsing; ++k) {
+        if (!(p->sing_amp[k] >= 0.0) || !std::isfinite(p->sing_amp[k]) || !std::isfinite(p->sing_loc[k]))
+            return fail(TSW_ERR_ARG, "singular term %d: amplitude must be >= 0", k);
+        if (p->sing_order[k] != 1 && p->sing_order[k] != 2) return fail(TSW_ERR_ARG, "singular order must be 1 or 2");
+    }
+    std::vector<double> ev(eps, eps + c->g.batch), sc(size_t(c->g.batch), 1.0);
+    if (scale) sc.assign(scale, scale + c->g.batch);
+    for (int b = 0; b < c->g.batch; ++b) {
+        if (!(ev[b] > 0.0 && ev[b] <= 1.0)) return fail(TSW_ERR_ARG, "eps[%d] = %g outside (0, 1] (P:335)", b, ev[b]);
+        if (!(sc[b] >= 0.0) || !std::isfinite(sc[b])) return fail(TSW_ERR_ARG, "scale[%d] must be >= 0", b);
+    }
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    if ((st = alloc_coeff(c, MODE_LINE))) return st;
+    std::vector<double> data;
+    data.insert(data.end(), p->seg_value, p->seg_value + p->nseg);
+    if (p->nseg > 1) data.insert(data.end(), p->seg_break, p->seg_break + p->nseg - 1);
+    data.insert(data.end(), p->sing_loc, p->sing_loc + p->nsing);
+    data.insert(data.end(), p->sing_amp, p->sing_amp + p->nsing);
+    for (int k = 0; k < p->nsing; ++k) data.push_back(double(p->sing_order[k]));
+    double* d_data = nullptr;
+    CK(cudaMalloc(&d_data, std::max<size_t>(1, data.size()) * sizeof(double)));
+    CK(cudaMemcpy(d_data, data.data(), data.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(c->d_eps, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_amp, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
+    ProfileArgs a;
+    a.nseg = p->nseg;
+    a.nsing = p->nsing;
+    a.isotropic = p->isotropic;
+    a.data = d_data;
+    a.eps = c->d_eps;
+    a.scale = c->d_amp;
+    a.nx = c->g.nx;
+    a.cpitch = c->cstride1;
+    a.dx = c->g.dx;
+    dim3 grid(unsigned(grid_for(c->cstride1, 128, 4 * c->sm_count)), unsigned(c->g.batch));
+    k_coeff_profile<<<grid, 128, 0, c->stream>>>(a, c->h1, c->h2);
+    cudaError_t e = cudaGetLastError();
+    cudaError_t e2 = cudaStreamSynchronize(c->stream);
+    cudaFree(d_data);
+    if (e != cudaSuccess || e2 != cudaSuccess)
+        return fail(TSW_ERR_CUDA, "k_coeff_profile: %s", cudaGetErrorString(e != cudaSuccess ? e : e2));
+    c->launches++;
+    c->kind = TSW_H_PROFILE_X;
+    // A₂ (R18) measures left of the first singular term, else of the first jump
+    c->xs = p->nsing > 0 ? p->sing_loc[0] : (p->nseg > 1 ? p->seg_break[0] : 0.0);
+    c->ys = 0.0;
+    c->have_eps = true;
+    if ((st = check_faces(c))) return st;
+    c->have_coeff = true;
+    c->have_init = false;
+    return TSW_OK;
+}
+
 tsw_status tsw_set_coeff_faces(tsw_ctx* c, const double* h1, const double* h2, int on_device) {
     if (!c || !h1) return fail(TSW_ERR_ARG, "NULL argument");
     if (c->g.dim == 2 && !h2) return fail(TSW_ERR_ARG, "h2 is required in 2D");
@@ -920,8 +985,8 @@ tsw_status tsw_set_coeff_faces(tsw_ctx* c, const double* h1, const double* h2, i
     if (c->g.dim == 1) {
         CK(cudaMemcpy2DAsync(c->h1, c->cstride1 * sizeof(double), h1, (nx - 1) * sizeof(double), (nx - 1) * sizeof(double),
                              B, kind, c->stream));
-        std::vector<double> hb(B, 1.0);
-        CK(cudaMemcpyAsync(c->h2, hb.data(), B * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        std::vector<double> hb(B * c->cstride2, 1.0);  // unused in 1D (no y faces)
+        CK(cudaMemcpy(c->h2, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice));
     } else {
         CK(cudaMemsetAsync(c->h1, 0, B * c->cstride1 * sizeof(double), c->stream));
         CK(cudaMemsetAsync(c->h2, 0, B * c->cstride2 * sizeof(double), c->stream));
@@ -951,9 +1016,9 @@ tsw_status tsw_read_faces(tsw_ctx* c, double* h1, double* h2) {
     if (st) return st;
     const size_t B = size_t(c->g.batch), nx = size_t(c->g.nx), rows = size_t(c->ny_local);
     if (c->mode == MODE_LINE) {
-        std::vector<double> line(B * c->cstride1), hy(B);
+        std::vector<double> line(B * c->cstride1), hy(B * c->cstride2);
         CK(cudaMemcpyAsync(line.data(), c->h1, line.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(hy.data(), c->h2, B * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hy.data(), c->h2, hy.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         const size_t nrow = (c->g.dim == 1) ? 1 : rows;
         for (size_t b = 0; b < B; ++b)
@@ -964,7 +1029,7 @@ tsw_status tsw_read_faces(tsw_ctx* c, double* h1, double* h2) {
                 for (size_t k = 0; k <= rows; ++k) {
                     const int64_t g = c->r0 + int64_t(k) - 1;
                     for (size_t i = 0; i < nx; ++i)
-                        h2[(b * (rows + 1) + k) * nx + i] = (g >= 0 && g <= c->g.ny - 2) ? hy[b] : 0.0;
+                        h2[(b * (rows + 1) + k) * nx + i] = (g >= 0 && g <= c->g.ny - 2) ? hy[b * c->cstride2 + i] : 0.0;
                 }
         return TSW_OK;
     }

@@ -182,3 +182,66 @@ def slab_rows(ny: int, rank: int, nranks: int) -> tuple:
     r0 = rank * base + min(rank, rem)
     r1 = r0 + base + (1 if rank < rem else 0)
     return r0, r1
+
+
+# ---------------------------------------------------------------------------------------------
+# The paper's own scenarios, in the centred coordinates of R9: the paper's
+# domain [0, 100] is x + 50 here, so its jump at 75 is at x = 25, its δ at 70 is at x = 20.
+# ---------------------------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class Scenario:
+    """A depth profile + data of PAPER.md §3 (configuration only — no arithmetic of the method)."""
+    name: str
+    dim: int
+    nx: int
+    ny: int
+    dx: float
+    seg_value: List[float]
+    seg_break: List[float]
+    sing_loc: List[float]
+    sing_amp: List[float]
+    sing_order: List[int]
+    isotropic: bool
+    eps: List[float]
+    scale: List[float]
+    T: float
+    data: str           # "gauss1d" | "lorentz" | "gauss2d"
+    e: float = 0.0      # Lorentzian width
+
+    @property
+    def batch(self) -> int:
+        return len(self.eps)
+
+    def initial(self) -> np.ndarray:
+        x = node_coords(self.nx, self.dx)
+        if self.data == "gauss1d":      # P:809 u0 = 40 exp(−(x−40)²/8)  (x_paper = x + 50)
+            return zero_boundary(40.0 * np.exp(-((x + 10.0) ** 2) / 8.0), 1)
+        if self.data == "lorentz":      # P:1091 u0 = e/((x−60)² + e²)
+            return zero_boundary(self.e / ((x - 10.0) ** 2 + self.e ** 2), 1)
+        if self.data == "gauss2d":      # P:1156 u0 = 50 exp(−((x−40)² + (y−50)²)/8)
+            y = node_coords(self.ny, self.dx)
+            u = 50.0 * np.exp(-(((x[None, :] + 10.0) ** 2) + y[:, None] ** 2) / 8.0)
+            return zero_boundary(u, 2)
+        raise ValueError(self.data)
+
+
+def paper_case(case: str, eps: float = 0.2, data: str = "gauss1d", e: float = 0.1, T: float = 5.0,
+               dx: float = 0.005, amp: float = 1.0) -> Scenario:
+    """PAPER.md §3.1 / §3.2.3, 1D on [0, 100] (dx = 0.005 as P:821 ⇒ 20001 nodes).
+
+    case "1": h_0 = 100 on [0,75), 10 on [75,100] (eq. (h2case), P:758–769);
+    case "2": h_0 + amp·δ(x−70) (P:773–780; amp = 100 is §3.2.3's singular type I);
+    case "3": h_0 + amp·δ²(x−70) (amp = 100 is §3.2.3's singular type II).
+    """
+    nx = int(round(100.0 / dx)) + 1
+    sing = {"1": ([], [], []), "2": ([20.0], [amp], [1]), "3": ([20.0], [amp], [2])}[case]
+    return Scenario(f"paper_case{case}_{data}", 1, nx, 1, dx, [100.0, 10.0], [25.0], sing[0], sing[1], sing[2],
+                    False, [eps], [1.0], T, data, e)
+
+
+def paper_2d(eps: float = 0.8, dx: float = 0.05, T: float = 5.0) -> Scenario:
+    """PAPER.md §3.3: H(x, y) = h_0(x) isotropic, Gaussian u0, ε = 0.8 (Fig. 6)."""
+    n = int(round(100.0 / dx)) + 1
+    return Scenario("paper_2d_H_h0", 2, n, n, dx, [100.0, 10.0], [25.0], [], [], [], True, [eps], [1.0], T,
+                    "gauss2d")

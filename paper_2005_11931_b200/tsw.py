@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_PKG, "libtsw.so")
 
 TSW_OK, TSW_ERR_ARG, TSW_ERR_CFL, TSW_ERR_STATE, TSW_ERR_CUDA, TSW_ERR_NCCL, TSW_ERR_OOM, TSW_ERR_UNSTABLE = range(8)
 TSW_F32, TSW_F64 = 0, 1
-TSW_H_CONST, TSW_H_DELTA_LINE_X, TSW_H_DELTA_POINT, TSW_H_FACES = range(4)
+TSW_H_CONST, TSW_H_DELTA_LINE_X, TSW_H_DELTA_POINT, TSW_H_FACES, TSW_H_PROFILE_X = range(5)
 TSW_ALLOW_UNSTABLE = 1
 TSW_INIT_SHARED = 2
 TSW_OPT_ROWS_PER_ITEM = 1
@@ -33,7 +33,7 @@ STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STA
                 5: "TSW_ERR_NCCL", 6: "TSW_ERR_OOM", 7: "TSW_ERR_UNSTABLE"}
 
 # every symbol include/tsw.h declares (tests check the library exports all of them)
-EXPORTS = ["tsw_create", "tsw_destroy", "tsw_set_coeff", "tsw_set_coeff_faces", "tsw_read_faces", "tsw_set_initial", "tsw_step",
+EXPORTS = ["tsw_create", "tsw_destroy", "tsw_set_coeff", "tsw_set_coeff_faces", "tsw_set_coeff_profile", "tsw_read_faces", "tsw_set_initial", "tsw_step",
            "tsw_group_step", "tsw_energy", "tsw_wave2", "tsw_read", "tsw_set_state", "tsw_info", "tsw_sync",
            "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
            "tsw_version"]
@@ -50,6 +50,13 @@ class tsw_grid_desc(ctypes.Structure):
                 ("dx", ctypes.c_double), ("dy", ctypes.c_double), ("batch", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+
+
+class tsw_profile_desc(ctypes.Structure):
+    _fields_ = [("nseg", ctypes.c_int32), ("seg_value", ctypes.POINTER(ctypes.c_double)),
+                ("seg_break", ctypes.POINTER(ctypes.c_double)), ("nsing", ctypes.c_int32),
+                ("sing_loc", ctypes.POINTER(ctypes.c_double)), ("sing_amp", ctypes.POINTER(ctypes.c_double)),
+                ("sing_order", ctypes.POINTER(ctypes.c_int32)), ("isotropic", ctypes.c_int32)]
 
 
 class tsw_coeff_desc(ctypes.Structure):
@@ -77,6 +84,7 @@ def load(path: Optional[str] = None):
         "tsw_destroy": (None, [vp]),
         "tsw_set_coeff": (i32, [vp, ctypes.POINTER(tsw_coeff_desc)]),
         "tsw_set_coeff_faces": (i32, [vp, vp, vp, i32]),
+        "tsw_set_coeff_profile": (i32, [vp, ctypes.POINTER(tsw_profile_desc), vp, vp]),
         "tsw_read_faces": (i32, [vp, vp, vp]),
         "tsw_set_initial": (i32, [vp, vp, vp, d, i32, u32]),
         "tsw_step": (i32, [vp, i64]),
@@ -156,6 +164,27 @@ def tsw_set_coeff(ctx, kind: int, eps: Sequence[float], h_background: float = 1.
                           ctypes.cast(e, ctypes.POINTER(ctypes.c_double)),
                           None if a is None else ctypes.cast(a, ctypes.POINTER(ctypes.c_double)))
     _check(load().tsw_set_coeff(ctx, ctypes.byref(desc)), ctx)
+
+
+def _dbl(vals):
+    vals = list(vals)
+    return (ctypes.c_double * max(1, len(vals)))(*vals)
+
+
+def tsw_set_coeff_profile(ctx, seg_value: Sequence[float], seg_break: Sequence[float], eps: Sequence[float],
+                          sing_loc: Sequence[float] = (), sing_amp: Sequence[float] = (),
+                          sing_order: Sequence[int] = (), isotropic: bool = False,
+                          scale: Optional[Sequence[float]] = None) -> None:
+    sv, sb, sl, sa = _dbl(seg_value), _dbl(seg_break), _dbl(sing_loc), _dbl(sing_amp)
+    so = (ctypes.c_int32 * max(1, len(sing_order)))(*list(sing_order))
+    P = ctypes.POINTER(ctypes.c_double)
+    desc = tsw_profile_desc(len(seg_value), ctypes.cast(sv, P), ctypes.cast(sb, P), len(sing_loc),
+                            ctypes.cast(sl, P), ctypes.cast(sa, P), ctypes.cast(so, ctypes.POINTER(ctypes.c_int32)),
+                            int(bool(isotropic)))
+    e = _dbl(eps)
+    sc = None if scale is None else _dbl(scale)
+    _check(load().tsw_set_coeff_profile(ctx, ctypes.byref(desc), ctypes.cast(e, ctypes.c_void_p),
+                                        None if sc is None else ctypes.cast(sc, ctypes.c_void_p)), ctx)
 
 
 def tsw_set_coeff_faces(ctx, h1, h2=None) -> None:
@@ -299,6 +328,11 @@ class Solver:
 
     def set_coeff(self, kind, eps, h_background=1.0, amp=1.0, order=1, xs=0.0, ys=0.0, amp_per_member=None):
         tsw_set_coeff(self.ctx, kind, list(eps), h_background, amp, order, xs, ys, amp_per_member)
+
+    def set_coeff_profile(self, seg_value, seg_break, eps, sing_loc=(), sing_amp=(), sing_order=(),
+                          isotropic=False, scale=None):
+        tsw_set_coeff_profile(self.ctx, seg_value, seg_break, list(eps), sing_loc, sing_amp, sing_order,
+                              isotropic, scale)
 
     def set_coeff_faces(self, h1, h2=None):
         tsw_set_coeff_faces(self.ctx, h1, h2)

@@ -1,0 +1,126 @@
+"""Pins for the paper's own scenarios in the oracle (-m "not gpu").
+
+* Φ, the mollifier's primitive: against 40-digit mpmath quadrature, Φ(0) = ½,
+  Φ(t) + Φ(−t) = 1, Φ′ = φ.
+* The regularised discontinuous depth (PAPER.md eq. (h2case)) and Cases 2–3
+  (P:773–789): SPEC S:545's locality/midpoint checks, h_{1,ε}(70) = h_{0,ε}(70) + φ_ε(0).
+* The paper's own statement about the reflected wave (§3.2.3): "In all cases the second
+  wave is smaller in size. The reflected wave has only one positive component in Case I, while
+  it has both positive and negative parts in Cases II and III" — checked on leapfrog runs of the
+  paper's §3.2.3 set-up (Lorentzian u0, e ∈ {0.5, 0.3, 0.1}, ε = 0.2, 100δ / 100δ²).
+"""
+import math
+
+import mpmath
+import numpy as np
+import pytest
+
+import oracle
+from paper_2005_11931_b200 import inputs
+
+mpmath.mp.dps = 40
+C_MP = 1 / mpmath.quad(lambda x: mpmath.exp(1 / (x * x - 1)), [-1, 0, 1])
+
+
+def _Phi_mp(t):
+    return float(C_MP * mpmath.quad(lambda x: mpmath.exp(1 / (x * x - 1)), [-1, t]))
+
+
+def test_primitive_against_mpmath_and_symmetry():
+    ts = np.linspace(-0.999, 0.999, 37)
+    got = oracle.mollifier_primitive(ts)
+    ref = np.array([_Phi_mp(t) for t in ts])
+    assert np.max(np.abs(got - ref)) < 2e-15
+    assert oracle.mollifier_primitive([-1.0, -3.0])[0] == 0.0
+    assert np.all(oracle.mollifier_primitive([1.0, 7.0]) == 1.0)
+    assert abs(oracle.mollifier_primitive([0.0])[0] - 0.5) < 1e-15
+    np.testing.assert_allclose(oracle.mollifier_primitive(ts) + oracle.mollifier_primitive(-ts), 1.0, atol=2e-15)
+    # Φ′ = φ (central difference)
+    h = 1e-5
+    for t in (-0.7, -0.2, 0.0, 0.45):
+        d = (oracle.mollifier_primitive([t + h])[0] - oracle.mollifier_primitive([t - h])[0]) / (2 * h)
+        assert abs(d - oracle.phi_eps([t], 1.0)[0]) < 1e-8
+
+
+def test_case1_profile_locality_and_midpoint():
+    """SPEC S:545 (PAPER eq. (h2case)): ε = 0.2 ⇒ h_ε(50) = 100, h_ε(90) = 10 exactly, h_ε(75) = 55."""
+    sc = inputs.paper_case("1")
+    P = oracle.Profile(sc.seg_value, sc.seg_break)
+    # paper coordinates x_p = x + 50
+    assert P.eval([0.0], 0.2)[0] == 100.0
+    assert P.eval([40.0], 0.2)[0] == 10.0
+    assert abs(P.eval([25.0], 0.2)[0] - 55.0) < 1e-12
+    xs = np.linspace(24.7, 25.3, 61)
+    v = P.eval(xs, 0.2)
+    assert np.all(np.diff(v) <= 0.0)                          # monotone across the jump
+    assert np.all(v[xs <= 24.8 - 1e-9] == 100.0) and np.all(v[xs >= 25.2 + 1e-9] == 10.0)
+    # the convolution with φ_ε of a step is the primitive (closed form of h_0 * φ_ε)
+    for xp in (24.9, 25.05, 25.17):
+        ref = 100.0 + (10.0 - 100.0) * _Phi_mp((xp - 25.0) / 0.2)
+        assert abs(P.eval([xp], 0.2)[0] - ref) < 1e-12
+
+
+def test_case2_case3_singular_terms():
+    """P:779 h_{1,ε} = h_{0,ε} + φ_ε(x−70); P:787 h_{2,ε} = h_{0,ε} + φ_ε²(x−70); S:87 ≈ 104.14."""
+    c2 = inputs.paper_case("2")
+    c3 = inputs.paper_case("3")
+    P2 = oracle.Profile(c2.seg_value, c2.seg_break, c2.sing_loc, c2.sing_amp, c2.sing_order)
+    P3 = oracle.Profile(c3.seg_value, c3.seg_break, c3.sing_loc, c3.sing_amp, c3.sing_order)
+    peak = float(C_MP) * math.exp(-1.0) / 0.2
+    assert abs(P2.eval([20.0], 0.2)[0] - (100.0 + peak)) < 1e-12
+    assert abs(P2.eval([20.0], 0.2)[0] - 104.14) < 5e-3         # SPEC S:87 example
+    assert abs(P3.eval([20.0], 0.2)[0] - (100.0 + peak * peak)) < 1e-11
+    xs = np.array([19.7, 19.9, 20.1, 20.3])
+    np.testing.assert_allclose(P2.eval(xs, 0.2) - 100.0, oracle.phi_eps(xs - 20.0, 0.2), rtol=1e-14, atol=0)
+
+
+def _reflected_components(sc, e):
+    """Leapfrog run of §3.2.3's set-up to t = 2.5; the wave between the left-going main pulse and
+    the singular point: sign components above 1 % of the main pulse (SPEC S:354's threshold)."""
+    sc = inputs.paper_case(sc, data="lorentz", e=e, amp=100.0)
+    P = oracle.Profile(sc.seg_value, sc.seg_break, sc.sing_loc, sc.sing_amp, sc.sing_order)
+    h1, _ = oracle.build_faces_profile(1, P, sc.eps[0], sc.nx, 1, sc.dx)
+    dt = 0.9 * oracle.gershgorin_dt_max(1, h1, None, sc.dx, sc.dx)
+    T = 2.5
+    n = int(math.ceil(T / dt))
+    dt = T / n
+    c1 = oracle.prescale(h1, dt, sc.dx, np.float64)
+    un, _ = oracle.run(1, c1, None, sc.initial(), None, dt, n)
+    x = inputs.node_coords(sc.nx, sc.dx)
+    main = np.max(np.abs(un[(x > -20.0) & (x < -10.0)]))     # left-going half of u0 (x_p ≈ 35)
+    r = un[(x > -5.0) & (x < 19.5)]                          # between it and x_p = 70
+    thr = 0.01 * main
+    signs, prev = [], 0
+    for v in np.where(r > thr, 1, np.where(r < -thr, -1, 0)):
+        if v != 0 and v != prev:
+            signs.append(int(v))
+        if v != 0:
+            prev = v
+    return main, r, signs
+
+
+@pytest.mark.parametrize("e", [0.5, 0.3, 0.1])
+def test_paper_reflected_wave_structure(e):
+    # Case I (discontinuous h_0): one positive component
+    main, r, signs = _reflected_components("1", e)
+    assert signs == [1]
+    assert np.max(np.abs(r)) < main                          # "the second wave is smaller in size"
+    # Cases II and III (100δ, 100δ²): both positive and negative parts
+    for case in ("2", "3"):
+        main, r, signs = _reflected_components(case, e)
+        assert 1 in signs and -1 in signs
+        assert np.max(np.abs(r)) < main
+
+
+def test_profile_faces_2d_isotropic_and_vector():
+    sc = inputs.paper_2d(dx=0.5)
+    P = oracle.Profile([100.0, 10.0], [25.0], [20.0], [3.0], [1], isotropic=True)
+    h1, h2 = oracle.build_faces_profile(2, P, 0.8, sc.nx, sc.ny, sc.dx)
+    x_nodes = inputs.node_coords(sc.nx, sc.dx)
+    x_faces = ((2 * np.arange(sc.nx - 1) + 2 - sc.nx) * sc.dx) / 2
+    assert np.all(h1 == h1[0]) and np.all(h2 == h2[0])       # x-only
+    np.testing.assert_array_equal(h1[0], P.eval(x_faces, 0.8))
+    np.testing.assert_array_equal(h2[0], P.eval(x_nodes, 0.8))
+    Pv = oracle.Profile([100.0, 10.0], [25.0], [20.0], [3.0], [1], isotropic=False)
+    _, h2v = oracle.build_faces_profile(2, Pv, 0.8, sc.nx, sc.ny, sc.dx)
+    np.testing.assert_array_equal(h2v[0], Pv.eval(x_nodes, 0.8, with_sing=False))
