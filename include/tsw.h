@@ -166,6 +166,25 @@ tsw_status tsw_energy(tsw_ctx* ctx, double* out_B);
  *   out_B2: host double[batch][2]; argidx_B2: host int64[batch][2] (may be NULL). */
 tsw_status tsw_wave2(tsw_ctx* ctx, int32_t bg_member, double* out_B2, int64_t* argidx_B2);
 
+/* ---- ε-family diagnostics -------------------------------------------- */
+
+/* Pairwise L² distances of the members at the current level (§3.2.1, P:831–838:
+ * ‖u_{ε1}(t,·) − u_{ε2}(t,·)‖_{L²}, the ε → 0 limit study of the very weak solution net):
+ *   out_BB[i][j] = sqrt(dx·dy · Σ_nodes (u_i − u_j)²)   (1D: dx), symmetric, zero diagonal,
+ * summed over ranks.  out_BB: host double[batch][batch]; batch ≤ 200.  Synchronises. */
+tsw_status tsw_family_l2(tsw_ctx* ctx, double* out_BB);
+
+/* The L² quantities of Theorem "lem 1" (energy estimate) at the current level:
+ * out_B4[b] = { ‖u^n‖, ‖(u^n − u^{n−1})/dt‖ (0 at n = 0), ‖∂x u^n‖, ‖∂y u^n‖ } with forward
+ * differences over all faces and the rectangle rule (weight dx·dy; 1D: dx).  Synchronises. */
+tsw_status tsw_field_norms(tsw_ctx* ctx, double* out_B4);
+
+/* W^{1,∞} norms of the regularised depth (Assumption eq. (assum coeff), P:344–345:
+ * ‖h_ε‖_{W^{1,∞}} ≲ ε^{−N0}): out_B3[b] = { sup |h1| over the x faces, sup |∇h_ε| at the x faces
+ * (analytic derivative of the regulariser for the δ-line, δ-point and profile kinds; a finite
+ * difference of the faces for TSW_H_FACES), sup |h2| over the y faces (0 in 1D) }.  Synchronises. */
+tsw_status tsw_coeff_norms(tsw_ctx* ctx, double* out_B3);
+
 /* Copy a level of this rank's slab out: which = 0 ⇒ u^n, 1 ⇒ u^{n−1}; dst is [batch][ny_local][nx]
  * in the ctx dtype, host (to_device = 0, synchronous) or device (to_device = 1, stream-ordered). */
 tsw_status tsw_read(tsw_ctx* ctx, int32_t which, void* dst, int32_t to_device);

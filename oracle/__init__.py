@@ -307,3 +307,57 @@ def window_value(cfg, member: int, dtype, nsteps: int, samples: Sequence[Tuple[i
         un, _ = run(2, c1, c2, u0, None, cfg.dt, nsteps)
         out[k] = un[j - j0, i - i0]
     return out
+
+
+# --- NEXT 2: ε-family diagnostics (definitions written out, numpy fp64) ------------------------
+
+def family_l2(U: np.ndarray, w: float) -> np.ndarray:
+    """‖u_i − u_j‖_{L²} = sqrt(w·Σ (u_i − u_j)²) for every pair of members."""
+    U = np.asarray(U, dtype=np.float64).reshape(U.shape[0], -1)
+    B = U.shape[0]
+    D = np.zeros((B, B))
+    for i in range(B):
+        for j in range(i + 1, B):
+            D[i, j] = D[j, i] = np.sqrt(w * np.sum((U[i] - U[j]) ** 2))
+    return D
+
+
+def field_norms(dim: int, un: np.ndarray, unm1: np.ndarray, dx: float, dy: float, dt: float) -> np.ndarray:
+    """Theorem lem 1's L² quantities: ‖u‖, ‖(u^n − u^{n−1})/dt‖, ‖∂x u‖, ‖∂y u‖
+    (forward differences over all faces, rectangle rule)."""
+    u = np.asarray(un, dtype=np.float64)
+    p = np.asarray(unm1, dtype=np.float64)
+    w = dx if dim == 1 else dx * dy
+    out = [np.sqrt(w * np.sum(u * u)), np.sqrt(w * np.sum((u - p) ** 2)) / dt,
+           np.sqrt(w * np.sum(np.diff(u, axis=-1) ** 2)) / dx]
+    out.append(np.sqrt(w * np.sum(np.diff(u, axis=0) ** 2)) / dy if dim == 2 else 0.0)
+    return np.array(out)
+
+
+def dphi_eps(d, eps: float) -> np.ndarray:
+    """φ_ε′(d) = φ_ε(d)·(−2t/((t²−1)²·ε)), t = d/ε (derivative of P:745–750's φ_ε)."""
+    d = np.atleast_1d(np.asarray(d, dtype=np.float64))
+    t = d / eps
+    out = np.zeros_like(d)
+    m = np.abs(t) < 1.0
+    out[m] = phi_eps(d[m], eps) * (-2.0 * t[m] / ((t[m] ** 2 - 1.0) ** 2 * eps))
+    return out
+
+
+def profile_derivative(prof: "Profile", x, eps: float, sing_scale: float = 1.0) -> np.ndarray:
+    """h_ε′(x) = Σ_k (v_k − v_{k−1}) φ_ε(x − b_k) + Σ_j s·A_j·(φ_ε^{o_j})′(x − x_j)  (Φ′ = φ)."""
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    d = np.zeros_like(x)
+    for k in range(1, prof.nseg):
+        d += (prof.seg_value[k] - prof.seg_value[k - 1]) * phi_eps(x - prof.seg_break[k - 1], eps)
+    for j in range(prof.nsing):
+        p, q = phi_eps(x - prof.sing_loc[j], eps), dphi_eps(x - prof.sing_loc[j], eps)
+        d += sing_scale * prof.sing_amp[j] * (2.0 * p * q if prof.sing_order[j] == 2 else q)
+    return d
+
+
+def moderateness_exponent(eps_list, norms) -> float:
+    """Least-squares slope N of log‖h_ε‖_{W^{1,∞}} against log(1/ε) (Assumption)."""
+    x = np.log(1.0 / np.asarray(eps_list, dtype=np.float64))
+    y = np.log(np.asarray(norms, dtype=np.float64))
+    return float(np.polyfit(x, y, 1)[0])

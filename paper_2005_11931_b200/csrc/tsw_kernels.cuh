@@ -964,6 +964,234 @@ __global__ void k_wave2_final(const ArgVal* __restrict__ partial, int nblk, doub
 }
 
 // ------------------------------------------------------------------------------------------
+// NEXT 2 diagnostics of an ε-family: pairwise L² distances (§3.2.1,
+// P:831–838 ‖u_{ε1}(t) − u_{ε2}(t)‖_{L²}), the L² pieces of Theorem lem 1's energy estimate
+// and the W^{1,∞} norms of the regularised depth (Assumption).
+// ------------------------------------------------------------------------------------------
+// Pairwise Σ_nodes (u_i − u_j)²: a CTA stages TN consecutive nodes of one row of ALL members in
+// shared memory; each thread owns a 4×4 block of member pairs (register blocking: 8 loads for 16
+// differences).  Partial sums per CTA, summed in a fixed order by k_family_final.
+constexpr int FAM_TN = 64;
+struct FamilyArgs {
+    const void* u;
+    int64_t nx, pitch, mstride;
+    int32_t rows;      // rows of the slab (1D: 1)
+    int32_t row0;      // first storage row (2D: 1, 1D: 0)
+    int32_t B, nblk;   // members, member blocks of 4
+    int64_t tiles_per_row;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_family_l2(const FamilyArgs a, double* __restrict__ partial) {
+    extern __shared__ __align__(16) double tile[];  // [B][FAM_TN + 1]
+    const int npairs = a.nblk * (a.nblk + 1) / 2;
+    double acc[4][4];
+    // this thread's block pair (I ≤ J); threads beyond npairs only help loading
+    int I = 0, J = 0;
+    const bool owner = threadIdx.x < npairs;
+    if (owner) {
+        int p = threadIdx.x, row = 0;
+        while (p >= a.nblk - row) { p -= a.nblk - row; ++row; }
+        I = row;
+        J = row + p;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc[k][l] = 0.0;
+    const T* U = static_cast<const T*>(a.u);
+    const int64_t ntiles = int64_t(a.rows) * a.tiles_per_row;
+    for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
+        const int64_t r = a.row0 + tile_id / a.tiles_per_row;
+        const int64_t c0 = (tile_id % a.tiles_per_row) * FAM_TN;
+        __syncthreads();
+        for (int e = threadIdx.x; e < a.B * FAM_TN; e += blockDim.x) {
+            const int m = e / FAM_TN, cc = e % FAM_TN;
+            const int64_t col = c0 + cc;
+            tile[m * (FAM_TN + 1) + cc] = (col < a.nx) ? (double)U[m * a.mstride + r * a.pitch + col] : 0.0;
+        }
+        __syncthreads();
+        if (owner) {
+            for (int n = 0; n < FAM_TN; ++n) {
+                double x[4], y[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = 4 * I + k, j = 4 * J + k;
+                    x[k] = (i < a.B) ? tile[i * (FAM_TN + 1) + n] : 0.0;
+                    y[k] = (j < a.B) ? tile[j * (FAM_TN + 1) + n] : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        const double d = x[k] - y[l];
+                        acc[k][l] += d * d;
+                    }
+            }
+        }
+    }
+    if (owner) {
+        double* out = partial + size_t(blockIdx.x) * a.B * a.B;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int i = 4 * I + k, j = 4 * J + l;
+                if (i < a.B && j < a.B && i < j) out[i * a.B + j] = acc[k][l];
+            }
+    }
+}
+
+// out[i][j] = out[j][i] = sqrt(w · Σ_cta partial[cta][i][j]) (fixed order), diagonal 0.
+__global__ void k_family_final(const double* __restrict__ partial, int ncta, int B, double w, double* __restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B * B; e += gridDim.x * blockDim.x) {
+        const int i = e / B, j = e % B;
+        if (i >= j) continue;
+        double s = 0.0;
+        for (int k = 0; k < ncta; ++k) s += partial[size_t(k) * B * B + e];
+        const double v = sqrt(w * s);
+        out[i * B + j] = v;
+        out[j * B + i] = v;
+    }
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < B; i += blockDim.x) out[i * B + i] = 0.0;
+}
+
+// Σ u², Σ (u − u_prev)², Σ (Δx u)², Σ (Δy u)² per member (all nodes / all faces of the slab).
+struct NormArgs {
+    int dim;
+    const void* un;
+    const void* unm1;
+    int64_t nx, ny, r0, pitch, mstride;
+    int32_t rows;
+    int nblk;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_norms(const NormArgs a, double* __restrict__ partial) {
+    const int b = blockIdx.y;
+    const T* A = static_cast<const T*>(a.un) + b * a.mstride;
+    const T* P = static_cast<const T*>(a.unm1) + b * a.mstride;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t total = int64_t(a.rows) * a.nx;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k % a.nx;
+        const int64_t sr = (a.dim == 1) ? 0 : 1 + k / a.nx;
+        const int64_t g = (a.dim == 1) ? 0 : a.r0 + sr - 1;
+        const int64_t o = sr * a.pitch + i;
+        const double u = (double)A[o], p = (double)P[o];
+        s[0] += u * u;
+        s[1] += (u - p) * (u - p);
+        if (i <= a.nx - 2) {
+            const double d = (double)A[o + 1] - u;
+            s[2] += d * d;
+        }
+        if (a.dim == 2 && g <= a.ny - 2) {
+            const double d = (double)A[o + a.pitch] - u;
+            s[3] += d * d;
+        }
+    }
+    __shared__ double red[4][8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double v = warp_sum(s[q]);
+        if (lane == 0) red[q][w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double v = 0.0;
+        for (int k = 0; k < int(blockDim.x >> 5); ++k) v += red[threadIdx.x][k];
+        partial[(size_t(b) * a.nblk + blockIdx.x) * 4 + threadIdx.x] = v;
+    }
+}
+
+__global__ void k_norms_final(const double* __restrict__ partial, int nblk, int B, double* __restrict__ out) {
+    const int b = blockIdx.x, q = threadIdx.x;
+    if (q >= 4) return;
+    double v = 0.0;
+    for (int k = 0; k < nblk; ++k) v += partial[(size_t(b) * nblk + k) * 4 + q];
+    out[b * 4 + q] = v;
+}
+
+// W^{1,∞}: sup |h| over all stored faces and sup |∇h| from the analytic derivative of the
+// regulariser at the x faces (φ_ε′(d) = φ_ε(d)·(−2t/((t²−1)²·ε)), t = d/ε).
+__device__ __forceinline__ double dphi_eps(double d, double eps) {
+    const double t = d / eps;
+    if (!(fabs(t) < 1.0)) return 0.0;
+    const double q = t * t - 1.0;
+    return phi_eps(d, eps) * (-2.0 * t / (q * q * eps));
+}
+
+struct CoeffNormArgs {
+    int kind, order;
+    double hb, xs, ys, dx, dy;
+    const double* eps;
+    const double* amp;     // δ kinds: amplitude per member; profile: scale per member
+    const double* prof;    // profile data (kind 4) or nullptr
+    int nseg, nsing;
+    const double* h1;
+    const double* h2;
+    int64_t nx, ny, r0, rows, pitch, cstride1, cstride2, mstride;
+    int mode;
+};
+
+__global__ void k_coeff_norms(const CoeffNormArgs a, unsigned long long* __restrict__ out /* [B][3] */) {
+    const int b = blockIdx.y;
+    const double eps = a.eps[b], am = a.amp[b];
+    double mh = 0.0, md = 0.0, mh2 = 0.0;
+    const int64_t nrow = (a.mode == MODE_LINE) ? 1 : a.rows;
+    const int64_t total = nrow * a.nx;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k % a.nx;
+        const int64_t sr = (a.mode == MODE_LINE) ? 0 : 1 + k / a.nx;
+        if (i <= a.nx - 2) {
+            const double h = (a.mode == MODE_LINE) ? a.h1[b * a.cstride1 + i] : a.h1[b * a.cstride1 + sr * a.pitch + i];
+            mh = fmax(mh, fabs(h));
+            const double x = grid_face(i, a.nx, a.dx);
+            double d = 0.0;
+            if (a.kind == 1) {
+                const double p = phi_eps(x - a.xs, eps), q = dphi_eps(x - a.xs, eps);
+                d = am * ((a.order == 2) ? 2.0 * p * q : q);
+            } else if (a.kind == 2) {
+                const double y = grid_node(a.r0 + sr - 1, a.ny, a.dy);
+                const double px = phi_eps(x - a.xs, eps), py = phi_eps(y - a.ys, eps);
+                const double gx = dphi_eps(x - a.xs, eps) * py, gy = px * dphi_eps(y - a.ys, eps);
+                const double f = (a.order == 2) ? 2.0 * px * py : 1.0;
+                d = am * f * sqrt(gx * gx + gy * gy);
+            } else if (a.kind == 4) {
+                const double* v = a.prof;
+                const double* br = v + a.nseg;
+                const double* loc = br + (a.nseg - 1);
+                const double* amp = loc + a.nsing;
+                const double* ord = amp + a.nsing;
+                for (int s = 1; s < a.nseg; ++s) d += (v[s] - v[s - 1]) * phi_eps(x - br[s - 1], eps);
+                for (int j = 0; j < a.nsing; ++j) {
+                    const double p = phi_eps(x - loc[j], eps), q = dphi_eps(x - loc[j], eps);
+                    d += am * amp[j] * ((ord[j] == 2.0) ? 2.0 * p * q : q);
+                }
+            } else if (i >= 1) {  // caller faces: finite difference at node i
+                const double* hr = a.h1 + b * a.cstride1 + ((a.mode == MODE_LINE) ? 0 : sr * a.pitch);
+                d = (hr[i] - hr[i - 1]) / a.dx;
+            }
+            md = fmax(md, fabs(d));
+        }
+        if (a.h2) {
+            const double h = (a.mode == MODE_LINE) ? a.h2[b * a.cstride2 + i] : a.h2[b * a.cstride2 + sr * a.pitch + i];
+            mh2 = fmax(mh2, fabs(h));
+        }
+    }
+    mh = warp_max(mh);
+    md = warp_max(md);
+    mh2 = warp_max(mh2);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_pos(&out[b * 3 + 0], mh);
+        atomic_max_pos(&out[b * 3 + 1], md);
+        atomic_max_pos(&out[b * 3 + 2], mh2);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // plumbing kernels
 // ------------------------------------------------------------------------------------------
 // Force the Dirichlet nodes of the slab (global rows 0 / ny−1, columns 0 / nx−1) and the padding

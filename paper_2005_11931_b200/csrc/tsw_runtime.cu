@@ -144,6 +144,12 @@ struct tsw_ctx {
     double* d_eps = nullptr;
     double* d_amp = nullptr;
     double xs = 0.0, ys = 0.0;
+    double hb = 1.0;
+    int order = 1;
+    double* d_prof = nullptr;  // profile data of TSW_H_PROFILE_X (kept for tsw_coeff_norms)
+    int prof_nseg = 0, prof_nsing = 0;
+    double* d_fam = nullptr;   // family-distance partials
+    size_t fam_cap = 0;
     bool have_eps = false;
     double dt_max = 0.0;
     // state
@@ -819,7 +825,7 @@ void tsw_destroy(tsw_ctx* c) {
     dfree_guarded(c->h2);
     dfree_guarded(c->c1);
     dfree_guarded(c->c2);
-    void* ptrs[] = {c->d_eps, c->d_amp, c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64};
+    void* ptrs[] = {c->d_eps, c->d_amp, c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64, c->d_prof, c->d_fam};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -882,6 +888,8 @@ tsw_status tsw_set_coeff(tsw_ctx* c, const tsw_coeff_desc* h) {
     c->kind = h->kind;
     c->xs = h->xs;
     c->ys = h->ys;
+    c->hb = h->h_background;
+    c->order = h->order;
     c->have_eps = true;
     if ((st = check_faces(c))) return st;
     c->have_coeff = true;
@@ -939,7 +947,10 @@ tsw_status tsw_set_coeff_profile(tsw_ctx* c, const tsw_profile_desc* p, const do
     k_coeff_profile<<<grid, 128, 0, c->stream>>>(a, c->h1, c->h2);
     cudaError_t e = cudaGetLastError();
     cudaError_t e2 = cudaStreamSynchronize(c->stream);
-    cudaFree(d_data);
+    if (c->d_prof) cudaFree(c->d_prof);
+    c->d_prof = d_data;  // kept for tsw_coeff_norms
+    c->prof_nseg = p->nseg;
+    c->prof_nsing = p->nsing;
     if (e != cudaSuccess || e2 != cudaSuccess)
         return fail(TSW_ERR_CUDA, "k_coeff_profile: %s", cudaGetErrorString(e != cudaSuccess ? e : e2));
     c->launches++;
@@ -1269,6 +1280,168 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
     for (int k = 0; k < 2 * B; ++k) {
         out_B2[k] = v[k];
         if (idx_B2) idx_B2[k] = ix[k];
+    }
+    return TSW_OK;
+}
+
+tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
+    if (!c || !out_BB) return fail(TSW_ERR_ARG, "NULL argument");
+    if (!c->have_init) return fail(TSW_ERR_STATE, "no field");
+    const int B = c->g.batch;
+    if (B > 200) return fail(TSW_ERR_ARG, "family distances support batch <= 200");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    FamilyArgs a;
+    a.u = c->buf[c->cur];
+    a.nx = c->g.nx;
+    a.pitch = c->pitch;
+    a.mstride = c->mstride;
+    a.rows = int32_t(c->g.dim == 1 ? 1 : c->ny_local);
+    a.row0 = (c->g.dim == 1) ? 0 : 1;
+    a.B = B;
+    a.nblk = (B + 3) / 4;
+    a.tiles_per_row = (c->g.nx + FAM_TN - 1) / FAM_TN;
+    if (a.nblk * (a.nblk + 1) / 2 > 256) return fail(TSW_ERR_ARG, "too many members for one CTA of pair blocks");
+    const int64_t ntiles = int64_t(a.rows) * a.tiles_per_row;
+    const int ncta = int(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * c->sm_count)));
+    const size_t need = size_t(ncta) * B * B;
+    if (c->fam_cap < need) {
+        if (c->d_fam) cudaFree(c->d_fam);
+        c->d_fam = nullptr;
+        c->fam_cap = 0;
+        CK(cudaMalloc(&c->d_fam, need * sizeof(double)));
+        c->fam_cap = need;
+    }
+    CK(cudaMemsetAsync(c->d_fam, 0, need * sizeof(double), c->stream));
+    const size_t smem = size_t(B) * (FAM_TN + 1) * sizeof(double);
+    if (smem > 48 * 1024) {
+        if (is_f64(c)) CK(cudaFuncSetAttribute(k_family_l2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        else CK(cudaFuncSetAttribute(k_family_l2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    }
+    if (is_f64(c))
+        k_family_l2<double><<<ncta, 256, smem, c->stream>>>(a, c->d_fam);
+    else
+        k_family_l2<float><<<ncta, 256, smem, c->stream>>>(a, c->d_fam);
+    CKL();
+    // root of the sums Σ (u_i − u_j)² (weight applied below); with ranks: re-square, sum, root
+    double* d_sum = nullptr;
+    CK(cudaMalloc(&d_sum, sizeof(double) * B * B));
+    k_family_final<<<std::max(1, (B * B + 255) / 256), 256, 0, c->stream>>>(c->d_fam, ncta, B, 1.0, d_sum);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && c->g.nranks > 1 && c->comm) {
+        // square, sum over ranks, take the root again on the host
+        std::vector<double> h(size_t(B) * B);
+        e = cudaMemcpyAsync(h.data(), d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        for (double& v : h) v = v * v;
+        if (e == cudaSuccess) e = cudaMemcpy(d_sum, h.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice);
+        int r = (e == cudaSuccess) ? nccl().AllReduce(d_sum, d_sum, size_t(B) * B, NCCL_F64, NCCL_SUM, c->comm, c->stream) : 0;
+        if (r != 0) {
+            cudaFree(d_sum);
+            return fail(TSW_ERR_NCCL, "family allreduce: %s", nccl().GetErrorString(r));
+        }
+        std::vector<double> g(size_t(B) * B);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g.data(), d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        for (size_t k = 0; k < g.size(); ++k) g[k] = std::sqrt(g[k]);
+        if (e == cudaSuccess) e = cudaMemcpy(d_sum, g.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_BB, d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(d_sum);
+    if (e != cudaSuccess) return fail(TSW_ERR_CUDA, "family distances: %s", cudaGetErrorString(e));
+    c->launches += 2;
+    const double w = (c->g.dim == 1) ? c->g.dx : c->g.dx * c->g.dy;
+    for (int k = 0; k < B * B; ++k) out_BB[k] *= std::sqrt(w);
+    return TSW_OK;
+}
+
+tsw_status tsw_field_norms(tsw_ctx* c, double* out_B4) {
+    if (!c || !out_B4) return fail(TSW_ERR_ARG, "NULL argument");
+    if (!c->have_init) return fail(TSW_ERR_STATE, "no field");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    NormArgs a;
+    a.dim = c->g.dim;
+    a.un = c->buf[c->cur];
+    a.unm1 = c->buf[c->cur ^ 1];
+    a.nx = c->g.nx;
+    a.ny = c->g.ny;
+    a.r0 = c->r0;
+    a.pitch = c->pitch;
+    a.mstride = c->mstride;
+    a.rows = int32_t(c->g.dim == 1 ? 1 : c->ny_local);
+    a.nblk = grid_for(int64_t(a.rows) * c->g.nx, 256, std::min(c->nblk_red / 4, 4 * c->sm_count));
+    dim3 grid(unsigned(a.nblk), unsigned(c->g.batch));
+    if (is_f64(c))
+        k_norms<double><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+    else
+        k_norms<float><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+    CKL();
+    double* d4 = reinterpret_cast<double*>(c->d_argpart);  // scratch: 4·B doubles
+    k_norms_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_partial, a.nblk, c->g.batch, d4);
+    CKL();
+    c->launches += 2;
+    if (c->g.nranks > 1 && c->comm) NK(nccl().AllReduce(d4, d4, size_t(4) * c->g.batch, NCCL_F64, NCCL_SUM, c->comm, c->stream));
+    CK(cudaMemcpyAsync(out_B4, d4, sizeof(double) * 4 * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const double w = (c->g.dim == 1) ? c->g.dx : c->g.dx * c->g.dy;
+    for (int b = 0; b < c->g.batch; ++b) {
+        double* o = out_B4 + 4 * b;
+        o[0] = std::sqrt(w * o[0]);
+        o[1] = (c->n >= 1) ? std::sqrt(w * o[1]) / c->dt : 0.0;  // u_t needs two levels
+        o[2] = std::sqrt(w * o[2]) / c->g.dx;
+        o[3] = (c->g.dim == 2) ? std::sqrt(w * o[3]) / c->g.dy : 0.0;
+    }
+    return TSW_OK;
+}
+
+tsw_status tsw_coeff_norms(tsw_ctx* c, double* out_B3) {
+    if (!c || !out_B3) return fail(TSW_ERR_ARG, "NULL argument");
+    if (!c->have_coeff) return fail(TSW_ERR_STATE, "no coefficients");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    CoeffNormArgs a;
+    a.kind = c->kind;
+    a.order = c->order;
+    a.hb = c->hb;
+    a.xs = c->xs;
+    a.ys = c->ys;
+    a.dx = c->g.dx;
+    a.dy = c->g.dy;
+    a.eps = c->d_eps;
+    a.amp = c->d_amp;
+    a.prof = c->d_prof;
+    a.nseg = c->prof_nseg;
+    a.nsing = c->prof_nsing;
+    a.h1 = c->h1;
+    a.h2 = (c->g.dim == 2) ? c->h2 : nullptr;
+    a.nx = c->g.nx;
+    a.ny = c->g.ny;
+    a.r0 = c->r0;
+    a.rows = c->ny_local;
+    a.pitch = c->pitch;
+    a.cstride1 = c->cstride1;
+    a.cstride2 = c->cstride2;
+    a.mstride = c->mstride;
+    a.mode = c->mode;
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(c->d_argpart);
+    CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 3 * c->g.batch, c->stream));
+    const int64_t total = ((c->mode == MODE_LINE) ? 1 : c->ny_local) * c->g.nx;
+    dim3 grid(unsigned(grid_for(total, 256, 4 * c->sm_count)), unsigned(c->g.batch));
+    k_coeff_norms<<<grid, 256, 0, c->stream>>>(a, d);
+    CKL();
+    c->launches++;
+    std::vector<unsigned long long> bits(size_t(3) * c->g.batch);
+    CK(cudaMemcpyAsync(bits.data(), d, sizeof(unsigned long long) * bits.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t k = 0; k < bits.size(); ++k) memcpy(&out_B3[k], &bits[k], sizeof(double));
+    if (c->g.nranks > 1 && c->comm) {
+        double* dd = reinterpret_cast<double*>(d);
+        CK(cudaMemcpy(dd, out_B3, sizeof(double) * bits.size(), cudaMemcpyHostToDevice));
+        NK(nccl().AllReduce(dd, dd, bits.size(), NCCL_F64, NCCL_MAX, c->comm, c->stream));
+        CK(cudaMemcpyAsync(out_B3, dd, sizeof(double) * bits.size(), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
     }
     return TSW_OK;
 }

@@ -34,7 +34,7 @@ STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STA
 
 # every symbol include/tsw.h declares (tests check the library exports all of them)
 EXPORTS = ["tsw_create", "tsw_destroy", "tsw_set_coeff", "tsw_set_coeff_faces", "tsw_set_coeff_profile", "tsw_read_faces", "tsw_set_initial", "tsw_step",
-           "tsw_group_step", "tsw_energy", "tsw_wave2", "tsw_read", "tsw_set_state", "tsw_info", "tsw_sync",
+           "tsw_group_step", "tsw_energy", "tsw_wave2", "tsw_read", "tsw_family_l2", "tsw_field_norms", "tsw_coeff_norms", "tsw_set_state", "tsw_info", "tsw_sync",
            "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
            "tsw_version"]
 
@@ -92,6 +92,9 @@ def load(path: Optional[str] = None):
         "tsw_energy": (i32, [vp, vp]),
         "tsw_wave2": (i32, [vp, i32, vp, vp]),
         "tsw_read": (i32, [vp, i32, vp, i32]),
+        "tsw_family_l2": (i32, [vp, vp]),
+        "tsw_field_norms": (i32, [vp, vp]),
+        "tsw_coeff_norms": (i32, [vp, vp]),
         "tsw_set_state": (i32, [vp, vp, vp, i64, d, i32, u32]),
         "tsw_info": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(d), ctypes.POINTER(d)]),
         "tsw_sync": (i32, [vp]),
@@ -239,6 +242,27 @@ def tsw_wave2(ctx, bg_member: int, batch: int) -> Tuple[np.ndarray, np.ndarray]:
     return out, idx
 
 
+def tsw_family_l2(ctx, batch: int) -> np.ndarray:
+    """[batch][batch] ‖u_i − u_j‖_{L²} at the current level."""
+    out = np.zeros((batch, batch), dtype=np.float64)
+    _check(load().tsw_family_l2(ctx, out.ctypes.data), ctx)
+    return out
+
+
+def tsw_field_norms(ctx, batch: int) -> np.ndarray:
+    """[batch][4]: ‖u‖, ‖u_t‖, ‖∂x u‖, ‖∂y u‖ (L², Theorem lem 1 P:181–183)."""
+    out = np.zeros((batch, 4), dtype=np.float64)
+    _check(load().tsw_field_norms(ctx, out.ctypes.data), ctx)
+    return out
+
+
+def tsw_coeff_norms(ctx, batch: int) -> np.ndarray:
+    """[batch][3]: sup|h1|, sup|∇h|, sup|h2| (W^{1,∞}, P:344–345)."""
+    out = np.zeros((batch, 3), dtype=np.float64)
+    _check(load().tsw_coeff_norms(ctx, out.ctypes.data), ctx)
+    return out
+
+
 def tsw_read(ctx, which: int, out) -> object:
     """Copy u^n (which=0) or u^{n−1} (which=1) into `out` (numpy host array or CUDA tensor)."""
     if hasattr(out, "data_ptr") and getattr(out, "is_cuda", False):
@@ -367,6 +391,15 @@ class Solver:
         if out is None:
             out = np.empty(self.field_shape, dtype=self.np_dtype)
         return tsw_read(self.ctx, which, out)
+
+    def family_l2(self) -> np.ndarray:
+        return tsw_family_l2(self.ctx, self.batch)
+
+    def field_norms(self) -> np.ndarray:
+        return tsw_field_norms(self.ctx, self.batch)
+
+    def coeff_norms(self) -> np.ndarray:
+        return tsw_coeff_norms(self.ctx, self.batch)
 
     def info(self):
         return tsw_info(self.ctx)

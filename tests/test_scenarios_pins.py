@@ -124,3 +124,69 @@ def test_profile_faces_2d_isotropic_and_vector():
     Pv = oracle.Profile([100.0, 10.0], [25.0], [20.0], [3.0], [1], isotropic=False)
     _, h2v = oracle.build_faces_profile(2, Pv, 0.8, sc.nx, sc.ny, sc.dx)
     np.testing.assert_array_equal(h2v[0], Pv.eval(x_nodes, 0.8, with_sing=False))
+
+
+# --- NEXT 2 diagnostics: pins of the oracle definitions ---------------------------------------
+
+def test_family_l2_metric_and_closed_form():
+    x = inputs.node_coords(4001, 0.005)
+    g = np.exp(-(x ** 2) / 0.08)                              # ‖g‖² = √(π·0.04) (closed form)
+    U = np.stack([g, g + 0.5 * g, g - 2.0 * g, np.sin(x)])
+    D = oracle.family_l2(U, 0.005)
+    assert np.all(D == D.T) and np.all(np.diag(D) == 0.0)
+    ng = (math.pi * 0.04) ** 0.25
+    assert abs(D[0, 1] - 0.5 * ng) < 1e-12 and abs(D[0, 2] - 2.0 * ng) < 1e-12
+    for i in range(4):
+        for j in range(4):
+            for k in range(4):
+                assert D[i, j] <= D[i, k] + D[k, j] + 1e-14
+
+
+def test_field_norms_closed_forms():
+    """Gaussian g = e^{−(x²+y²)/w}: ‖g‖² = πw/2, ‖∂x g‖² = π/2 (any w) — second-order accurate."""
+    n, dx, w = 801, 0.005, 0.08
+    x = inputs.node_coords(n, dx)
+    g = np.exp(-(x[None, :] ** 2 + x[:, None] ** 2) / w)
+    out = oracle.field_norms(2, g, 0.5 * g, dx, dx, 0.1)
+    assert abs(out[0] - math.sqrt(math.pi * w / 2)) < 1e-9
+    assert abs(out[1] - 5.0 * math.sqrt(math.pi * w / 2)) < 1e-9     # ‖(g − g/2)/0.1‖
+    assert abs(out[2] - math.sqrt(math.pi / 2)) < 1e-4 and abs(out[3] - out[2]) < 1e-12
+
+
+def test_dphi_and_moderateness_exponents():
+    """φ_ε′ against central differences; SPEC S:89–97 / S:369–377: N0 ≈ 1, 2, 3 for Cases 1, 2, 3."""
+    for eps in (0.05, 0.3):
+        d = np.linspace(-0.95 * eps, 0.95 * eps, 41)
+        h = 1e-6 * eps
+        fd = (oracle.phi_eps(d + h, eps) - oracle.phi_eps(d - h, eps)) / (2 * h)
+        np.testing.assert_allclose(oracle.dphi_eps(d, eps), fd, rtol=1e-6, atol=1e-6 / eps ** 2)
+    # the derivative seminorm of each singular part scales as an exact power of ε⁻¹ (SPEC S:97:
+    # jump 90·φ(0)/ε ⇒ 1; δ: φ_ε′ = ε⁻²φ′ ⇒ 2; δ²: (φ_ε²)′ ∝ ε⁻³ ⇒ 3); the full W^{1,∞} norm
+    # approaches these slopes as ε → 0
+    ladder = [0.2, 0.1, 0.05, 0.025]
+    parts = {"1": oracle.Profile([100.0, 10.0], [25.0]),
+             "2": oracle.Profile([100.0], [], [20.0], [1.0], [1]),
+             "3": oracle.Profile([100.0], [], [20.0], [1.0], [2])}
+    for case, N0 in (("1", 1.0), ("2", 2.0), ("3", 3.0)):
+        P = parts[case]
+        c0 = 25.0 if case == "1" else 20.0
+        semi = []
+        for e in ladder:
+            xs = c0 + np.linspace(-e, e, 20001)
+            semi.append(np.max(np.abs(oracle.profile_derivative(P, xs, e))))
+        assert abs(oracle.moderateness_exponent(ladder, semi) - N0) < 0.01
+
+def test_paper_difference_kernel_H():
+    """H = h_{ε1} − h_{ε2} = 90 ∫_{(x−75)/ε1}^{(x−75)/ε2} φ(z) dz, and H ≡ 0 away from
+    the jump (outside the union of supports)."""
+    sc = inputs.paper_case("1")
+    P = oracle.Profile(sc.seg_value, sc.seg_break)
+    e1, e2 = 0.2, 0.1
+    for xp in (24.85, 24.95, 25.0, 25.07, 25.15):
+        H = P.eval([xp], e1)[0] - P.eval([xp], e2)[0]
+        t1, t2 = (xp - 25.0) / e1, (xp - 25.0) / e2
+        ref = 90.0 * float(C_MP * mpmath.quad(lambda z: mpmath.exp(1 / (z * z - 1)) if abs(z) < 1 else 0,
+                                              [t1, t2]))
+        assert abs(H - ref) < 1e-11
+    far = np.array([10.0, 24.79, 25.21, 40.0])
+    assert np.all(P.eval(far, e1) - P.eval(far, e2) == 0.0)
