@@ -25,7 +25,7 @@ oracle.set_threads(host_cores())
 def test_family_l2_and_norms_small(dtype, dim):
     B = 7
     if dim == 1:
-        cfg = inputs.config(1, nx=1999, eps=[0.03 + 0.02 * k for k in range(B)], amp=[1.0] * (B - 1) + [0.0])
+        cfg = inputs.config(1, nx=1999, eps=[0.03 + 0.02 * k for k in range(B)], amp=[1.0] * (B - 1) + [0.0], dt=7e-4)
     else:
         cfg = inputs.config(3, nx=301, ny=123, dx=0.02, dy=0.02, eps=[0.05 + 0.05 * k for k in range(B)],
                             amp=[1.0] * (B - 1) + [0.0], dt=2e-3)

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$?
-tail -30 gpurun_out/pytest_gpu.log | grep -E "passed|failed|Error|assert|FAILED" | head -30
+grep -E "passed|failed|^E |FAILED" gpurun_out/pytest_gpu.log | head -30
