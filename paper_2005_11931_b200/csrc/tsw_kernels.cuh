@@ -450,6 +450,227 @@ __global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs
 }
 
 // ------------------------------------------------------------------------------------------
+// S3, temporally blocked: K leapfrog levels per HBM pass, out of place.
+// ------------------------------------------------------------------------------------------
+// A CTA (8 consumer warps + 1 producer warp) owns an extended strip of WE = 256·V columns (4 KB of
+// a row): WO = WE − 2H output columns plus H ≥ K halo columns per side, recomputed redundantly.
+// It marches a chunk of output rows [s0, s1) reading input rows [s0 − K, s1 + K) (clipped at the
+// Dirichlet rows).  At input row R it advances a wavefront: level m (1..K) at row R − m, from
+// level m−1 rows R−m−1..R−m+1 and level m−2 at row R−m (leapfrog).  Each thread keeps a 3-row
+// register window per level for its own V columns; the row each level produced in the previous
+// iteration (the next iteration's centre row) sits in shared memory, double-buffered by row
+// parity, for the left/right neighbours — one CTA barrier per input row.  Inputs (u^n, u^{n−1})
+// arrive by TMA bulk copies into a D-stage ring; outputs u^{n+K}, u^{n+K−1} go to two other
+// buffers (out of place: the halo columns of u^n, u^{n−1} are read by the neighbouring strips).
+// HBM traffic per node and pass: 2 reads + 2 writes for K levels (vs 3K words unblocked).
+// Every node value is the same canonical expression as k_step2d (bitwise identical results);
+// Dirichlet rows/columns are forced to +0 at every level.
+constexpr int TB_NC = 8;
+
+template <typename T, int K>
+struct TbGeom {
+    static constexpr int V = Vec16<T>::N;
+    static constexpr int NT = TB_NC * 32;
+    static constexpr int H = ((K + V - 1) / V) * V;
+    static constexpr int WE = NT * V;
+    static constexpr int WO = WE - 2 * H;
+};
+
+template <typename T>
+struct TbArgs {
+    const T* un;
+    const T* unm1;
+    T* out_k;    // u^{n+K}
+    T* out_km1;  // u^{n+K−1}
+    const T* c1;
+    const T* c2;
+    int64_t pitch, mstride, cstride, nx, ny, r0;
+    int32_t s_lo, s_hi;  // output storage rows
+    int32_t smin, smax;  // storage rows inside the grid (global rows 0 .. ny−1 of this slab)
+    int32_t rows_per_item, chunks;
+    int64_t strips, items;
+    T dtT;
+};
+
+template <typename T, int K>
+__host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
+    return size_t(depth) * 2 * TbGeom<T, K>::WE * sizeof(T) + size_t(K) * 2 * TbGeom<T, K>::WE * sizeof(T) +
+           size_t(depth) * 2 * sizeof(uint64_t);
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__((TB_NC + 1) * 32) k_step2d_tb(const TbArgs<T> a, int depth) {
+    using G = TbGeom<T, K>;
+    constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* ring = reinterpret_cast<T*>(smem);                 // [depth][2][WE]
+    T* cen = ring + size_t(depth) * 2 * WE;               // [K][2][WE]
+    uint64_t* full = reinterpret_cast<uint64_t*>(cen + size_t(K) * 2 * WE);
+    uint64_t* empty = full + depth;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < depth; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], TB_NC);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    auto geom = [&](int64_t item, int64_t& cs, int& s0, int& s1, int& b, int& in_lo, int& in_hi) {
+        const int64_t strip = item % a.strips;
+        const int64_t rest = item / a.strips;
+        const int chunk = int(rest % a.chunks);
+        b = int(rest / a.chunks);
+        cs = strip * WO;
+        s0 = a.s_lo + chunk * a.rows_per_item;
+        s1 = min(s0 + a.rows_per_item, a.s_hi);
+        in_lo = max(s0 - K, a.smin);
+        in_hi = min(s1 + K, a.smax + 1);
+    };
+
+    if (warp == TB_NC) {
+        if (lane != 0) return;
+        int64_t it = 0;
+        for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+            int64_t cs;
+            int s0, s1, b, in_lo, in_hi;
+            geom(item, cs, s0, s1, b, in_lo, in_hi);
+            const T* ub = a.un + b * a.mstride;
+            const T* pb = a.unm1 + b * a.mstride;
+            for (int R = in_lo; R < in_hi; ++R, ++it) {
+                const int slot = int(it % depth);
+                if (it >= depth) mbar_wait(&empty[slot], uint32_t(((it / depth) - 1) & 1));
+                T* st = ring + size_t(slot) * 2 * WE;
+                mbar_arrive_expect_tx(&full[slot], 2 * WE * sizeof(T));
+                bulk_g2s(st, ub + R * a.pitch + cs - H, WE * sizeof(T), &full[slot]);
+                bulk_g2s(st + WE, pb + R * a.pitch + cs - H, WE * sizeof(T), &full[slot]);
+            }
+        }
+        return;
+    }
+
+    const int tid = threadIdx.x;
+    const int e0 = tid * V;  // my first column of the extended strip
+    int64_t it = 0;
+    for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+        int64_t cs;
+        int s0, s1, b, in_lo, in_hi;
+        geom(item, cs, s0, s1, b, in_lo, in_hi);
+        const int64_t gc0 = cs - H + e0;  // global column of my first element
+        bool colint[V];
+        T c1l[V], c1r[V], c2v[V];
+        const T* c1b = a.c1 + b * a.cstride;
+        const T* c2b = a.c2 + b * a.cstride;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const int64_t gcol = gc0 + k;
+            colint[k] = (gcol >= 1) && (gcol <= a.nx - 2);
+            c1r[k] = colint[k] ? __ldg(c1b + gcol) : (T)0;
+            c1l[k] = colint[k] ? __ldg(c1b + gcol - 1) : (T)0;
+            c2v[k] = colint[k] ? __ldg(c2b + gcol) : (T)0;
+        }
+        const bool out_cols = (e0 >= H) && (e0 < H + WO) && (cs - H + e0 < a.pitch);
+        T* ok = a.out_k + b * a.mstride;
+        T* okm1 = a.out_km1 + b * a.mstride;
+        T w[K][3][V];  // level m window: rows (r−1, r, r+1) of its newest production
+#pragma unroll
+        for (int m = 0; m < K; ++m)
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+#pragma unroll
+                for (int k = 0; k < V; ++k) w[m][q][k] = (T)0;
+        T pm1[V];  // u^{n−1} at row R − 1
+#pragma unroll
+        for (int k = 0; k < V; ++k) pm1[k] = (T)0;
+        const int nload = in_hi - in_lo;
+        const int L = s1 + K - in_lo;
+        for (int i = 0; i < L; ++i) {
+            const int R = in_lo + i;
+            asm volatile("bar.sync 1, %0;" ::"r"(TB_NC * 32) : "memory");  // consumers only
+            T nw[V], pv_new[V];
+            if (i < nload) {
+                const int slot = int(it % depth);
+                mbar_wait(&full[slot], uint32_t((it / depth) & 1));
+                const T* st = ring + size_t(slot) * 2 * WE;
+                lds_vec(st + e0, nw);
+                lds_vec(st + WE + e0, pv_new);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                ++it;
+            } else {
+#pragma unroll
+                for (int k = 0; k < V; ++k) nw[k] = pv_new[k] = (T)0;
+            }
+            const int par = R & 1;
+            // level 0: window shift; its new row (R) is the next iteration's centre
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                w[0][0][k] = w[0][1][k];
+                w[0][1][k] = w[0][2][k];
+                w[0][2][k] = nw[k];
+            }
+            {
+                using VT = typename Vec16<T>::type;
+                VT x;
+                T* e = reinterpret_cast<T*>(&x);
+#pragma unroll
+                for (int k = 0; k < V; ++k) e[k] = nw[k];
+                *reinterpret_cast<VT*>(cen + (size_t(0) * 2 + par) * WE + e0) = x;
+            }
+            T lastk[V];
+#pragma unroll
+            for (int m = 1; m <= K; ++m) {
+                const int r = R - m;
+                const int64_t g = a.r0 + r - 1;
+                const bool rowint = (g >= 1) && (g <= a.ny - 2);
+                const T* ce = cen + (size_t(m - 1) * 2 + (par ^ 1)) * WE;
+                const T left = (e0 > 0) ? ce[e0 - 1] : (T)0;
+                const T right = (e0 + V < WE) ? ce[e0 + V] : (T)0;
+                T nv[V];
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    const T cu = w[m - 1][1][k];
+                    const T ul = (k == 0) ? left : w[m - 1][1][k - 1];
+                    const T ur = (k == V - 1) ? right : w[m - 1][1][k + 1];
+                    const T pr = (m == 1) ? pm1[k] : w[(m >= 2) ? m - 2 : 0][0][k];
+                    const T v = node_update<T, false, true>(cu, ul, ur, w[m - 1][0][k], w[m - 1][2][k], pr, c1l[k],
+                                                            c1r[k], c2v[k], c2v[k], a.dtT);
+                    nv[k] = (rowint && colint[k]) ? v : (T)0;
+                }
+                if (m < K) {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) {
+                        w[m][0][k] = w[m][1][k];
+                        w[m][1][k] = w[m][2][k];
+                        w[m][2][k] = nv[k];
+                    }
+                    using VT = typename Vec16<T>::type;
+                    VT x;
+                    T* e = reinterpret_cast<T*>(&x);
+#pragma unroll
+                    for (int k = 0; k < V; ++k) e[k] = nv[k];
+                    *reinterpret_cast<VT*>(cen + (size_t(m) * 2 + par) * WE + e0) = x;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) lastk[k] = nv[k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < V; ++k) pm1[k] = pv_new[k];
+            const int ro = R - K;
+            if (out_cols && ro >= s0 && ro < s1) {
+                T o2[V];
+#pragma unroll
+                for (int k = 0; k < V; ++k) o2[k] = w[K - 1][1][k];
+                vstore(ok + ro * a.pitch + gc0, lastk);
+                vstore(okm1 + ro * a.pitch + gc0, o2);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // S2/S3: 1D, persistent — one CTA per member, both levels resident in shared memory, all
 // steps in one launch (config 1: 2000 fp64 nodes × 3 arrays = 48 KB).
 // ------------------------------------------------------------------------------------------

@@ -129,9 +129,10 @@ struct tsw_ctx {
     // slab geometry
     int64_t r0 = 0, r1 = 0, ny_local = 1, rows_alloc = 1, pitch = 0, mstride = 0;
     int32_t s_lo = 0, s_hi = 0;  // storage rows of updated nodes (2D)
-    // time levels: buf[cur] = u^n, buf[cur ^ 1] = u^{n−1}
-    void* buf[2] = {nullptr, nullptr};
-    int cur = 0;
+    // time levels: buf[ic] = u^n, buf[ip] = u^{n−1}; buf[2], buf[3] exist only for the
+    // temporally blocked stencil (out of place)
+    void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+    int ic = 0, ip = 1;
     // coefficients (fp64 faces h, prescaled T faces c)
     bool have_coeff = false;
     int mode = MODE_LINE;
@@ -169,6 +170,9 @@ struct tsw_ctx {
     int rows_per_item_opt = 0;
     int kernel_opt = 0;   // 0: CTA-wide TMA bulk-copy pipeline (default), 1: register-prefetch kernel
     int depth_opt = 4;    // TMA ring stages per CTA (sweep: 4 best at 32768-wide rows)
+    int tblock = 1;       // levels per HBM pass of the temporally blocked stencil (1 = off)
+    int tb_depth = 4;     // its input ring stages
+    int tb_occ[2][9] = {};  // [f64][K] resident CTAs per SM (cached)
     int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
     int bulk_occ_key[2][2] = {{0, 0}, {0, 0}};
     int step_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};  // [mode][start]
@@ -182,7 +186,7 @@ struct tsw_ctx {
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
     // CUDA graphs of two leapfrog levels (single rank), one per buffer parity
     bool use_graphs = true;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    cudaGraphExec_t gexec[4][4] = {};  // keyed by (ic, ip)
     // NCCL
     void* comm = nullptr;
 };
@@ -204,11 +208,12 @@ int grid_for(int64_t n, int threads, int cap) {
 }
 
 void drop_graphs(tsw_ctx* c) {
-    for (int k = 0; k < 2; ++k)
-        if (c->gexec[k]) {
-            cudaGraphExecDestroy(c->gexec[k]);
-            c->gexec[k] = nullptr;
-        }
+    for (int i = 0; i < 4; ++i)
+        for (int k = 0; k < 4; ++k)
+            if (c->gexec[i][k]) {
+                cudaGraphExecDestroy(c->gexec[i][k]);
+                c->gexec[i][k] = nullptr;
+            }
 }
 
 // ---- live kernel timing ----------------------------------------------------------------------
@@ -227,17 +232,18 @@ tsw_status timing_events(tsw_ctx* c, cudaEvent_t* e0, cudaEvent_t* e1) {
 // Rows per work item: maximise the useful fraction of the last wave of items over the G
 // resident workers, discounted by the halo re-read (two extra u^n rows per item, u^n being a
 // third of the traffic); ties go to longer items.
-int choose_rows_per_item(int64_t rows, int64_t strips, int64_t batch, int64_t G) {
+int choose_rows_per_item(int64_t rows, int64_t strips, int64_t batch, int64_t G, double halo_rows = 2.0,
+                         double halo_weight = 1.0 / 3.0, int64_t min_rows = 8) {
     double best = -1.0;
     int bestR = int(rows);
-    const int64_t cmax = std::max<int64_t>(1, rows / 8);
+    const int64_t cmax = std::max<int64_t>(1, rows / std::max<int64_t>(1, min_rows));
     for (int64_t cch = 1; cch <= cmax; ++cch) {
         const int64_t R = (rows + cch - 1) / cch;
         const int64_t c2 = (rows + R - 1) / R;
         const int64_t items = strips * c2 * batch;
         const int64_t waves = (items + G - 1) / G;
         const double eff = double(items) / double(waves * G);
-        const double score = eff / (1.0 + (2.0 / double(R)) / 3.0);
+        const double score = eff / (1.0 + (halo_rows / double(R)) * halo_weight);
         if (score > best + 1e-9) {
             best = score;
             bestR = int(R);
@@ -265,15 +271,15 @@ tsw_status tma_occupancy(tsw_ctx* c, int* occ_out, size_t* smem_out) {
 }
 
 // ---- 2D stencil launch ---------------------------------------------------------------------
-// Updates storage rows [s_lo, s_hi) of every member: reads buf[cur] (u^n) and buf[cur^1]
-// (u^{n−1}), writes u^{n+1} in place into buf[cur^1].
+// Updates storage rows [s_lo, s_hi) of every member: reads buf[ic] (u^n) and buf[ip]
+// (u^{n−1}), writes u^{n+1} in place into buf[ip].
 template <typename T, int MODE, bool START>
 tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
     if (s_hi <= s_lo) return TSW_OK;
     const bool tma = (c->kernel_opt == 0);
     StepArgs<T> a;
-    a.ucur = static_cast<const T*>(c->buf[c->cur]);
-    a.uprev = static_cast<T*>(c->buf[c->cur ^ 1]);
+    a.ucur = static_cast<const T*>(c->buf[c->ic]);
+    a.uprev = static_cast<T*>(c->buf[c->ip]);
     a.c1 = static_cast<const T*>(c->c1);
     a.c2 = static_cast<const T*>(c->c2);
     a.pitch = c->pitch;
@@ -334,6 +340,89 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
     return TSW_OK;
 }
 
+// ---- temporally blocked pass: K levels, (buf[ic], buf[ip]) → (buf[fk], buf[fkm1]) -----------
+template <typename T, int K>
+tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1) {
+    using G = TbGeom<T, K>;
+    const int depth = c->tb_depth;
+    const size_t smem = tb_smem_bytes<T, K>(depth);
+    int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K];
+    if (occ == 0) {
+        CK(cudaFuncSetAttribute(k_step2d_tb<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K>, (TB_NC + 1) * 32, smem));
+        if (occ < 1) return fail(TSW_ERR_ARG, "temporally blocked stencil (K=%d) does not fit on an SM", K);
+    }
+    TbArgs<T> a;
+    a.un = static_cast<const T*>(c->buf[c->ic]);
+    a.unm1 = static_cast<const T*>(c->buf[c->ip]);
+    a.out_k = static_cast<T*>(c->buf[fk]);
+    a.out_km1 = static_cast<T*>(c->buf[fkm1]);
+    a.c1 = static_cast<const T*>(c->c1);
+    a.c2 = static_cast<const T*>(c->c2);
+    a.pitch = c->pitch;
+    a.mstride = c->mstride;
+    a.cstride = c->cstride1;
+    a.nx = c->g.nx;
+    a.ny = c->g.ny;
+    a.r0 = c->r0;
+    a.s_lo = c->s_lo;
+    a.s_hi = c->s_hi;
+    a.smin = 1;
+    a.smax = int32_t(c->ny_local);
+    a.strips = (c->pitch + G::WO - 1) / G::WO;
+    a.dtT = (T)c->dt;
+    const int64_t rows = c->s_hi - c->s_lo;
+    const int64_t Gw = int64_t(occ) * c->sm_count;
+    int R = c->rows_per_item_opt;
+    if (R <= 0) R = choose_rows_per_item(rows, a.strips, c->g.batch, Gw, 2.0 * K, 0.5, 4 * K);
+    if (R > rows) R = int(rows);
+    a.rows_per_item = R;
+    a.chunks = int((rows + R - 1) / R);
+    a.items = a.strips * a.chunks * c->g.batch;
+    const int64_t blocks = std::min<int64_t>(a.items, Gw);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        tsw_status st = timing_events(c, &e0, &e1);
+        if (st) return st;
+        CK(cudaEventRecord(e0, c->stream));
+    }
+    k_step2d_tb<T, K><<<unsigned(blocks), (TB_NC + 1) * 32, smem, c->stream>>>(a, depth);
+    CKL();
+    if (c->timing) {
+        CK(cudaEventRecord(e1, c->stream));
+        c->timed_launches++;
+        c->timed_updates += rows * (c->g.nx - 2) * c->g.batch * K;
+    }
+    c->launches++;
+    return TSW_OK;
+}
+
+template <typename T>
+tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1) {
+    switch (K) {
+        case 2: return launch_tb_t<T, 2>(c, fk, fkm1);
+        case 3: return launch_tb_t<T, 3>(c, fk, fkm1);
+        case 4: return launch_tb_t<T, 4>(c, fk, fkm1);
+        case 6: return launch_tb_t<T, 6>(c, fk, fkm1);
+        case 8: return launch_tb_t<T, 8>(c, fk, fkm1);
+        default: return fail(TSW_ERR_ARG, "unsupported temporal blocking depth %d", K);
+    }
+}
+
+// One pass of K levels; afterwards u^n = buf[fk], u^{n−1} = buf[fkm1].
+tsw_status tb_pass(tsw_ctx* c) {
+    int free_ids[2], nf = 0;
+    for (int k = 0; k < 4 && nf < 2; ++k)
+        if (k != c->ic && k != c->ip) free_ids[nf++] = k;
+    const int fk = free_ids[0], fkm1 = free_ids[1];
+    tsw_status st = is_f64(c) ? launch_tb_k<double>(c, c->tblock, fk, fkm1) : launch_tb_k<float>(c, c->tblock, fk, fkm1);
+    if (st) return st;
+    c->ic = fk;
+    c->ip = fkm1;
+    c->n += c->tblock;
+    return TSW_OK;
+}
+
 tsw_status launch_step2d(tsw_ctx* c, bool start, int32_t s_lo, int32_t s_hi) {
     if (is_f64(c)) {
         if (c->mode == MODE_LINE)
@@ -354,8 +443,8 @@ template <typename T>
 tsw_status step1d_t(tsw_ctx* c, int64_t k) {
     const bool start = (c->n == 0);
     const size_t smem = size_t(3) * c->pitch * sizeof(T);
-    T* u = static_cast<T*>(c->buf[c->cur]);
-    T* p = static_cast<T*>(c->buf[c->cur ^ 1]);
+    T* u = static_cast<T*>(c->buf[c->ic]);
+    T* p = static_cast<T*>(c->buf[c->ip]);
     const T* c1 = static_cast<const T*>(c->c1);
     if (smem <= 200 * 1024) {
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_step1d_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -375,20 +464,20 @@ tsw_status step1d_t(tsw_ctx* c, int64_t k) {
             c->timed_updates += k * (c->g.nx - 2) * c->g.batch;
         }
         c->launches++;
-        c->n += k;  // the kernel writes the newest level back into buf[cur]
+        c->n += k;  // the kernel writes the newest level back into buf[ic]
         return TSW_OK;
     }
     const dim3 grid(unsigned(grid_for(c->g.nx, 256, 4 * c->sm_count)), unsigned(c->g.batch));
     for (int64_t s = 0; s < k; ++s) {
-        const T* uc = static_cast<const T*>(c->buf[c->cur]);
-        T* up = static_cast<T*>(c->buf[c->cur ^ 1]);
+        const T* uc = static_cast<const T*>(c->buf[c->ic]);
+        T* up = static_cast<T*>(c->buf[c->ip]);
         if (c->n == 0)
             k_step1d_global<T, true><<<grid, 256, 0, c->stream>>>(uc, up, c1, c->g.nx, c->pitch, c->cstride1, (T)c->dt);
         else
             k_step1d_global<T, false><<<grid, 256, 0, c->stream>>>(uc, up, c1, c->g.nx, c->pitch, c->cstride1, (T)c->dt);
         CKL();
         c->launches++;
-        c->cur ^= 1;
+        std::swap(c->ic, c->ip);
         c->n++;
     }
     return TSW_OK;
@@ -422,7 +511,7 @@ tsw_status exchange_nccl(tsw_ctx* c, void* field, cudaStream_t stream = nullptr)
 }
 
 // Loopback: ranks are ctxs on one device and stream; copy rows device-to-device.
-// level 0 = u^n (buf[cur]), 1 = u^{n−1} (buf[cur^1]).
+// level 0 = u^n (buf[ic]), 1 = u^{n−1} (buf[ip]).
 tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0, cudaStream_t stream = nullptr) {
     if (!stream) stream = cs[0]->stream;
     for (int r = 0; r + 1 < n; ++r) {
@@ -431,8 +520,8 @@ tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0, cudaStream_t st
         const size_t row_a = size_t(a->pitch) * a->esz;
         const size_t row_b = size_t(b->pitch) * b->esz;
         for (int m = 0; m < a->g.batch; ++m) {
-            char* ma = static_cast<char*>(a->buf[a->cur ^ level]) + size_t(m) * a->mstride * a->esz;
-            char* mb = static_cast<char*>(b->buf[b->cur ^ level]) + size_t(m) * b->mstride * b->esz;
+            char* ma = static_cast<char*>(a->buf[level ? a->ip : a->ic]) + size_t(m) * a->mstride * a->esz;
+            char* mb = static_cast<char*>(b->buf[level ? b->ip : b->ic]) + size_t(m) * b->mstride * b->esz;
             // a's last owned row → b's ghost row 0 ; b's first owned row → a's ghost row ny_local+1
             CK(cudaMemcpyAsync(mb, ma + size_t(a->ny_local) * row_a, size_t(a->g.nx) * a->esz, cudaMemcpyDeviceToDevice,
                                stream));
@@ -573,9 +662,10 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     const bool shared = (flags & TSW_INIT_SHARED) != 0;
     const size_t bytes = size_t(c->g.batch) * c->mstride * c->esz;
     drop_graphs(c);  // captured launches bake in dt
-    c->cur = 0;
-    CK(cudaMemsetAsync(c->buf[0], 0, bytes, c->stream));
-    CK(cudaMemsetAsync(c->buf[1], 0, bytes, c->stream));
+    c->ic = 0;
+    c->ip = 1;
+    for (int k = 0; k < 4; ++k)
+        if (c->buf[k]) CK(cudaMemsetAsync(c->buf[k], 0, bytes, c->stream));
     tsw_status st = load_field(c, c->buf[0], a, shared, on_device);
     if (st) return st;
     if (b) {
@@ -643,30 +733,31 @@ tsw_status step_slab_overlapped(tsw_ctx* c) {
     if ((st = launch_boundary_rows(c, start))) return st;
     CK(cudaEventRecord(c->ev_bnd, c->stream));
     CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
-    if ((st = exchange_nccl(c, c->buf[c->cur ^ 1], c->aux))) return st;
+    if ((st = exchange_nccl(c, c->buf[c->ip], c->aux))) return st;
     CK(cudaEventRecord(c->ev_comm, c->aux));
     if ((st = launch_interior_rows(c, start))) return st;
     CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
-    c->cur ^= 1;
+    std::swap(c->ic, c->ip);
     c->n++;
     return TSW_OK;
 }
 
-// Two leapfrog levels captured once per buffer parity and replayed (single rank, n ≥ 1).
+// Two leapfrog levels captured once per (ic, ip) and replayed (single rank, n ≥ 1).
 tsw_status step_pair_graph(tsw_ctx* c) {
-    cudaGraphExec_t& ge = c->gexec[c->cur];
+    cudaGraphExec_t& ge = c->gexec[c->ic][c->ip];
     if (!ge) {
-        const int cur0 = c->cur;
+        const int ic0 = c->ic, ip0 = c->ip;
         const int64_t launches0 = c->launches;
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
         tsw_status st = launch_step2d(c, false, c->s_lo, c->s_hi);
         if (!st) {
-            c->cur ^= 1;
+            std::swap(c->ic, c->ip);
             st = launch_step2d(c, false, c->s_lo, c->s_hi);
         }
         cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
-        c->cur = cur0;
+        c->ic = ic0;
+        c->ip = ip0;
         c->launches = launches0;
         if (st) {
             if (graph) cudaGraphDestroy(graph);
@@ -698,16 +789,19 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
     int64_t s = 0;
     if (c->n == 0) {  // the start-up level
         if ((st = launch_step2d(c, true, c->s_lo, c->s_hi))) return st;
-        c->cur ^= 1;
+        std::swap(c->ic, c->ip);
         c->n++;
         s = 1;
     }
+    if (c->tblock > 1 && c->mode == MODE_LINE && c->buf[2] && c->buf[3])
+        for (; s + c->tblock <= k; s += c->tblock)
+            if ((st = tb_pass(c))) return st;
     const bool graphs = c->use_graphs && !c->timing;
     for (; s + 1 < k && graphs; s += 2)
         if ((st = step_pair_graph(c))) return st;
     for (; s < k; ++s) {
         if ((st = launch_step2d(c, false, c->s_lo, c->s_hi))) return st;
-        c->cur ^= 1;
+        std::swap(c->ic, c->ip);
         c->n++;
     }
     return TSW_OK;
@@ -819,8 +913,7 @@ void tsw_destroy(tsw_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    dfree_guarded(c->buf[0]);
-    dfree_guarded(c->buf[1]);
+    for (int k = 0; k < 4; ++k) dfree_guarded(c->buf[k]);
     dfree_guarded(c->h1);
     dfree_guarded(c->h2);
     dfree_guarded(c->c1);
@@ -1126,7 +1219,7 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
             if ((st = launch_interior_rows(cs[r], start))) return st;
         CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
         for (int r = 0; r < n; ++r) {
-            cs[r]->cur ^= 1;
+            std::swap(cs[r]->ic, cs[r]->ip);
             cs[r]->n++;
         }
     }
@@ -1142,8 +1235,8 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     if (c->g.dim == 2) {
         Energy2Args a;
         a.mode = c->mode;
-        a.unp1 = c->buf[c->cur];
-        a.un = c->buf[c->cur ^ 1];
+        a.unp1 = c->buf[c->ic];
+        a.un = c->buf[c->ip];
         a.c1 = c->c1;
         a.c2 = c->c2;
         a.nx = c->g.nx;
@@ -1175,8 +1268,8 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
         EnergyArgs a;
         a.dim = c->g.dim;
         a.mode = c->mode;
-        a.unp1 = c->buf[c->cur];
-        a.un = c->buf[c->cur ^ 1];
+        a.unp1 = c->buf[c->ic];
+        a.un = c->buf[c->ip];
         a.c1 = c->c1;
         a.c2 = c->c2;
         a.nx = c->g.nx;
@@ -1216,7 +1309,7 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
     if (st) return st;
     Wave2Args a;
     a.dim = c->g.dim;
-    a.u = c->buf[c->cur];
+    a.u = c->buf[c->ic];
     a.nx = c->g.nx;
     a.ny = c->g.ny;
     a.r0 = c->r0;
@@ -1292,7 +1385,7 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
     tsw_status st = set_dev(c);
     if (st) return st;
     FamilyArgs a;
-    a.u = c->buf[c->cur];
+    a.u = c->buf[c->ic];
     a.nx = c->g.nx;
     a.pitch = c->pitch;
     a.mstride = c->mstride;
@@ -1363,8 +1456,8 @@ tsw_status tsw_field_norms(tsw_ctx* c, double* out_B4) {
     if (st) return st;
     NormArgs a;
     a.dim = c->g.dim;
-    a.un = c->buf[c->cur];
-    a.unm1 = c->buf[c->cur ^ 1];
+    a.un = c->buf[c->ic];
+    a.unm1 = c->buf[c->ip];
     a.nx = c->g.nx;
     a.ny = c->g.ny;
     a.r0 = c->r0;
@@ -1451,7 +1544,7 @@ tsw_status tsw_read(tsw_ctx* c, int32_t which, void* dst, int32_t to_device) {
     if (which != 0 && which != 1) return fail(TSW_ERR_ARG, "which must be 0 (u^n) or 1 (u^{n-1})");
     tsw_status st = set_dev(c);
     if (st) return st;
-    const void* src = c->buf[c->cur ^ which];
+    const void* src = c->buf[which ? c->ip : c->ic];
     const cudaMemcpyKind kind = to_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     const size_t w = size_t(c->g.nx) * c->esz;
     const size_t rows = size_t(c->ny_local);
@@ -1491,6 +1584,38 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
     drop_graphs(c);  // captured launches bake in the kernel variant and its shape
     if (key == TSW_OPT_GRAPHS) {
         c->use_graphs = value != 0;
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_TBLOCK) {
+        if (!(value == 1 || value == 2 || value == 3 || value == 4 || value == 6 || value == 8))
+            return fail(TSW_ERR_ARG, "temporal blocking depth must be 1, 2, 3, 4, 6 or 8");
+        if (value > 1 && (c->g.dim != 2 || c->g.nranks != 1))
+            return fail(TSW_ERR_ARG, "temporal blocking needs a single-rank 2D grid");
+        tsw_status st = set_dev(c);
+        if (st) return st;
+        if (value > 1 && !c->buf[2]) {
+            // two more levels for the out-of-place passes (zeroed: boundaries stay +0)
+            const size_t bytes = size_t(c->g.batch) * c->mstride * c->esz;
+            for (int k = 2; k < 4; ++k) {
+                cudaError_t e = dmalloc_guarded(&c->buf[k], bytes);
+                if (e != cudaSuccess) {
+                    for (int j = 2; j < 4; ++j) {
+                        dfree_guarded(c->buf[j]);
+                        c->buf[j] = nullptr;
+                    }
+                    return fail(e == cudaErrorMemoryAllocation ? TSW_ERR_OOM : TSW_ERR_CUDA, "TB buffers: %s",
+                                cudaGetErrorString(e));
+                }
+            }
+        }
+        c->tblock = int(value);
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_TB_DEPTH) {
+        if (value < 2 || value > 16) return fail(TSW_ERR_ARG, "TB ring depth must be in [2, 16]");
+        c->tb_depth = int(value);
+        for (auto& r : c->tb_occ)
+            for (int& o : r) o = 0;
         return TSW_OK;
     }
     if (key == TSW_OPT_ROWS_PER_ITEM) {

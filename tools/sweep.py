@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--kind", type=int, default=1)
     ap.add_argument("--reg", action="store_true", help="also time the register kernel")
+    ap.add_argument("--tblocks", default="", help="temporal blocking depths to time, e.g. 2,4,8")
+    ap.add_argument("--tbdepths", default="4")
     args = ap.parse_args()
     import torch
     from paper_2005_11931_b200 import inputs, tsw
@@ -38,6 +40,26 @@ def main():
         [int(x) for x in args.rows.split(",")])]
     if args.reg:
         combos = [(1, 0, 0, r) for r in [int(x) for x in args.rows.split(",")]] + combos
+    for K in [int(x) for x in args.tblocks.split(",") if x]:
+        for td in [int(x) for x in args.tbdepths.split(",")]:
+            for r in [int(x) for x in args.rows.split(",")]:
+                s.set_option(tsw.TSW_OPT_TBLOCK, K)
+                s.set_option(tsw.TSW_OPT_TB_DEPTH, td)
+                s.set_option(tsw.TSW_OPT_ROWS_PER_ITEM, r)
+                try:
+                    s.step(4 * K)
+                    s.set_option(tsw.TSW_OPT_TIME_KERNELS, 1)
+                    s.step((args.steps // K) * K)
+                    ms, n, upd = s.kernel_stats()
+                    s.set_option(tsw.TSW_OPT_TIME_KERNELS, 0)
+                except tsw.TswError as e:
+                    print(json.dumps({"tblock": K, "tbdepth": td, "rows": r, "error": str(e)}), flush=True)
+                    continue
+                print(json.dumps({"kernel": "tb", "K": K, "tbdepth": td, "rows": r, "ms_per_level": ms / (n * K),
+                                  "Gpts": round(upd / (ms * 1e-3) / 1e9, 2),
+                                  "hbm_GBs_4words_per_pass": round(upd / K * 4 * esz / (ms * 1e-3) / 1e9, 1)}),
+                      flush=True)
+        s.set_option(tsw.TSW_OPT_TBLOCK, 1)
     for kern, d, w, r in combos:
         s.set_option(tsw.TSW_OPT_KERNEL, kern)
         if kern == 0:
