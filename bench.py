@@ -49,12 +49,12 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(dtype: str, workload: str):
+def ncu_traffic(dtype: str, workload: str, tblock: int = 1):
     """dram bytes per stencil launch from the committed ncu --set full summary, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        e = t.get(dtype)
+        e = t.get(dtype if tblock == 1 else f"{dtype}_tb{tblock}")
         if e and e.get("workload") == workload:
             return float(e["dram_bytes_per_launch"])
     except Exception:
@@ -193,6 +193,8 @@ def main():
     ap.add_argument("--no-also", action="store_true", help="skip the second-precision line item")
     ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--rows-per-item", type=int, default=0)
+    ap.add_argument("--tblock", type=int, default=5,
+                    help="levels per HBM pass of the temporally blocked stencil (1 = per-step TMA kernel)")
     args = ap.parse_args()
 
     from paper_2005_11931_b200 import inputs, parallel
@@ -216,6 +218,8 @@ def main():
         s = tsw.Solver.from_config(cfg, dtype, rank=rank, nranks=world, device=local, stream=stream.cuda_stream)
         if args.rows_per_item:
             s.set_option(tsw.TSW_OPT_ROWS_PER_ITEM, args.rows_per_item)
+        if tblock > 1:
+            s.set_option(tsw.TSW_OPT_TBLOCK, tblock)
         parallel.nccl_bootstrap(s)
         r0, r1 = parallel.slab(cfg.ny, rank, world)
         u0_host = torch.from_numpy(inputs.uniform_dense_rows(cfg.nx, cfg.ny, r0, r1 - r0).astype(npdt)).pin_memory()
@@ -294,16 +298,28 @@ def main():
         torch.cuda.empty_cache()
         return res
 
+    tblock = args.tblock if world == 1 else 1  # slabs exchange one ghost row per level
     main_res = run(args.dtype, True)
     other = "f32" if args.dtype == "f64" else "f64"
     also = None if args.no_also else run(other, False)
+    per_step = None
+    if tblock > 1 and not args.no_also:
+        tb_saved, tblock = tblock, 1
+        per_step = run(args.dtype, False)  # the one-level-per-pass kernel on the same workload
+        tblock = tb_saved
 
     if rank == 0:
         peak, peak_src = measured_peak()
         esz = ESZ[args.dtype]
-        achieved = main_res["kernel_updates_per_launch"] * 3 * esz / (main_res["kernel_avg_ms"] * 1e-3) / 1e9
+        # algorithmic bytes per point-update: 3 words per step; with temporal
+        # blocking of depth K, (2 reads + 2 writes)/K words
+        words = 3.0 if tblock == 1 else 4.0 / tblock
+        upd_s = main_res["kernel_updates_per_launch"] / (main_res["kernel_avg_ms"] * 1e-3)
+        achieved = upd_s * words * esz / 1e9
         wl = workload_name(cfg, world)
-        traffic = ncu_traffic(args.dtype, wl)
+        traffic = ncu_traffic(args.dtype, wl, tblock)
+        clk = (main_res["clocks"] or {}).get("sm_mhz") or 1965.0
+        fp_peak = (64.0 if args.dtype == "f64" else 128.0) * 148 * clk * 1e6 / 1e12  # non-FMA ops/clk/SM
         line = {
             "metric": METRIC, "value": main_res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": main_res["ms"] / args.steps, "higher_is_better": True,
@@ -311,14 +327,22 @@ def main():
             "data": "synthetic (dense uniform[-1,1] u0, u1 = 0, seed 0; delta-line h_eps, eps = 0.05)",
             "config": {"workload": wl, "nx": cfg.nx, "ny_global": cfg.ny, "rows_per_gpu": cfg.ny // world,
                        "dx": cfg.dx, "dt": cfg.dt, "eps": cfg.eps[0], "energy_every": args.energy_every,
+                       "temporal_blocking": tblock,
                        "parallelism": f"row-slab x{world} (NCCL ghost rows)" if world > 1 else "single GPU",
                        "l2": "inputs exceed L2 (2 levels x %.2f GB per GPU), no flush" %
                              ((cfg.nx * (cfg.ny // world) * esz) / 1e9)},
-            "hbm_gbs_effective": main_res["value"] * 3 * esz,
+            "hbm_gbs_effective": main_res["value"] * words * esz,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_step2d (S3 leapfrog stencil)",
-                         "algorithmic_bytes_per_update": 3 * esz, "peak_source": peak_src,
-                         "kernel_avg_ms": main_res["kernel_avg_ms"]},
+                         "traffic": traffic,
+                         "kernel": ("k_step2d_tma (S3 leapfrog, one level per pass)" if tblock == 1 else
+                                    f"k_step2d_tb (S3 leapfrog, K={tblock} levels per HBM pass)"),
+                         "algorithmic_bytes_per_update": words * esz, "peak_source": peak_src,
+                         "kernel_avg_ms": main_res["kernel_avg_ms"],
+                         "per_step_roofline_gpts": peak / (3 * esz),
+                         "alu_view": {"unit": "TFLOP/s", "achieved": upd_s * 14 / 1e12, "peak": fp_peak,
+                                      "frac": upd_s * 14 / 1e12 / fp_peak,
+                                      "note": "14 non-contracted ops per update (canonical tree, no FMA); "
+                                              "peak = 64 (fp64) / 128 (fp32) ops/clk/SM x 148 SMs x median SM clock"}},
             "gpu_launches": main_res["launches"],
             "clocks": main_res["clocks"],
         }
@@ -326,10 +350,14 @@ def main():
             line["e2e"] = main_res["e2e"]
         if also:
             e2 = ESZ[other]
-            ach2 = also["kernel_updates_per_launch"] * 3 * e2 / (also["kernel_avg_ms"] * 1e-3) / 1e9
+            ach2 = also["kernel_updates_per_launch"] / (also["kernel_avg_ms"] * 1e-3) * words * e2 / 1e9
             line["also"] = {"dtype": other, "value": also["value"], "unit": UNIT,
-                            "ms_per_step": also["ms"] / args.steps, "hbm_gbs_effective": also["value"] * 3 * e2,
-                            "roofline_frac": ach2 / peak, "achieved_gbs": ach2}
+                            "ms_per_step": also["ms"] / args.steps, "roofline_frac": ach2 / peak, "achieved_gbs": ach2}
+        if per_step:
+            ach1 = per_step["kernel_updates_per_launch"] * 3 * esz / (per_step["kernel_avg_ms"] * 1e-3) / 1e9
+            line["per_step_kernel"] = {"kernel": "k_step2d_tma", "value": per_step["value"], "unit": UNIT,
+                                       "achieved_gbs": ach1, "roofline_frac": ach1 / peak,
+                                       "traffic": ncu_traffic(args.dtype, wl, 1)}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, args.dtype)
         print(json.dumps(line), flush=True)

@@ -244,6 +244,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs
 // ------------------------------------------------------------------------------------------
 // S3, temporally blocked: K leapfrog levels per HBM pass, out of place.
 // ------------------------------------------------------------------------------------------
-// A CTA (8 consumer warps + 1 producer warp) owns an extended strip of WE = 256·V columns (4 KB of
+// A CTA of 8 warps owns an extended strip of WE = 256·V columns (4 KB of
 // a row): WO = WE − 2H output columns plus H ≥ K halo columns per side, recomputed redundantly.
 // It marches a chunk of output rows [s0, s1) reading input rows [s0 − K, s1 + K) (clipped at the
 // Dirichlet rows).  At input row R it advances a wavefront: level m (1..K) at row R − m, from
@@ -460,8 +463,9 @@ __global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs
 // register window per level for its own V columns; the row each level produced in the previous
 // iteration (the next iteration's centre row) sits in shared memory, double-buffered by row
 // parity, for the left/right neighbours — one CTA barrier per input row.  Inputs (u^n, u^{n−1})
-// arrive by TMA bulk copies into a D-stage ring; outputs u^{n+K}, u^{n+K−1} go to two other
-// buffers (out of place: the halo columns of u^n, u^{n−1} are read by the neighbouring strips).
+// arrive by TMA bulk copies (issued by thread 0) into a D-stage ring; outputs u^{n+K}, u^{n+K−1}
+// go to two other buffers (out of place: the halo columns of u^n, u^{n−1} are read by the
+// neighbouring strips).
 // HBM traffic per node and pass: 2 reads + 2 writes for K levels (vs 3K words unblocked).
 // Every node value is the same canonical expression as k_step2d (bitwise identical results);
 // Dirichlet rows/columns are forced to +0 at every level.
@@ -495,24 +499,23 @@ struct TbArgs {
 template <typename T, int K>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
     return size_t(depth) * 2 * TbGeom<T, K>::WE * sizeof(T) + size_t(K) * 2 * TbGeom<T, K>::WE * sizeof(T) +
-           size_t(depth) * 2 * sizeof(uint64_t);
+           size_t(depth) * sizeof(uint64_t);
 }
 
+// The producer is thread 0: at input row i it refills the stage consumed at row i − 1 (every
+// thread has passed the per-row barrier, so that stage is free) with the stream's stage i − 1 + D.
 template <typename T, int K>
-__global__ void __launch_bounds__((TB_NC + 1) * 32) k_step2d_tb(const TbArgs<T> a, int depth) {
+__global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
     extern __shared__ __align__(128) unsigned char smem[];
     T* ring = reinterpret_cast<T*>(smem);                 // [depth][2][WE]
     T* cen = ring + size_t(depth) * 2 * WE;               // [K][2][WE]
     uint64_t* full = reinterpret_cast<uint64_t*>(cen + size_t(K) * 2 * WE);
-    uint64_t* empty = full + depth;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < depth; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], TB_NC);
-        }
+    const int lane = threadIdx.x & 31;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int k = 0; k < depth; ++k) mbar_init(&full[k], 1);
         fence_barrier_init();
     }
     __syncthreads();
@@ -529,30 +532,36 @@ __global__ void __launch_bounds__((TB_NC + 1) * 32) k_step2d_tb(const TbArgs<T> 
         in_hi = min(s1 + K, a.smax + 1);
     };
 
-    if (warp == TB_NC) {
-        if (lane != 0) return;
-        int64_t it = 0;
-        for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
-            int64_t cs;
-            int s0, s1, b, in_lo, in_hi;
-            geom(item, cs, s0, s1, b, in_lo, in_hi);
-            const T* ub = a.un + b * a.mstride;
-            const T* pb = a.unm1 + b * a.mstride;
-            for (int R = in_lo; R < in_hi; ++R, ++it) {
-                const int slot = int(it % depth);
-                if (it >= depth) mbar_wait(&empty[slot], uint32_t(((it / depth) - 1) & 1));
-                T* st = ring + size_t(slot) * 2 * WE;
-                mbar_arrive_expect_tx(&full[slot], 2 * WE * sizeof(T));
-                bulk_g2s(st, ub + R * a.pitch + cs - H, WE * sizeof(T), &full[slot]);
-                bulk_g2s(st + WE, pb + R * a.pitch + cs - H, WE * sizeof(T), &full[slot]);
+    // ---- producer state (thread 0): the stream of (item, input row) stages ----
+    int64_t p_item = blockIdx.x;
+    int p_R = 0, p_hi = 0, p_b = 0, p_slot = 0;
+    int64_t p_cs = 0;
+    if (tid == 0 && p_item < a.items) {
+        int s0, s1;
+        geom(p_item, p_cs, s0, s1, p_b, p_R, p_hi);
+    }
+    auto produce = [&]() {  // thread 0 only
+        if (p_item >= a.items) return;
+        T* st = ring + size_t(p_slot) * 2 * WE;
+        mbar_arrive_expect_tx(&full[p_slot], 2 * WE * sizeof(T));
+        bulk_g2s(st, a.un + p_b * a.mstride + p_R * a.pitch + p_cs - H, WE * sizeof(T), &full[p_slot]);
+        bulk_g2s(st + WE, a.unm1 + p_b * a.mstride + p_R * a.pitch + p_cs - H, WE * sizeof(T), &full[p_slot]);
+        if (++p_slot == depth) p_slot = 0;
+        if (++p_R == p_hi) {
+            p_item += gridDim.x;
+            if (p_item < a.items) {
+                int s0, s1;
+                geom(p_item, p_cs, s0, s1, p_b, p_R, p_hi);
             }
         }
-        return;
-    }
+    };
+    if (tid == 0)
+        for (int k = 0; k < depth; ++k) produce();
 
-    const int tid = threadIdx.x;
     const int e0 = tid * V;  // my first column of the extended strip
-    int64_t it = 0;
+    int cslot = 0;
+    uint32_t cphase = 0;
+    bool refill = false;     // a stage was consumed at the previous row
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
         int64_t cs;
         int s0, s1, b, in_lo, in_hi;
@@ -587,23 +596,28 @@ __global__ void __launch_bounds__((TB_NC + 1) * 32) k_step2d_tb(const TbArgs<T> 
         const int L = s1 + K - in_lo;
         for (int i = 0; i < L; ++i) {
             const int R = in_lo + i;
-            asm volatile("bar.sync 1, %0;" ::"r"(TB_NC * 32) : "memory");  // consumers only
+            __syncthreads();  // the previous row's stage and centre rows are consumed / published
+            if (tid == 0 && refill) {
+                fence_proxy_async_smem();  // generic reads of that stage before the async refill
+                produce();
+            }
             T nw[V], pv_new[V];
-            if (i < nload) {
-                const int slot = int(it % depth);
-                mbar_wait(&full[slot], uint32_t((it / depth) & 1));
-                const T* st = ring + size_t(slot) * 2 * WE;
+            refill = (i < nload);
+            if (refill) {
+                mbar_wait(&full[cslot], cphase);
+                const T* st = ring + size_t(cslot) * 2 * WE;
                 lds_vec(st + e0, nw);
                 lds_vec(st + WE + e0, pv_new);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
-                ++it;
+                if (++cslot == depth) {
+                    cslot = 0;
+                    cphase ^= 1u;
+                }
             } else {
 #pragma unroll
                 for (int k = 0; k < V; ++k) nw[k] = pv_new[k] = (T)0;
             }
             const int par = R & 1;
-            // level 0: window shift; its new row (R) is the next iteration's centre
+            // level 0: window shift; its new row (R) is the next row's centre
 #pragma unroll
             for (int k = 0; k < V; ++k) {
                 w[0][0][k] = w[0][1][k];

@@ -261,6 +261,7 @@ tsw_status tma_occupancy(tsw_ctx* c, int* occ_out, size_t* smem_out) {
     int& key = c->bulk_occ_key[MODE][START ? 1 : 0];
     if (ob == 0 || key != depth) {
         CK(cudaFuncSetAttribute(k_step2d_tma<T, MODE, START>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaFuncSetAttribute(k_step2d_tma<T, MODE, START>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_step2d_tma<T, MODE, START>, (TMA_NC + 1) * 32, smem));
         if (ob < 1) return fail(TSW_ERR_ARG, "TMA stencil does not fit on an SM (depth %d)", depth);
         key = depth;
@@ -349,7 +350,8 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1) {
     int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K];
     if (occ == 0) {
         CK(cudaFuncSetAttribute(k_step2d_tb<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K>, (TB_NC + 1) * 32, smem));
+        CK(cudaFuncSetAttribute(k_step2d_tb<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K>, TB_NC * 32, smem));
         if (occ < 1) return fail(TSW_ERR_ARG, "temporally blocked stencil (K=%d) does not fit on an SM", K);
     }
     TbArgs<T> a;
@@ -386,7 +388,7 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1) {
         if (st) return st;
         CK(cudaEventRecord(e0, c->stream));
     }
-    k_step2d_tb<T, K><<<unsigned(blocks), (TB_NC + 1) * 32, smem, c->stream>>>(a, depth);
+    k_step2d_tb<T, K><<<unsigned(blocks), TB_NC * 32, smem, c->stream>>>(a, depth);
     CKL();
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
@@ -403,6 +405,7 @@ tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1) {
         case 2: return launch_tb_t<T, 2>(c, fk, fkm1);
         case 3: return launch_tb_t<T, 3>(c, fk, fkm1);
         case 4: return launch_tb_t<T, 4>(c, fk, fkm1);
+        case 5: return launch_tb_t<T, 5>(c, fk, fkm1);
         case 6: return launch_tb_t<T, 6>(c, fk, fkm1);
         case 8: return launch_tb_t<T, 8>(c, fk, fkm1);
         default: return fail(TSW_ERR_ARG, "unsupported temporal blocking depth %d", K);
@@ -1587,8 +1590,8 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     if (key == TSW_OPT_TBLOCK) {
-        if (!(value == 1 || value == 2 || value == 3 || value == 4 || value == 6 || value == 8))
-            return fail(TSW_ERR_ARG, "temporal blocking depth must be 1, 2, 3, 4, 6 or 8");
+        if (!(value >= 1 && value <= 6) && value != 8)
+            return fail(TSW_ERR_ARG, "temporal blocking depth must be 1..6 or 8");
         if (value > 1 && (c->g.dim != 2 || c->g.nranks != 1))
             return fail(TSW_ERR_ARG, "temporal blocking needs a single-rank 2D grid");
         tsw_status st = set_dev(c);
