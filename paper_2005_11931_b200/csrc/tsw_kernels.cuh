@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace tsw {
 
 // PAPER.md §3.1, "c ≃ 2.2523 to get ∫φ = 1" (R4: 1/∫_{-1}^{1} e^{1/(x²−1)} dx).
@@ -30,6 +32,10 @@ __device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b
 template <typename T> struct Vec16;
 template <> struct Vec16<double> { using type = double2; static constexpr int N = 2; };
 template <> struct Vec16<float> { using type = float4; static constexpr int N = 4; };
+// two-element vectors (the temporally blocked kernel uses 2 columns per thread in both precisions)
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
 
 template <typename T>
 __device__ __forceinline__ void vload(const T* __restrict__ p, T (&v)[Vec16<T>::N]) {
@@ -473,12 +479,34 @@ constexpr int TB_NC = 8;
 
 template <typename T, int K>
 struct TbGeom {
-    static constexpr int V = Vec16<T>::N;
+    static constexpr int V = 2;                                  // columns per thread
     static constexpr int NT = TB_NC * 32;
-    static constexpr int H = ((K + V - 1) / V) * V;
-    static constexpr int WE = NT * V;
+    static constexpr int A = (16 / int(sizeof(T))) > V ? (16 / int(sizeof(T))) : V;  // 16-byte TMA alignment
+    static constexpr int H = ((K + A - 1) / A) * A;              // halo columns per side (≥ K)
+    static constexpr int WE = NT * V;                            // 512 columns
     static constexpr int WO = WE - 2 * H;
 };
+
+template <typename T>
+__device__ __forceinline__ void lds_v2(const T* p, T (&v)[2]) {
+    typename Vec2<T>::type x = *reinterpret_cast<const typename Vec2<T>::type*>(p);
+    v[0] = x.x;
+    v[1] = x.y;
+}
+template <typename T>
+__device__ __forceinline__ void sts_v2(T* p, const T (&v)[2]) {
+    typename Vec2<T>::type x;
+    x.x = v[0];
+    x.y = v[1];
+    *reinterpret_cast<typename Vec2<T>::type*>(p) = x;
+}
+template <typename T>
+__device__ __forceinline__ void stg_v2(T* p, const T (&v)[2]) {
+    typename Vec2<T>::type x;
+    x.x = v[0];
+    x.y = v[1];
+    __stcs(reinterpret_cast<typename Vec2<T>::type*>(p), x);
+}
 
 template <typename T>
 struct TbArgs {
@@ -496,10 +524,71 @@ struct TbArgs {
     T dtT;
 };
 
+// centre-row buffers are padded by one 16-byte vector on each side (zeros), so the left/right
+// neighbours of every thread are read without bounds checks
+template <typename T>
+struct TbPad {
+    static constexpr int P = 16 / sizeof(T);
+};
+
 template <typename T, int K>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
-    return size_t(depth) * 2 * TbGeom<T, K>::WE * sizeof(T) + size_t(K) * 2 * TbGeom<T, K>::WE * sizeof(T) +
-           size_t(depth) * sizeof(uint64_t);
+    return size_t(depth) * 2 * TbGeom<T, K>::WE * sizeof(T) +
+           size_t(K) * 2 * (TbGeom<T, K>::WE + 2 * TbPad<T>::P) * sizeof(T) + size_t(depth) * sizeof(uint64_t);
+}
+
+// Per-thread state of one item's wavefront.  Window slots rotate with the row phase PH ∈ {0,1,2}:
+// before row i (phase PH = i mod 3) level m holds rows (r−1, r, r+1) in slots (PH, PH+1, PH+2) mod 3;
+// its new row overwrites slot PH, so no register moves are needed.
+template <typename T, int K>
+struct TbState {
+    static constexpr int V = 2;
+    T w[K][3][V];
+    T pm1[V];
+    T c1l[V], c1r[V], c2v[V];
+    bool colint[V];
+};
+
+template <typename T, int K, int PH>
+__device__ __forceinline__ void tb_row(TbState<T, K>& S, T* __restrict__ cen, int e0, int rowlo, int rowhi, int R,
+                                       const T (&nw)[2], const T (&pv_new)[2], T dtT, T (&lastk)[2]) {
+    constexpr int V = 2;
+    constexpr int WEP = TbGeom<T, K>::WE + 2 * TbPad<T>::P;
+    constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
+    const int par = R & 1;
+    // level 0
+#pragma unroll
+    for (int k = 0; k < V; ++k) S.w[0][O][k] = nw[k];
+    sts_v2(cen + par * WEP + e0, nw);
+#pragma unroll
+    for (int m = 1; m <= K; ++m) {
+        // level m−1 after its update: rows (r−1, r, r+1) in slots (C, N, O); level m−2: row r in C
+        const bool rowok = unsigned(R - m - rowlo) <= unsigned(rowhi - rowlo);
+        const T* ce = cen + ((m - 1) * 2 + (par ^ 1)) * WEP + e0;
+        const T left = ce[-1];
+        const T right = ce[V];
+        T nv[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const T cu = S.w[m - 1][N][k];
+            const T ul = (k == 0) ? left : S.w[m - 1][N][k - 1];
+            const T ur = (k == V - 1) ? right : S.w[m - 1][N][k + 1];
+            const T pr = (m == 1) ? S.pm1[k] : S.w[(m >= 2) ? m - 2 : 0][C][k];
+            const T v = node_update<T, false, true>(cu, ul, ur, S.w[m - 1][C][k], S.w[m - 1][O][k], pr, S.c1l[k],
+                                                    S.c1r[k], S.c2v[k], S.c2v[k], dtT);
+            nv[k] = (rowok && S.colint[k]) ? v : (T)0;
+        }
+        if (m < K) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
+            sts_v2(cen + (m * 2 + par) * WEP + e0, nv);
+        } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) lastk[k] = nv[k];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) S.pm1[k] = pv_new[k];
 }
 
 // The producer is thread 0: at input row i it refills the stage consumed at row i − 1 (every
@@ -508,12 +597,14 @@ template <typename T, int K>
 __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
+    constexpr int PAD = TbPad<T>::P, WEP = WE + 2 * PAD;
     extern __shared__ __align__(128) unsigned char smem[];
-    T* ring = reinterpret_cast<T*>(smem);                 // [depth][2][WE]
-    T* cen = ring + size_t(depth) * 2 * WE;               // [K][2][WE]
-    uint64_t* full = reinterpret_cast<uint64_t*>(cen + size_t(K) * 2 * WE);
-    const int lane = threadIdx.x & 31;
+    T* ring = reinterpret_cast<T*>(smem);                    // [depth][2][WE]
+    T* cenp = ring + size_t(depth) * 2 * WE;                 // [K][2][WEP], row data at +PAD
+    uint64_t* full = reinterpret_cast<uint64_t*>(cenp + size_t(K) * 2 * WEP);
+    T* cen = cenp + PAD;
     const int tid = threadIdx.x;
+    for (int e = tid; e < K * 2 * WEP; e += blockDim.x) cenp[e] = (T)0;  // pads stay 0
     if (tid == 0) {
         for (int k = 0; k < depth; ++k) mbar_init(&full[k], 1);
         fence_barrier_init();
@@ -559,42 +650,44 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
         for (int k = 0; k < depth; ++k) produce();
 
     const int e0 = tid * V;  // my first column of the extended strip
+    // interior storage rows of the global grid: g ∈ [1, ny−2] ⇔ storage s ∈ [rowlo, rowhi]
+    const int rowlo = int(1 - a.r0 + 1), rowhi = int(a.ny - 2 - a.r0 + 1);
     int cslot = 0;
     uint32_t cphase = 0;
-    bool refill = false;     // a stage was consumed at the previous row
+    bool refill = false;  // a stage was consumed at the previous row
+    TbState<T, K> S;
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
         int64_t cs;
         int s0, s1, b, in_lo, in_hi;
         geom(item, cs, s0, s1, b, in_lo, in_hi);
         const int64_t gc0 = cs - H + e0;  // global column of my first element
-        bool colint[V];
-        T c1l[V], c1r[V], c2v[V];
         const T* c1b = a.c1 + b * a.cstride;
         const T* c2b = a.c2 + b * a.cstride;
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const int64_t gcol = gc0 + k;
-            colint[k] = (gcol >= 1) && (gcol <= a.nx - 2);
-            c1r[k] = colint[k] ? __ldg(c1b + gcol) : (T)0;
-            c1l[k] = colint[k] ? __ldg(c1b + gcol - 1) : (T)0;
-            c2v[k] = colint[k] ? __ldg(c2b + gcol) : (T)0;
+            S.colint[k] = (gcol >= 1) && (gcol <= a.nx - 2);
+            S.c1r[k] = S.colint[k] ? __ldg(c1b + gcol) : (T)0;
+            S.c1l[k] = S.colint[k] ? __ldg(c1b + gcol - 1) : (T)0;
+            S.c2v[k] = S.colint[k] ? __ldg(c2b + gcol) : (T)0;
         }
         const bool out_cols = (e0 >= H) && (e0 < H + WO) && (cs - H + e0 < a.pitch);
-        T* ok = a.out_k + b * a.mstride;
-        T* okm1 = a.out_km1 + b * a.mstride;
-        T w[K][3][V];  // level m window: rows (r−1, r, r+1) of its newest production
+        T* ok = a.out_k + b * a.mstride + gc0;
+        T* okm1 = a.out_km1 + b * a.mstride + gc0;
 #pragma unroll
         for (int m = 0; m < K; ++m)
 #pragma unroll
             for (int q = 0; q < 3; ++q)
 #pragma unroll
-                for (int k = 0; k < V; ++k) w[m][q][k] = (T)0;
-        T pm1[V];  // u^{n−1} at row R − 1
+                for (int k = 0; k < V; ++k) S.w[m][q][k] = (T)0;
 #pragma unroll
-        for (int k = 0; k < V; ++k) pm1[k] = (T)0;
+        for (int k = 0; k < V; ++k) S.pm1[k] = (T)0;
         const int nload = in_hi - in_lo;
         const int L = s1 + K - in_lo;
-        for (int i = 0; i < L; ++i) {
+
+        // one input row: barrier, refill, stage read, wavefront (phase PH), output
+        auto row = [&](auto ph, int i) {
+            constexpr int PH = decltype(ph)::value;
             const int R = in_lo + i;
             __syncthreads();  // the previous row's stage and centre rows are consumed / published
             if (tid == 0 && refill) {
@@ -606,8 +699,8 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
             if (refill) {
                 mbar_wait(&full[cslot], cphase);
                 const T* st = ring + size_t(cslot) * 2 * WE;
-                lds_vec(st + e0, nw);
-                lds_vec(st + WE + e0, pv_new);
+                lds_v2(st + e0, nw);
+                lds_v2(st + WE + e0, pv_new);
                 if (++cslot == depth) {
                     cslot = 0;
                     cphase ^= 1u;
@@ -616,71 +709,27 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
 #pragma unroll
                 for (int k = 0; k < V; ++k) nw[k] = pv_new[k] = (T)0;
             }
-            const int par = R & 1;
-            // level 0: window shift; its new row (R) is the next row's centre
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-                w[0][0][k] = w[0][1][k];
-                w[0][1][k] = w[0][2][k];
-                w[0][2][k] = nw[k];
-            }
-            {
-                using VT = typename Vec16<T>::type;
-                VT x;
-                T* e = reinterpret_cast<T*>(&x);
-#pragma unroll
-                for (int k = 0; k < V; ++k) e[k] = nw[k];
-                *reinterpret_cast<VT*>(cen + (size_t(0) * 2 + par) * WE + e0) = x;
-            }
             T lastk[V];
-#pragma unroll
-            for (int m = 1; m <= K; ++m) {
-                const int r = R - m;
-                const int64_t g = a.r0 + r - 1;
-                const bool rowint = (g >= 1) && (g <= a.ny - 2);
-                const T* ce = cen + (size_t(m - 1) * 2 + (par ^ 1)) * WE;
-                const T left = (e0 > 0) ? ce[e0 - 1] : (T)0;
-                const T right = (e0 + V < WE) ? ce[e0 + V] : (T)0;
-                T nv[V];
-#pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    const T cu = w[m - 1][1][k];
-                    const T ul = (k == 0) ? left : w[m - 1][1][k - 1];
-                    const T ur = (k == V - 1) ? right : w[m - 1][1][k + 1];
-                    const T pr = (m == 1) ? pm1[k] : w[(m >= 2) ? m - 2 : 0][0][k];
-                    const T v = node_update<T, false, true>(cu, ul, ur, w[m - 1][0][k], w[m - 1][2][k], pr, c1l[k],
-                                                            c1r[k], c2v[k], c2v[k], a.dtT);
-                    nv[k] = (rowint && colint[k]) ? v : (T)0;
-                }
-                if (m < K) {
-#pragma unroll
-                    for (int k = 0; k < V; ++k) {
-                        w[m][0][k] = w[m][1][k];
-                        w[m][1][k] = w[m][2][k];
-                        w[m][2][k] = nv[k];
-                    }
-                    using VT = typename Vec16<T>::type;
-                    VT x;
-                    T* e = reinterpret_cast<T*>(&x);
-#pragma unroll
-                    for (int k = 0; k < V; ++k) e[k] = nv[k];
-                    *reinterpret_cast<VT*>(cen + (size_t(m) * 2 + par) * WE + e0) = x;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < V; ++k) lastk[k] = nv[k];
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < V; ++k) pm1[k] = pv_new[k];
+            tb_row<T, K, PH>(S, cen, e0, rowlo, rowhi, R, nw, pv_new, a.dtT, lastk);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
+                // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH
+                constexpr int NS = (PH + 2) % 3;
                 T o2[V];
 #pragma unroll
-                for (int k = 0; k < V; ++k) o2[k] = w[K - 1][1][k];
-                vstore(ok + ro * a.pitch + gc0, lastk);
-                vstore(okm1 + ro * a.pitch + gc0, o2);
+                for (int k = 0; k < V; ++k) o2[k] = S.w[K - 1][NS][k];
+                stg_v2(ok + int64_t(ro) * a.pitch, lastk);
+                stg_v2(okm1 + int64_t(ro) * a.pitch, o2);
             }
+        };
+        int i = 0;
+        for (; i + 3 <= L; i += 3) {
+            row(std::integral_constant<int, 0>{}, i);
+            row(std::integral_constant<int, 1>{}, i + 1);
+            row(std::integral_constant<int, 2>{}, i + 2);
         }
+        if (i < L) row(std::integral_constant<int, 0>{}, i++);
+        if (i < L) row(std::integral_constant<int, 1>{}, i++);
     }
 }
 
