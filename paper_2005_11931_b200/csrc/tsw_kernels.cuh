@@ -476,6 +476,8 @@ __global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs
 // Every node value is the same canonical expression as k_step2d (bitwise identical results);
 // Dirichlet rows/columns are forced to +0 at every level.
 constexpr int TB_NC = 8;
+// ghost rows per side of a slab: the deepest temporal blocking (K = 8) exchanges 8 rows every 8 levels
+constexpr int TSW_MAX_GHOST = 8;
 
 template <typename T, int K>
 struct TbGeom {
@@ -813,6 +815,7 @@ struct CoeffArgs {
     int64_t r0;         // first global row of the slab
     int64_t rows_alloc, pitch, cpitch;
     int B;
+    int s_base;         // storage row of blockIdx.y = 0 (1 − G: the deepest ghost row)
 };
 
 // LINE (and CONST): h1[b][i], i < nx−1 (pad 0), h2[b] = h_b.
@@ -897,7 +900,7 @@ __global__ void k_coeff_profile(ProfileArgs a, double* __restrict__ h1, double* 
 // g = r0 + s − 1; entries outside the global grid are 0.
 __global__ void k_coeff_point(CoeffArgs a, double* __restrict__ h1, double* __restrict__ h2) {
     const int b = blockIdx.z;
-    const int64_t s = blockIdx.y;
+    const int64_t s = int64_t(blockIdx.y) + a.s_base;
     const int64_t g = a.r0 + s - 1;
     const double eps = a.eps[b], amp = a.amp[b];
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.pitch; i += int64_t(gridDim.x) * blockDim.x) {

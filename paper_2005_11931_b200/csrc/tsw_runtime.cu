@@ -104,16 +104,22 @@ int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
 // row's padding; for the first/last row of the array those bytes lie outside it (their values
 // are never used and never written).
 constexpr size_t GUARD = 16384;
-cudaError_t dmalloc_guarded(void** p, size_t bytes) {
+// `shift` bytes: the returned pointer is a VIEW that many bytes into the array (row-structured
+// arrays of slabs with G ghost rows per side are addressed so that storage row 1 is the first owned
+// row; ghost rows sit at rows 0, −1, …, 2 − G).
+// Zeroed on `stream` — never on the legacy default stream: the ctx streams are non-blocking, so a
+// legacy-stream memset would not be ordered before the ctx's own work (with another ctx keeping the
+// GPU busy it could land in the middle of it).
+cudaError_t dmalloc_guarded(void** p, size_t bytes, size_t shift, cudaStream_t stream) {
     void* raw = nullptr;
     cudaError_t e = cudaMalloc(&raw, bytes + 2 * GUARD);
     if (e != cudaSuccess) return e;
-    e = cudaMemset(raw, 0, bytes + 2 * GUARD);
-    *p = static_cast<char*>(raw) + GUARD;
+    e = cudaMemsetAsync(raw, 0, bytes + 2 * GUARD, stream);
+    *p = static_cast<char*>(raw) + GUARD + shift;
     return e;
 }
-void dfree_guarded(void* p) {
-    if (p) cudaFree(static_cast<char*>(p) - GUARD);
+void dfree_guarded(void* p, size_t shift = 0) {
+    if (p) cudaFree(static_cast<char*>(p) - GUARD - shift);
 }
 
 }  // namespace
@@ -128,6 +134,10 @@ struct tsw_ctx {
     int V = 2;
     // slab geometry
     int64_t r0 = 0, r1 = 0, ny_local = 1, rows_alloc = 1, pitch = 0, mstride = 0;
+    int G = 1;               // ghost rows per side (1 single-rank; TSW_MAX_GHOST for slabs)
+    size_t fshift = 0;       // view shift of field arrays in bytes: (G − 1)·pitch·esz
+    size_t cshift = 0;       // view shift of the current coefficient arrays (DENSE) per element size
+    size_t cshift_h = 0;     // … of the fp64 face arrays
     int32_t s_lo = 0, s_hi = 0;  // storage rows of updated nodes (2D)
     // time levels: buf[ic] = u^n, buf[ip] = u^{n−1}; buf[2], buf[3] exist only for the
     // temporally blocked stencil (out of place)
@@ -156,6 +166,7 @@ struct tsw_ctx {
     // state
     bool have_init = false;
     bool ghosts_valid = false;  // ghost rows of u^n hold the neighbours' rows
+    int gdepth[4] = {0, 0, 0, 0};  // ghost rows of each buffer that hold the neighbours' rows
     int64_t n = 0;
     double dt = 0.0;
     // scratch
@@ -343,7 +354,8 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
 
 // ---- temporally blocked pass: K levels, (buf[ic], buf[ip]) → (buf[fk], buf[fkm1]) -----------
 template <typename T, int K>
-tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1) {
+tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
+    if (s_hi <= s_lo) return TSW_OK;
     using G = TbGeom<T, K>;
     const int depth = c->tb_depth;
     const size_t smem = tb_smem_bytes<T, K>(depth);
@@ -367,13 +379,14 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1) {
     a.nx = c->g.nx;
     a.ny = c->g.ny;
     a.r0 = c->r0;
-    a.s_lo = c->s_lo;
-    a.s_hi = c->s_hi;
-    a.smin = 1;
-    a.smax = int32_t(c->ny_local);
+    a.s_lo = s_lo;
+    a.s_hi = s_hi;
+    // storage rows that hold data: the slab plus, towards a neighbour, its G ghost rows
+    a.smin = (c->g.rank > 0) ? 1 - c->G : 1;
+    a.smax = int32_t(c->ny_local) + ((c->g.rank < c->g.nranks - 1) ? c->G : 0);
     a.strips = (c->pitch + G::WO - 1) / G::WO;
     a.dtT = (T)c->dt;
-    const int64_t rows = c->s_hi - c->s_lo;
+    const int64_t rows = s_hi - s_lo;
     const int64_t Gw = int64_t(occ) * c->sm_count;
     int R = c->rows_per_item_opt;
     if (R <= 0) R = choose_rows_per_item(rows, a.strips, c->g.batch, Gw, 2.0 * K, 0.5, 4 * K);
@@ -400,29 +413,90 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1) {
 }
 
 template <typename T>
-tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1) {
+tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
     switch (K) {
-        case 2: return launch_tb_t<T, 2>(c, fk, fkm1);
-        case 3: return launch_tb_t<T, 3>(c, fk, fkm1);
-        case 4: return launch_tb_t<T, 4>(c, fk, fkm1);
-        case 5: return launch_tb_t<T, 5>(c, fk, fkm1);
-        case 6: return launch_tb_t<T, 6>(c, fk, fkm1);
-        case 8: return launch_tb_t<T, 8>(c, fk, fkm1);
+        case 2: return launch_tb_t<T, 2>(c, fk, fkm1, s_lo, s_hi);
+        case 3: return launch_tb_t<T, 3>(c, fk, fkm1, s_lo, s_hi);
+        case 4: return launch_tb_t<T, 4>(c, fk, fkm1, s_lo, s_hi);
+        case 5: return launch_tb_t<T, 5>(c, fk, fkm1, s_lo, s_hi);
+        case 6: return launch_tb_t<T, 6>(c, fk, fkm1, s_lo, s_hi);
+        case 8: return launch_tb_t<T, 8>(c, fk, fkm1, s_lo, s_hi);
         default: return fail(TSW_ERR_ARG, "unsupported temporal blocking depth %d", K);
     }
 }
 
-// One pass of K levels; afterwards u^n = buf[fk], u^{n−1} = buf[fkm1].
-tsw_status tb_pass(tsw_ctx* c) {
-    int free_ids[2], nf = 0;
+tsw_status exchange_nccl(tsw_ctx* c, void* field, cudaStream_t stream, int nrows);
+
+void free_pair(const tsw_ctx* c, int* fk, int* fkm1) {
+    int ids[2], nf = 0;
     for (int k = 0; k < 4 && nf < 2; ++k)
-        if (k != c->ic && k != c->ip) free_ids[nf++] = k;
-    const int fk = free_ids[0], fkm1 = free_ids[1];
-    tsw_status st = is_f64(c) ? launch_tb_k<double>(c, c->tblock, fk, fkm1) : launch_tb_k<float>(c, c->tblock, fk, fkm1);
-    if (st) return st;
+        if (k != c->ic && k != c->ip) ids[nf++] = k;
+    *fk = ids[0];
+    *fkm1 = ids[1];
+}
+
+tsw_status launch_tb_rows(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
+    return is_f64(c) ? launch_tb_k<double>(c, c->tblock, fk, fkm1, s_lo, s_hi)
+                     : launch_tb_k<float>(c, c->tblock, fk, fkm1, s_lo, s_hi);
+}
+
+// Output rows of a slab pass that neighbours need: the first / last K owned rows.
+struct TbSplit {
+    int32_t top_lo = 0, top_hi = 0, bot_lo = 0, bot_hi = 0, ilo = 0, ihi = 0;
+    bool split = false;
+};
+TbSplit tb_split(const tsw_ctx* c) {
+    TbSplit p;
+    const int K = c->tblock;
+    p.ilo = c->s_lo;
+    p.ihi = c->s_hi;
+    if (c->g.nranks == 1 || c->ny_local < 3 * K) return p;  // single rank / tiny slab: one launch
+    p.split = true;
+    if (c->g.rank > 0) {
+        p.top_lo = c->s_lo;
+        p.top_hi = c->s_lo + K;
+        p.ilo = p.top_hi;
+    }
+    if (c->g.rank < c->g.nranks - 1) {
+        p.bot_lo = c->s_hi - K;
+        p.bot_hi = c->s_hi;
+        p.ihi = p.bot_lo;
+    }
+    return p;
+}
+
+// One pass of K levels; afterwards u^n = buf[fk], u^{n−1} = buf[fkm1].  Slabs: the first/last K
+// owned rows first, then their K-row exchange (both levels) on the aux stream concurrently with
+// the interior rows (k-deep halos, one exchange per K levels).
+tsw_status tb_pass(tsw_ctx* c) {
+    int fk, fkm1;
+    free_pair(c, &fk, &fkm1);
+    const int K = c->tblock;
+    tsw_status st;
+    if (c->g.nranks == 1) {
+        if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
+    } else {
+        const TbSplit p = tb_split(c);
+        if (p.split) {
+            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi))) return st;
+            if ((st = launch_tb_rows(c, fk, fkm1, p.bot_lo, p.bot_hi))) return st;
+            CK(cudaEventRecord(c->ev_bnd, c->stream));
+            CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
+            if ((st = exchange_nccl(c, c->buf[fk], c->aux, K))) return st;
+            if ((st = exchange_nccl(c, c->buf[fkm1], c->aux, K))) return st;
+            CK(cudaEventRecord(c->ev_comm, c->aux));
+            if ((st = launch_tb_rows(c, fk, fkm1, p.ilo, p.ihi))) return st;
+            CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+        } else {
+            if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
+            if ((st = exchange_nccl(c, c->buf[fk], c->stream, K))) return st;
+            if ((st = exchange_nccl(c, c->buf[fkm1], c->stream, K))) return st;
+        }
+        c->gdepth[fk] = c->gdepth[fkm1] = K;
+    }
     c->ic = fk;
     c->ip = fkm1;
-    c->n += c->tblock;
+    c->n += K;
     return TSW_OK;
 }
 
@@ -489,50 +563,58 @@ tsw_status step1d_t(tsw_ctx* c, int64_t k) {
 // ---- ghost rows -------------------------------------------------------------------------------
 // NCCL: send my first owned row up to rank−1 and my last owned row down to rank+1; receive their
 // rows into my ghost rows (storage rows 0 and ny_local+1).  Rows are contiguous: no packing.
-tsw_status exchange_nccl(tsw_ctx* c, void* field, cudaStream_t stream = nullptr) {
+tsw_status exchange_nccl(tsw_ctx* c, void* field, cudaStream_t stream, int nrows) {
     if (!stream) stream = c->stream;
     if (c->g.nranks <= 1) return TSW_OK;
     if (!c->comm) return fail(TSW_ERR_STATE, "nranks > 1 but tsw_nccl_init was not called");
     Nccl& N = nccl();
     const int dt = is_f64(c) ? NCCL_F64 : NCCL_F32;
+    // nrows owned rows [1, nrows] go up and [ny_local − nrows + 1, ny_local] go down; the ghost rows
+    // [1 − nrows, 0] and [ny_local + 1, ny_local + nrows] receive (contiguous: one message each)
     char* base = static_cast<char*>(field);
     const size_t row = size_t(c->pitch) * c->esz;
+    const size_t cnt = (nrows == 1) ? size_t(c->g.nx) : size_t(nrows) * size_t(c->pitch);
+    const int64_t up_send = 1, up_recv = 1 - nrows, dn_send = c->ny_local - nrows + 1, dn_recv = c->ny_local + 1;
     NK(N.GroupStart());
     for (int b = 0; b < c->g.batch; ++b) {
         char* m = base + size_t(b) * c->mstride * c->esz;
         if (c->g.rank > 0) {
-            NK(N.Send(m + 1 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, stream));
-            NK(N.Recv(m + 0 * row, size_t(c->g.nx), dt, c->g.rank - 1, c->comm, stream));
+            NK(N.Send(m + up_send * int64_t(row), cnt, dt, c->g.rank - 1, c->comm, stream));
+            NK(N.Recv(m + up_recv * int64_t(row), cnt, dt, c->g.rank - 1, c->comm, stream));
         }
         if (c->g.rank < c->g.nranks - 1) {
-            NK(N.Send(m + size_t(c->ny_local) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, stream));
-            NK(N.Recv(m + size_t(c->ny_local + 1) * row, size_t(c->g.nx), dt, c->g.rank + 1, c->comm, stream));
+            NK(N.Send(m + dn_send * int64_t(row), cnt, dt, c->g.rank + 1, c->comm, stream));
+            NK(N.Recv(m + dn_recv * int64_t(row), cnt, dt, c->g.rank + 1, c->comm, stream));
         }
     }
     NK(N.GroupEnd());
     return TSW_OK;
 }
 
-// Loopback: ranks are ctxs on one device and stream; copy rows device-to-device.
-// level 0 = u^n (buf[ic]), 1 = u^{n−1} (buf[ip]).
-tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0, cudaStream_t stream = nullptr) {
-    if (!stream) stream = cs[0]->stream;
+// Loopback: ranks are ctxs on one device and stream; copy rows device-to-device.  bi = buffer
+// index (the same in every member of a lock-stepped group); nrows rows per direction.
+tsw_status exchange_loopback_buf(tsw_ctx** cs, int n, int bi, cudaStream_t stream, int nrows) {
     for (int r = 0; r + 1 < n; ++r) {
         tsw_ctx* a = cs[r];      // upper slab (smaller rows)
         tsw_ctx* b = cs[r + 1];  // lower slab
-        const size_t row_a = size_t(a->pitch) * a->esz;
-        const size_t row_b = size_t(b->pitch) * b->esz;
+        const int64_t row = int64_t(a->pitch) * int64_t(a->esz);
+        const size_t bytes = (nrows == 1) ? size_t(a->g.nx) * a->esz : size_t(nrows) * size_t(row);
         for (int m = 0; m < a->g.batch; ++m) {
-            char* ma = static_cast<char*>(a->buf[level ? a->ip : a->ic]) + size_t(m) * a->mstride * a->esz;
-            char* mb = static_cast<char*>(b->buf[level ? b->ip : b->ic]) + size_t(m) * b->mstride * b->esz;
-            // a's last owned row → b's ghost row 0 ; b's first owned row → a's ghost row ny_local+1
-            CK(cudaMemcpyAsync(mb, ma + size_t(a->ny_local) * row_a, size_t(a->g.nx) * a->esz, cudaMemcpyDeviceToDevice,
-                               stream));
-            CK(cudaMemcpyAsync(ma + size_t(a->ny_local + 1) * row_a, mb + row_b, size_t(b->g.nx) * b->esz,
+            char* ma = static_cast<char*>(a->buf[bi]) + size_t(m) * a->mstride * a->esz;
+            char* mb = static_cast<char*>(b->buf[bi]) + size_t(m) * b->mstride * b->esz;
+            // a's last nrows owned rows → b's upper ghost rows; b's first nrows → a's lower ghost rows
+            CK(cudaMemcpyAsync(mb + (1 - nrows) * row, ma + (a->ny_local - nrows + 1) * row, bytes,
                                cudaMemcpyDeviceToDevice, stream));
+            CK(cudaMemcpyAsync(ma + (a->ny_local + 1) * row, mb + 1 * row, bytes, cudaMemcpyDeviceToDevice, stream));
         }
     }
     return TSW_OK;
+}
+
+// level 0 = u^n (buf[ic]), 1 = u^{n−1} (buf[ip]).
+tsw_status exchange_loopback(tsw_ctx** cs, int n, int level = 0, cudaStream_t stream = nullptr, int nrows = 1) {
+    if (!stream) stream = cs[0]->stream;
+    return exchange_loopback_buf(cs, n, level ? cs[0]->ip : cs[0]->ic, stream, nrows);
 }
 
 tsw_status prescale_all(tsw_ctx* c) {
@@ -561,10 +643,11 @@ tsw_status prescale_all(tsw_ctx* c) {
 
 tsw_status alloc_coeff(tsw_ctx* c, int mode) {
     if (c->have_coeff && c->mode == mode) return TSW_OK;
-    dfree_guarded(c->h1);
-    dfree_guarded(c->h2);
-    dfree_guarded(c->c1);
-    dfree_guarded(c->c2);
+    CK(cudaStreamSynchronize(c->stream));  // queued work may still read the old arrays
+    dfree_guarded(c->h1, c->cshift_h);
+    dfree_guarded(c->h2, c->cshift_h);
+    dfree_guarded(c->c1, c->cshift);
+    dfree_guarded(c->c2, c->cshift);
     c->h1 = c->h2 = nullptr;
     c->c1 = c->c2 = nullptr;
     c->have_coeff = false;
@@ -577,12 +660,14 @@ tsw_status alloc_coeff(tsw_ctx* c, int mode) {
         c->cstride2 = c->mstride;
     }
     const size_t B = size_t(c->g.batch);
-    CK(dmalloc_guarded(reinterpret_cast<void**>(&c->h1), B * c->cstride1 * sizeof(double)));  // (guards: see GUARD)
-    CK(dmalloc_guarded(reinterpret_cast<void**>(&c->h2), B * c->cstride2 * sizeof(double)));
-    CK(dmalloc_guarded(&c->c1, B * c->cstride1 * c->esz));
-    CK(dmalloc_guarded(&c->c2, B * c->cstride2 * c->esz));
-    CK(cudaMemsetAsync(c->h1, 0, B * c->cstride1 * sizeof(double), c->stream));
-    CK(cudaMemsetAsync(c->h2, 0, B * c->cstride2 * sizeof(double), c->stream));
+    // DENSE arrays are row-structured like the fields: same ghost-row view shift
+    const size_t rows_shift = (mode == MODE_DENSE) ? size_t(c->G - 1) * size_t(c->pitch) : 0;
+    c->cshift_h = rows_shift * sizeof(double);
+    c->cshift = rows_shift * c->esz;
+    CK(dmalloc_guarded(reinterpret_cast<void**>(&c->h1), B * c->cstride1 * sizeof(double), c->cshift_h, c->stream));
+    CK(dmalloc_guarded(reinterpret_cast<void**>(&c->h2), B * c->cstride2 * sizeof(double), c->cshift_h, c->stream));
+    CK(dmalloc_guarded(&c->c1, B * c->cstride1 * c->esz, c->cshift, c->stream));
+    CK(dmalloc_guarded(&c->c2, B * c->cstride2 * c->esz, c->cshift, c->stream));
     return TSW_OK;
 }
 
@@ -668,7 +753,7 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     c->ic = 0;
     c->ip = 1;
     for (int k = 0; k < 4; ++k)
-        if (c->buf[k]) CK(cudaMemsetAsync(c->buf[k], 0, bytes, c->stream));
+        if (c->buf[k]) CK(cudaMemsetAsync(static_cast<char*>(c->buf[k]) - c->fshift, 0, bytes, c->stream));
     tsw_status st = load_field(c, c->buf[0], a, shared, on_device);
     if (st) return st;
     if (b) {
@@ -680,11 +765,13 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     c->dt = dt;
     if ((st = prescale_all(c))) return st;
     c->ghosts_valid = false;
+    for (int& d : c->gdepth) d = 0;
     if (c->g.dim == 2 && c->g.nranks > 1 && c->comm) {
         // ghost rows of both levels (the energy of (u^n, u^{n−1}) reads both; loopback groups
         // exchange in tsw_group_step instead)
-        if ((st = exchange_nccl(c, c->buf[0]))) return st;
-        if ((st = exchange_nccl(c, c->buf[1]))) return st;
+        if ((st = exchange_nccl(c, c->buf[0], c->stream, c->G))) return st;
+        if ((st = exchange_nccl(c, c->buf[1], c->stream, c->G))) return st;
+        c->gdepth[0] = c->gdepth[1] = c->G;
         c->ghosts_valid = true;
     }
     c->n = n;
@@ -736,13 +823,30 @@ tsw_status step_slab_overlapped(tsw_ctx* c) {
     if ((st = launch_boundary_rows(c, start))) return st;
     CK(cudaEventRecord(c->ev_bnd, c->stream));
     CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
-    if ((st = exchange_nccl(c, c->buf[c->ip], c->aux))) return st;
+    if ((st = exchange_nccl(c, c->buf[c->ip], c->aux, 1))) return st;
     CK(cudaEventRecord(c->ev_comm, c->aux));
     if ((st = launch_interior_rows(c, start))) return st;
     CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
     std::swap(c->ic, c->ip);
+    c->gdepth[c->ic] = 1;
     c->n++;
     return TSW_OK;
+}
+
+// Make the K outermost ghost rows of both current levels valid before temporally blocked passes.
+tsw_status ensure_ghosts_nccl(tsw_ctx* c, int K) {
+    tsw_status st;
+    for (int which : {c->ic, c->ip})
+        if (c->gdepth[which] < K) {
+            if ((st = exchange_nccl(c, c->buf[which], c->stream, K))) return st;
+            c->gdepth[which] = K;
+        }
+    return TSW_OK;
+}
+
+bool tb_usable(const tsw_ctx* c) {
+    return c->tblock > 1 && c->g.dim == 2 && c->mode == MODE_LINE && c->buf[2] && c->buf[3] &&
+           c->tblock <= c->G + (c->g.nranks == 1 ? 1 << 20 : 0);
 }
 
 // Two leapfrog levels captured once per (ic, ip) and replayed (single rank, n ≥ 1).
@@ -785,7 +889,17 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
     if (c->g.dim == 1) return is_f64(c) ? step1d_t<double>(c, k) : step1d_t<float>(c, k);
     tsw_status st;
     if (c->g.nranks > 1) {
-        for (int64_t s = 0; s < k; ++s)
+        int64_t s = 0;
+        if (c->n == 0) {
+            if ((st = step_slab_overlapped(c))) return st;
+            s = 1;
+        }
+        if (tb_usable(c) && s + c->tblock <= k) {
+            if ((st = ensure_ghosts_nccl(c, c->tblock))) return st;
+            for (; s + c->tblock <= k; s += c->tblock)
+                if ((st = tb_pass(c))) return st;
+        }
+        for (; s < k; ++s)
             if ((st = step_slab_overlapped(c))) return st;
         return TSW_OK;
     }
@@ -796,7 +910,7 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
         c->n++;
         s = 1;
     }
-    if (c->tblock > 1 && c->mode == MODE_LINE && c->buf[2] && c->buf[3])
+    if (tb_usable(c))
         for (; s + c->tblock <= k; s += c->tblock)
             if ((st = tb_pass(c))) return st;
     const bool graphs = c->use_graphs && !c->timing;
@@ -868,12 +982,14 @@ tsw_status tsw_create(const tsw_grid_desc* gd, tsw_ctx** out) {
         c->r0 = g.rank * base + std::min<int64_t>(g.rank, rem);
         c->r1 = c->r0 + base + (g.rank < rem ? 1 : 0);
         c->ny_local = c->r1 - c->r0;
-        c->rows_alloc = c->ny_local + 2;
+        c->G = (g.nranks > 1) ? TSW_MAX_GHOST : 1;
+        c->rows_alloc = c->ny_local + 2 * c->G;
         c->pitch = round_up(g.nx, 32 * c->V);
         c->s_lo = (c->r0 == 0) ? 2 : 1;
         c->s_hi = int32_t((c->r1 == g.ny) ? c->ny_local : c->ny_local + 1);
     }
     c->mstride = c->rows_alloc * c->pitch;
+    c->fshift = size_t(c->G - 1) * size_t(c->pitch) * c->esz;
     if (g.stream) {
         c->stream = static_cast<cudaStream_t>(g.stream);
     } else {
@@ -891,11 +1007,11 @@ tsw_status tsw_create(const tsw_grid_desc* gd, tsw_ctx** out) {
     }
     const size_t bytes = size_t(g.batch) * c->mstride * c->esz;
     for (int k = 0; k < 2; ++k) {
-        e = dmalloc_guarded(&c->buf[k], bytes);
+        e = dmalloc_guarded(&c->buf[k], bytes, c->fshift, c->stream);
         if (e != cudaSuccess)
             return bail(fail(e == cudaErrorMemoryAllocation ? TSW_ERR_OOM : TSW_ERR_CUDA, "cudaMalloc(%zu): %s", bytes,
                              cudaGetErrorString(e)));
-        cudaMemsetAsync(c->buf[k], 0, bytes, c->stream);
+        cudaMemsetAsync(static_cast<char*>(c->buf[k]) - c->fshift, 0, bytes, c->stream);
     }
     c->nblk_red = 4096;  // partials per member (energy / wave2 reductions)
     if (cudaMalloc(&c->d_partial, sizeof(double) * size_t(g.batch) * c->nblk_red) != cudaSuccess ||
@@ -916,11 +1032,11 @@ void tsw_destroy(tsw_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    for (int k = 0; k < 4; ++k) dfree_guarded(c->buf[k]);
-    dfree_guarded(c->h1);
-    dfree_guarded(c->h2);
-    dfree_guarded(c->c1);
-    dfree_guarded(c->c2);
+    for (int k = 0; k < 4; ++k) dfree_guarded(c->buf[k], c->fshift);
+    dfree_guarded(c->h1, c->cshift_h);
+    dfree_guarded(c->h2, c->cshift_h);
+    dfree_guarded(c->c1, c->cshift);
+    dfree_guarded(c->c2, c->cshift);
     void* ptrs[] = {c->d_eps, c->d_amp, c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64, c->d_prof, c->d_fam};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -972,10 +1088,12 @@ tsw_status tsw_set_coeff(tsw_ctx* c, const tsw_coeff_desc* h) {
     a.pitch = c->pitch;
     a.cpitch = c->cstride1;
     a.B = c->g.batch;
+    a.s_base = 0;
     if (mode == MODE_LINE) {
         dim3 grid(unsigned(grid_for(c->cstride1, 256, 4 * c->sm_count)), unsigned(c->g.batch));
         k_coeff_line<<<grid, 256, 0, c->stream>>>(a, c->h1, c->h2);
     } else {
+        a.s_base = 1 - c->G;
         dim3 grid(unsigned(grid_for(c->pitch, 256, 64)), unsigned(c->rows_alloc), unsigned(c->g.batch));
         k_coeff_point<<<grid, 256, 0, c->stream>>>(a, c->h1, c->h2);
     }
@@ -1026,7 +1144,7 @@ tsw_status tsw_set_coeff_profile(tsw_ctx* c, const tsw_profile_desc* p, const do
     for (int k = 0; k < p->nsing; ++k) data.push_back(double(p->sing_order[k]));
     double* d_data = nullptr;
     CK(cudaMalloc(&d_data, std::max<size_t>(1, data.size()) * sizeof(double)));
-    CK(cudaMemcpy(d_data, data.data(), data.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(d_data, data.data(), data.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_eps, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_amp, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, c->stream));
     ProfileArgs a;
@@ -1093,10 +1211,11 @@ tsw_status tsw_set_coeff_faces(tsw_ctx* c, const double* h1, const double* h2, i
         CK(cudaMemcpy2DAsync(c->h1, c->cstride1 * sizeof(double), h1, (nx - 1) * sizeof(double), (nx - 1) * sizeof(double),
                              B, kind, c->stream));
         std::vector<double> hb(B * c->cstride2, 1.0);  // unused in 1D (no y faces)
-        CK(cudaMemcpy(c->h2, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(c->h2, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // hb is a local
     } else {
-        CK(cudaMemsetAsync(c->h1, 0, B * c->cstride1 * sizeof(double), c->stream));
-        CK(cudaMemsetAsync(c->h2, 0, B * c->cstride2 * sizeof(double), c->stream));
+        CK(cudaMemsetAsync(reinterpret_cast<char*>(c->h1) - c->cshift_h, 0, B * c->cstride1 * sizeof(double), c->stream));
+        CK(cudaMemsetAsync(reinterpret_cast<char*>(c->h2) - c->cshift_h, 0, B * c->cstride2 * sizeof(double), c->stream));
         const size_t rows = size_t(c->ny_local);
         for (size_t b = 0; b < B; ++b) {
             // h1 local row j → storage row j+1 ; h2 row k (face between global rows r0+k−1 and
@@ -1196,36 +1315,96 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
             return fail(TSW_ERR_ARG, "group member %d must be rank %d of %d (2D)", r, r, n);
         if (cs[r]->stream != cs[0]->stream || cs[r]->device != cs[0]->device)
             return fail(TSW_ERR_ARG, "loopback group members must share one device and stream");
-        if (cs[r]->n != cs[0]->n) return fail(TSW_ERR_STATE, "group members are at different levels");
+        if (cs[r]->n != cs[0]->n || cs[r]->ic != cs[0]->ic || cs[r]->ip != cs[0]->ip)
+            return fail(TSW_ERR_STATE, "group members are at different levels");
+        if (cs[r]->tblock != cs[0]->tblock || tb_usable(cs[r]) != tb_usable(cs[0]))
+            return fail(TSW_ERR_ARG, "group members must share the temporal blocking setting");
     }
-    tsw_status st = set_dev(cs[0]);
+    tsw_ctx* c0 = cs[0];
+    tsw_status st = set_dev(c0);
     if (st) return st;
     bool need = false;
     for (int r = 0; r < n; ++r) need = need || !cs[r]->ghosts_valid;
     if (need) {
         // ghost rows of both levels (set_initial / set_state cannot exchange without NCCL)
-        if ((st = exchange_loopback(cs, n, 0))) return st;
-        if ((st = exchange_loopback(cs, n, 1))) return st;
-        for (int r = 0; r < n; ++r) cs[r]->ghosts_valid = true;
-    }
-    // the slab schedule of step_slab_overlapped, with device copies on the aux stream
-    tsw_ctx* c0 = cs[0];
-    for (int64_t s = 0; s < nsteps; ++s) {
-        const bool start = (c0->n == 0);
-        for (int r = 0; r < n; ++r)
-            if ((st = launch_boundary_rows(cs[r], start))) return st;
-        CK(cudaEventRecord(c0->ev_bnd, c0->stream));
-        CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
-        if ((st = exchange_loopback(cs, n, 1, c0->aux))) return st;
-        CK(cudaEventRecord(c0->ev_comm, c0->aux));
-        for (int r = 0; r < n; ++r)
-            if ((st = launch_interior_rows(cs[r], start))) return st;
-        CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
+        if ((st = exchange_loopback(cs, n, 0, c0->stream, c0->G))) return st;
+        if ((st = exchange_loopback(cs, n, 1, c0->stream, c0->G))) return st;
         for (int r = 0; r < n; ++r) {
-            std::swap(cs[r]->ic, cs[r]->ip);
-            cs[r]->n++;
+            cs[r]->ghosts_valid = true;
+            cs[r]->gdepth[cs[r]->ic] = cs[r]->gdepth[cs[r]->ip] = c0->G;
         }
     }
+    auto advance = [&](int nic, int nip, int levels, int depth) {
+        for (int r = 0; r < n; ++r) {
+            cs[r]->ic = nic;
+            cs[r]->ip = nip;
+            cs[r]->n += levels;
+            cs[r]->gdepth[nic] = depth;
+            if (levels > 1) cs[r]->gdepth[nip] = depth;
+        }
+    };
+    // one level with the schedule of step_slab_overlapped, device copies on the aux stream
+    auto single = [&]() -> tsw_status {
+        const bool start = (c0->n == 0);
+        tsw_status e;
+        for (int r = 0; r < n; ++r)
+            if ((e = launch_boundary_rows(cs[r], start))) return e;
+        CK(cudaEventRecord(c0->ev_bnd, c0->stream));
+        CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
+        if ((e = exchange_loopback(cs, n, 1, c0->aux, 1))) return e;
+        CK(cudaEventRecord(c0->ev_comm, c0->aux));
+        for (int r = 0; r < n; ++r)
+            if ((e = launch_interior_rows(cs[r], start))) return e;
+        CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
+        advance(c0->ip, c0->ic, 1, 1);
+        return TSW_OK;
+    };
+    int64_t s = 0;
+    if (c0->n == 0 && nsteps > 0) {
+        if ((st = single())) return st;
+        s = 1;
+    }
+    const int K = c0->tblock;
+    if (tb_usable(c0) && s + K <= nsteps) {
+        for (int lv = 0; lv < 2; ++lv) {
+            const int bi = lv ? c0->ip : c0->ic;
+            if (c0->gdepth[bi] < K) {
+                if ((st = exchange_loopback_buf(cs, n, bi, c0->stream, K))) return st;
+                for (int r = 0; r < n; ++r) cs[r]->gdepth[bi] = K;
+            }
+        }
+        bool split = true;
+        for (int r = 0; r < n; ++r) split = split && tb_split(cs[r]).split;
+        for (; s + K <= nsteps; s += K) {
+            int fk, fkm1;
+            free_pair(c0, &fk, &fkm1);
+            if (split) {
+                for (int r = 0; r < n; ++r) {
+                    const TbSplit p = tb_split(cs[r]);
+                    if ((st = launch_tb_rows(cs[r], fk, fkm1, p.top_lo, p.top_hi))) return st;
+                    if ((st = launch_tb_rows(cs[r], fk, fkm1, p.bot_lo, p.bot_hi))) return st;
+                }
+                CK(cudaEventRecord(c0->ev_bnd, c0->stream));
+                CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
+                if ((st = exchange_loopback_buf(cs, n, fk, c0->aux, K))) return st;
+                if ((st = exchange_loopback_buf(cs, n, fkm1, c0->aux, K))) return st;
+                CK(cudaEventRecord(c0->ev_comm, c0->aux));
+                for (int r = 0; r < n; ++r) {
+                    const TbSplit p = tb_split(cs[r]);
+                    if ((st = launch_tb_rows(cs[r], fk, fkm1, p.ilo, p.ihi))) return st;
+                }
+                CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
+            } else {
+                for (int r = 0; r < n; ++r)
+                    if ((st = launch_tb_rows(cs[r], fk, fkm1, cs[r]->s_lo, cs[r]->s_hi))) return st;
+                if ((st = exchange_loopback_buf(cs, n, fk, c0->stream, K))) return st;
+                if ((st = exchange_loopback_buf(cs, n, fkm1, c0->stream, K))) return st;
+            }
+            advance(fk, fkm1, K, K);
+        }
+    }
+    for (; s < nsteps; ++s)
+        if ((st = single())) return st;
     return TSW_OK;
 }
 
@@ -1430,7 +1609,7 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
         e = cudaMemcpyAsync(h.data(), d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         for (double& v : h) v = v * v;
-        if (e == cudaSuccess) e = cudaMemcpy(d_sum, h.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_sum, h.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice, c->stream);
         int r = (e == cudaSuccess) ? nccl().AllReduce(d_sum, d_sum, size_t(B) * B, NCCL_F64, NCCL_SUM, c->comm, c->stream) : 0;
         if (r != 0) {
             cudaFree(d_sum);
@@ -1440,7 +1619,8 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
         if (e == cudaSuccess) e = cudaMemcpyAsync(g.data(), d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         for (size_t k = 0; k < g.size(); ++k) g[k] = std::sqrt(g[k]);
-        if (e == cudaSuccess) e = cudaMemcpy(d_sum, g.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_sum, g.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);  // g is a local
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_BB, d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -1534,7 +1714,7 @@ tsw_status tsw_coeff_norms(tsw_ctx* c, double* out_B3) {
     for (size_t k = 0; k < bits.size(); ++k) memcpy(&out_B3[k], &bits[k], sizeof(double));
     if (c->g.nranks > 1 && c->comm) {
         double* dd = reinterpret_cast<double*>(d);
-        CK(cudaMemcpy(dd, out_B3, sizeof(double) * bits.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(dd, out_B3, sizeof(double) * bits.size(), cudaMemcpyHostToDevice, c->stream));
         NK(nccl().AllReduce(dd, dd, bits.size(), NCCL_F64, NCCL_MAX, c->comm, c->stream));
         CK(cudaMemcpyAsync(out_B3, dd, sizeof(double) * bits.size(), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1592,18 +1772,19 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
     if (key == TSW_OPT_TBLOCK) {
         if (!(value >= 1 && value <= 6) && value != 8)
             return fail(TSW_ERR_ARG, "temporal blocking depth must be 1..6 or 8");
-        if (value > 1 && (c->g.dim != 2 || c->g.nranks != 1))
-            return fail(TSW_ERR_ARG, "temporal blocking needs a single-rank 2D grid");
+        if (value > 1 && c->g.dim != 2) return fail(TSW_ERR_ARG, "temporal blocking needs a 2D grid");
+        if (value > 1 && c->g.nranks > 1 && value > c->G)
+            return fail(TSW_ERR_ARG, "temporal blocking depth %d exceeds the %d ghost rows of a slab", int(value), c->G);
         tsw_status st = set_dev(c);
         if (st) return st;
         if (value > 1 && !c->buf[2]) {
             // two more levels for the out-of-place passes (zeroed: boundaries stay +0)
             const size_t bytes = size_t(c->g.batch) * c->mstride * c->esz;
             for (int k = 2; k < 4; ++k) {
-                cudaError_t e = dmalloc_guarded(&c->buf[k], bytes);
+                cudaError_t e = dmalloc_guarded(&c->buf[k], bytes, c->fshift, c->stream);
                 if (e != cudaSuccess) {
                     for (int j = 2; j < 4; ++j) {
-                        dfree_guarded(c->buf[j]);
+                        dfree_guarded(c->buf[j], c->fshift);
                         c->buf[j] = nullptr;
                     }
                     return fail(e == cudaErrorMemoryAllocation ? TSW_ERR_OOM : TSW_ERR_CUDA, "TB buffers: %s",
