@@ -6,7 +6,9 @@ Workload: config 4's weak-scaling unit (R22) — a 32768 × 4096
 GPU (global grid 32768 × 4096·N, dx = dy = 0.0025, ε = 0.05, dt = 4e−4), dense uniform [−1, 1]
 data (SURVEY §8(d) data-independence guard), fp64 by default.  One "step" = one pass of the
 hot path over the slab: the leapfrog stencil (S3), the NCCL ghost-row exchange at N > 1 (S4),
-and the discrete-energy reduction every `--energy-every` steps (S5).  Inputs (2 × 1.07 GB per
+and the discrete-energy reduction every `--energy-every` steps (S5).  By default the stencil is
+temporally blocked (`--tblock 5`: 5 levels per HBM pass, K-deep ghost rows exchanged every 5
+levels on slabs); `--tblock 1` times the one-level-per-pass kernel.  Inputs (2 × 1.07 GB per
 GPU in fp64) exceed the 126 MB L2, so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f64|f32] [--impl tsw|reference]
@@ -298,7 +300,7 @@ def main():
         torch.cuda.empty_cache()
         return res
 
-    tblock = args.tblock if world == 1 else 1  # slabs exchange one ghost row per level
+    tblock = args.tblock  # slabs exchange K ghost rows of both levels every K levels
     main_res = run(args.dtype, True)
     other = "f32" if args.dtype == "f64" else "f64"
     also = None if args.no_also else run(other, False)

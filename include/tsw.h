@@ -216,7 +216,7 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
 #define TSW_OPT_TBLOCK 6 /* K ∈ {1,…,6, 8}: levels per HBM pass of the temporally blocked stencil
                             (single-rank 2D, δ-line / constant / profile kinds; allocates two more
                             levels; results are bitwise those of K = 1).  Default 1. */
-#define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil, 2..16 (default 4) */
+#define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil, 3..16 (default 4) */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
 
 /* Live per-kernel timing of the stencil (S2/S3) launches recorded since TSW_OPT_TIME_KERNELS was

@@ -542,10 +542,16 @@ __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
 // Per-thread state of one item's wavefront.  Window slots rotate with the row phase PH ∈ {0,1,2}:
 // before row i (phase PH = i mod 3) level m holds rows (r−1, r, r+1) in slots (PH, PH+1, PH+2) mod 3;
 // its new row overwrites slot PH, so no register moves are needed.
+// caching the upper y-flux for the next row saves 2 ops per update but costs 2V registers per
+// level: on for fp32 (spare registers), off for fp64 (it would spill at K = 5)
+template <typename T> struct TbYCache { static constexpr bool on = sizeof(T) == 4; };
+
 template <typename T, int K>
 struct TbState {
     static constexpr int V = 2;
     T w[K][3][V];
+    T gup[TbYCache<T>::on ? K + 1 : 1][V];  // level m's y-flux c2·(u_{r+1} − u_r) of level m−1 at its last row r: the next
+                      // row's lower flux (identical operands, so the tree is unchanged bit for bit)
     T pm1[V];
     T c1l[V], c1r[V], c2v[V];
     bool colint[V];
@@ -569,15 +575,30 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, T* __restrict__ cen, in
         const T* ce = cen + ((m - 1) * 2 + (par ^ 1)) * WEP + e0;
         const T left = ce[-1];
         const T right = ce[V];
+        // canonical tree with shared face fluxes:
+        //   F_{i+1/2} = c1_{i+1/2}·(u_{i+1} − u_i) is node i's right and node i+1's left x-flux,
+        //   G_{j+1/2} = c2·(u_{j+1} − u_j) is row j's upper and row j+1's lower y-flux
+        //   lap = (F_{i+1/2} − F_{i−1/2}) + (G_{j+1/2} − G_{j−1/2});  u' = (2u − p) + lap
+        const T u0 = S.w[m - 1][N][0], u1 = S.w[m - 1][N][1];
+        const T F0 = r_mul(S.c1l[0], r_sub(u0, left));
+        const T F1 = r_mul(S.c1r[0], r_sub(u1, u0));
+        const T F2 = r_mul(S.c1r[1], r_sub(right, u1));
         T nv[V];
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const T cu = S.w[m - 1][N][k];
-            const T ul = (k == 0) ? left : S.w[m - 1][N][k - 1];
-            const T ur = (k == V - 1) ? right : S.w[m - 1][N][k + 1];
+            const T gu = r_mul(S.c2v[k], r_sub(S.w[m - 1][O][k], cu));
+            T gd;
+            if (TbYCache<T>::on) {
+                gd = S.gup[m][k];
+                S.gup[m][k] = gu;
+            } else {
+                gd = r_mul(S.c2v[k], r_sub(cu, S.w[m - 1][C][k]));
+            }
+            const T lapx = (k == 0) ? r_sub(F1, F0) : r_sub(F2, F1);
+            const T lap = r_add(lapx, r_sub(gu, gd));
             const T pr = (m == 1) ? S.pm1[k] : S.w[(m >= 2) ? m - 2 : 0][C][k];
-            const T v = node_update<T, false, true>(cu, ul, ur, S.w[m - 1][C][k], S.w[m - 1][O][k], pr, S.c1l[k],
-                                                    S.c1r[k], S.c2v[k], S.c2v[k], dtT);
+            const T v = r_add(r_sub(r_mul((T)2, cu), pr), lap);
             nv[k] = (rowok && S.colint[k]) ? v : (T)0;
         }
         if (m < K) {
@@ -593,8 +614,9 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, T* __restrict__ cen, in
     for (int k = 0; k < V; ++k) S.pm1[k] = pv_new[k];
 }
 
-// The producer is thread 0: at input row i it refills the stage consumed at row i − 1 (every
-// thread has passed the per-row barrier, so that stage is free) with the stream's stage i − 1 + D.
+// The producer is thread 0: after every second input row it refills the two stages consumed by
+// the previous rows (every thread has passed the per-row barrier, so they are free) with the next
+// stages of its stream (needs a ring of ≥ 3 stages).
 template <typename T, int K>
 __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K>;
@@ -656,7 +678,7 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
     const int rowlo = int(1 - a.r0 + 1), rowhi = int(a.ny - 2 - a.r0 + 1);
     int cslot = 0;
     uint32_t cphase = 0;
-    bool refill = false;  // a stage was consumed at the previous row
+    int pending = 0;  // stages consumed but not yet refilled (thread 0's count is the one used)
     TbState<T, K> S;
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
         int64_t cs;
@@ -669,8 +691,10 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
         for (int k = 0; k < V; ++k) {
             const int64_t gcol = gc0 + k;
             S.colint[k] = (gcol >= 1) && (gcol <= a.nx - 2);
-            S.c1r[k] = S.colint[k] ? __ldg(c1b + gcol) : (T)0;
-            S.c1l[k] = S.colint[k] ? __ldg(c1b + gcol - 1) : (T)0;
+            // face coefficients wherever the face exists (the shared x-flux of column k's right face
+            // is column k+1's left flux even when column k is a boundary node)
+            S.c1r[k] = (gcol >= 0 && gcol <= a.nx - 2) ? __ldg(c1b + gcol) : (T)0;
+            S.c1l[k] = (gcol >= 1 && gcol <= a.nx - 1) ? __ldg(c1b + gcol - 1) : (T)0;
             S.c2v[k] = S.colint[k] ? __ldg(c2b + gcol) : (T)0;
         }
         const bool out_cols = (e0 >= H) && (e0 < H + WO) && (cs - H + e0 < a.pitch);
@@ -684,6 +708,11 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
                 for (int k = 0; k < V; ++k) S.w[m][q][k] = (T)0;
 #pragma unroll
         for (int k = 0; k < V; ++k) S.pm1[k] = (T)0;
+        if (TbYCache<T>::on)
+#pragma unroll
+            for (int m = 0; m <= (TbYCache<T>::on ? K : 0); ++m)
+#pragma unroll
+                for (int k = 0; k < V; ++k) S.gup[m][k] = (T)0;
         const int nload = in_hi - in_lo;
         const int L = s1 + K - in_lo;
 
@@ -691,13 +720,17 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
         auto row = [&](auto ph, int i) {
             constexpr int PH = decltype(ph)::value;
             const int R = in_lo + i;
-            __syncthreads();  // the previous row's stage and centre rows are consumed / published
-            if (tid == 0 && refill) {
-                fence_proxy_async_smem();  // generic reads of that stage before the async refill
+            __syncthreads();  // the previous rows' stages and centre rows are consumed / published
+            // refill the consumed stages two at a time (their shared-memory reads completed before
+            // this barrier: the values were used in the previous rows' arithmetic)
+            if (tid == 0 && pending >= 2) {
                 produce();
+                produce();
+                pending = 0;
             }
             T nw[V], pv_new[V];
-            refill = (i < nload);
+            const bool refill = (i < nload);
+            pending += refill ? 1 : 0;
             if (refill) {
                 mbar_wait(&full[cslot], cphase);
                 const T* st = ring + size_t(cslot) * 2 * WE;

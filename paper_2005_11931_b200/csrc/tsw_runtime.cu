@@ -1796,7 +1796,7 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     if (key == TSW_OPT_TB_DEPTH) {
-        if (value < 2 || value > 16) return fail(TSW_ERR_ARG, "TB ring depth must be in [2, 16]");
+        if (value < 3 || value > 16) return fail(TSW_ERR_ARG, "TB ring depth must be in [3, 16]");
         c->tb_depth = int(value);
         for (auto& r : c->tb_occ)
             for (int& o : r) o = 0;

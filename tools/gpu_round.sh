@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python tools/debug_tb.py > gpurun_out/stress.log 2>&1; cat gpurun_out/stress.log
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$?
-grep -E "passed|failed|^E |FAILED" gpurun_out/pytest_gpu.log | head -10
-for k in 1 2 3; do timeout 600 python -m pytest tests/test_tblock_gpu.py::test_tblock_bench_shape_sampled -q -p no:cacheprovider 2>&1 | tail -1; done
+timeout 900 python -m pytest tests/test_tblock_gpu.py -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_tb.log 2>&1; echo pytest_exit=$?
+grep -E "passed|failed|^E |FAILED" gpurun_out/pytest_tb.log | head -10
+timeout 600 python tools/sweep.py --dtype f64 --depths 4 --tblocks 4,5 --tbdepths 4,6 > gpurun_out/sweep_tb64.log 2>&1; cat gpurun_out/sweep_tb64.log
+timeout 600 python tools/sweep.py --dtype f32 --depths 4 --tblocks 5,6,8 --tbdepths 4 > gpurun_out/sweep_tb32.log 2>&1; cat gpurun_out/sweep_tb32.log
