@@ -177,6 +177,10 @@ def run_reference(args, cfg, rank: int, world: int):
 
 
 def workload_name(cfg, world: int) -> str:
+    if cfg.batch > 1:
+        return f"config5_eps_family_{cfg.batch}x{cfg.nx}x{cfg.ny // world}_per_gpu"
+    if cfg.name.startswith("config3"):
+        return f"config3_delta_line_{cfg.nx}x{cfg.ny // world}_per_gpu"
     return f"config4_weak_unit_delta_line_{cfg.nx}x{cfg.ny // world}_per_gpu"
 
 
@@ -195,13 +199,21 @@ def main():
     ap.add_argument("--no-also", action="store_true", help="skip the second-precision line item")
     ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--rows-per-item", type=int, default=0)
+    ap.add_argument("--workload", choices=["config4", "config5", "config3"], default="config4",
+                    help="config4: the weak-scaling unit (default, the BASELINE metric's scaling "
+                         "workload); config5: 65-member eps family x 2048^2; config3: 4096^2 delta line")
     ap.add_argument("--tblock", type=int, default=5,
                     help="levels per HBM pass of the temporally blocked stencil (1 = per-step TMA kernel)")
     args = ap.parse_args()
 
     from paper_2005_11931_b200 import inputs, parallel
     rank, world, local = parallel.env_rank()
-    cfg = inputs.weak_unit(world, rows_per_rank=args.rows_per_gpu, nx=args.nx)
+    if args.workload == "config5":
+        cfg = inputs.config(5, ny=2048 * world)
+    elif args.workload == "config3":
+        cfg = inputs.config(3, ny=4096 * world)
+    else:
+        cfg = inputs.weak_unit(world, rows_per_rank=args.rows_per_gpu, nx=args.nx)
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
@@ -225,6 +237,7 @@ def main():
         parallel.nccl_bootstrap(s)
         r0, r1 = parallel.slab(cfg.ny, rank, world)
         u0_host = torch.from_numpy(inputs.uniform_dense_rows(cfg.nx, cfg.ny, r0, r1 - r0).astype(npdt)).pin_memory()
+        # (config 5: every member starts from the same field — TSW_INIT_SHARED)
         u0_dev = u0_host.to(dev)
         torch.cuda.synchronize()
         s.set_initial(u0_dev, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
@@ -267,13 +280,13 @@ def main():
             ms, kavg = float(t[0]), float(t[1])
         else:
             kavg = kms / max(klaunch, 1)
-        updates = (cfg.nx - 2) * (cfg.ny - 2) * args.steps
+        updates = (cfg.nx - 2) * (cfg.ny - 2) * cfg.batch * args.steps
         res = {"ms": ms, "value": updates / (ms * 1e-3) / 1e9, "launches": launches, "kernel_avg_ms": kavg,
                "kernel_updates_per_launch": kupd / max(klaunch, 1), "clocks": clocks.stop() if clocks else None}
         if full and not args.no_e2e:
             # e2e through the public API with host buffers: H2D of u0 (pinned), K steps (+ energy),
             # D2H of u^K — all inside the timed region.
-            out_host = torch.empty_like(u0_host).pin_memory()
+            out_host = torch.empty((cfg.batch, r1 - r0, cfg.nx), dtype=u0_host.dtype).pin_memory()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -286,15 +299,16 @@ def main():
                 done += k
                 if args.energy_every > 0 and done % args.energy_every == 0:
                     s.energy()
-            s.read(0, out_host.numpy().reshape(1, r1 - r0, cfg.nx))
+            s.read(0, out_host.numpy())
             el = time.perf_counter() - t0
             if world > 1:
                 t = torch.tensor([el], device=dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 el = float(t[0])
             nb = u0_host.numel() * u0_host.element_size()
+            nbo = out_host.numel() * out_host.element_size()
             res["e2e"] = {"value": updates / el / 1e9, "unit": UNIT, "h2d_bytes_per_step": nb / args.steps,
-                          "d2h_bytes_per_step": nb / args.steps}
+                          "d2h_bytes_per_step": nbo / args.steps}
         s.close()
         del u0_dev
         torch.cuda.empty_cache()
@@ -328,11 +342,13 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (dense uniform[-1,1] u0, u1 = 0, seed 0; delta-line h_eps, eps = 0.05)",
             "config": {"workload": wl, "nx": cfg.nx, "ny_global": cfg.ny, "rows_per_gpu": cfg.ny // world,
-                       "dx": cfg.dx, "dt": cfg.dt, "eps": cfg.eps[0], "energy_every": args.energy_every,
+                       "batch": cfg.batch, "dx": cfg.dx, "dt": cfg.dt,
+                       "eps": cfg.eps[0] if cfg.batch == 1 else [min(cfg.eps), max(cfg.eps)],
+                       "energy_every": args.energy_every,
                        "temporal_blocking": tblock,
                        "parallelism": f"row-slab x{world} (NCCL ghost rows)" if world > 1 else "single GPU",
                        "l2": "inputs exceed L2 (2 levels x %.2f GB per GPU), no flush" %
-                             ((cfg.nx * (cfg.ny // world) * esz) / 1e9)},
+                             ((cfg.nx * (cfg.ny // world) * esz * cfg.batch) / 1e9)},
             "hbm_gbs_effective": main_res["value"] * words * esz,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic,
