@@ -66,6 +66,9 @@ def _L():
             f.restype = d
             f.argtypes = [i32, i64, i64, vp, vp, vp, vp, d, d, d]
             getattr(lib, f"tswo_wave2_{s}").argtypes = [i32, i64, i64, vp, vp, d, d, d, vp, vp]
+            getattr(lib, f"tswo_implicit_solve_{s}").argtypes = [i32, i64, i64, vp, vp, vp, vp]
+            getattr(lib, f"tswo_implicit_steps_{s}").argtypes = [i32, i64, i64, vp, vp, vp, vp, i64]
+            getattr(lib, f"tswo_implicit_startup_{s}").argtypes = [i32, i64, i64, vp, vp, vp, vp, d, vp]
         _lib = lib
     return _lib
 
@@ -361,3 +364,31 @@ def moderateness_exponent(eps_list, norms) -> float:
     x = np.log(1.0 / np.asarray(eps_list, dtype=np.float64))
     y = np.log(np.asarray(norms, dtype=np.float64))
     return float(np.polyfit(x, y, 1)[0])
+
+
+# --- NEXT 3: the paper's implicit 2D method (R26/R27; §3.3, Table 1) ---
+
+def implicit_solve(dim: int, c1, c2, r: np.ndarray) -> np.ndarray:
+    """s = B⁻¹r, B = (I − ½L_x)(I − ½L_y), Thomas line solves (rows, then columns); ring → 0."""
+    dtype = r.dtype
+    r, c1 = _c(r, dtype), _c(c1, dtype)
+    c2 = None if dim == 1 else _c(c2, dtype)
+    nx, ny = _shape(dim, r)
+    out = np.empty_like(r)
+    getattr(_L(), f"tswo_implicit_solve_{_sfx(dtype)}")(dim, nx, ny, _p(c1), _p(c2), _p(r), _p(out))
+    return out
+
+
+def implicit_run(dim: int, c1, c2, u0: np.ndarray, u1: Optional[np.ndarray], dt: float, nsteps: int):
+    """R27 start u¹ = B⁻¹u⁰ + fl(dt·u₁), then u^{n+1} = B⁻¹(2u^n) − u^{n−1}: returns (u^N, u^{N−1})."""
+    dtype = u0.dtype
+    u0, c1 = _c(u0, dtype), _c(c1, dtype)
+    c2 = None if dim == 1 else _c(c2, dtype)
+    u1 = None if u1 is None else _c(u1, dtype)
+    nx, ny = _shape(dim, u0)
+    v = np.empty_like(u0)
+    L = _L()
+    getattr(L, f"tswo_implicit_startup_{_sfx(dtype)}")(dim, nx, ny, _p(c1), _p(c2), _p(u0), _p(u1), dt, _p(v))
+    un, unm1 = v.copy(), u0.copy()
+    getattr(L, f"tswo_implicit_steps_{_sfx(dtype)}")(dim, nx, ny, _p(c1), _p(c2), _p(un), _p(unm1), int(nsteps - 1))
+    return un, unm1

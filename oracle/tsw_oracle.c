@@ -360,3 +360,110 @@ void tswo_wave2_##SFX(int dim, int64_t nx, int64_t ny, const T* u, const T* ubg,
 
 ORACLE_DEFINE(double, f64)
 ORACLE_DEFINE(float, f32)
+
+/* ---------------------------------------------------------------------------
+ * the paper's 2D method as a second workload: "an implicit finite
+ * difference scheme [Sam] and the cyclic reduction method [Gode11]" (§3.3, P:1140;
+ * GPU timings Table 1).  Reading R26: the factorised three-level
+ * Crank–Nicolson scheme (u^{n+1} − 2u^n + u^{n−1})/τ² = A(u^{n+1} + u^{n−1})/2 with
+ * I − (τ²/2)A ≈ (I − ½L_x)(I − ½L_y), L = τ²A the prescaled operator of O5:
+ *     (I − ½L_x)(I − ½L_y)(u^{n+1} + u^{n−1}) = 2u^n        (1D: (I − ½L_x)(…) = 2u^n)
+ * and the implicit start (R27) u¹ = B⁻¹u⁰ + τ·u₁ (the same equation with u^{−1} = u¹ − 2τu₁).
+ * The oracle solves every line with the Thomas algorithm (no cyclic reduction: a plain,
+ * different solver), rows first, then columns; Dirichlet nodes stay 0.
+ * Line matrix (unknowns 1..n−2 of the line):  a_i = −½c_{i−1/2},  b_i = 1 + ½(c_{i−1/2} + c_{i+1/2}),
+ * c_i = −½c_{i+1/2}.
+ * ------------------------------------------------------------------------- */
+#define ORACLE_IMPLICIT(T, SFX)                                                                 \
+/* Dirichlet ring (R10) */                                                                     \
+static void zero_ring_##SFX(int dim, int64_t nx, int64_t ny, T* u) {                           \
+    if (dim == 1) { u[0] = (T)0; u[nx - 1] = (T)0; return; }                                   \
+    for (int64_t i = 0; i < nx; ++i) { u[i] = (T)0; u[(ny - 1) * nx + i] = (T)0; }             \
+    for (int64_t j = 0; j < ny; ++j) { u[j * nx] = (T)0; u[j * nx + nx - 1] = (T)0; }          \
+}                                                                                              \
+                                                                                               \
+/* Thomas algorithm on x[1..m] (x[0], x[m+1] are the Dirichlet zeros); face coefficient of    \
+ * face k+1/2 (between unknowns k and k+1) is cf[k * cstride].  x: rhs in, solution out. */    \
+static void thomas_line_##SFX(int64_t m, const T* cf, int64_t cstride, T* x, int64_t xstride,  \
+                              T* cp, T* dp) {                                                  \
+    const T half = (T)0.5;                                                                     \
+    for (int64_t i = 1; i <= m; ++i) {                                                         \
+        const T cl = cf[(i - 1) * cstride], cr = cf[i * cstride];                              \
+        const T a = -(half * cl), b = (T)1 + half * (cl + cr), c = -(half * cr);                \
+        const T d = x[i * xstride];                                                            \
+        if (i == 1) {                                                                          \
+            cp[i] = c / b;                                                                     \
+            dp[i] = d / b;                                                                     \
+        } else {                                                                               \
+            const T den = b - a * cp[i - 1];                                                   \
+            cp[i] = c / den;                                                                   \
+            dp[i] = (d - a * dp[i - 1]) / den;                                                 \
+        }                                                                                      \
+    }                                                                                          \
+    x[m * xstride] = dp[m];                                                                    \
+    for (int64_t i = m - 1; i >= 1; --i) x[i * xstride] = dp[i] - cp[i] * x[(i + 1) * xstride]; \
+}                                                                                              \
+                                                                                               \
+/* s = B⁻¹ r on the whole grid (r given on all nodes; ring ignored and s's ring set to 0). */  \
+void tswo_implicit_solve_##SFX(int dim, int64_t nx, int64_t ny, const T* c1, const T* c2,      \
+                               const T* r, T* s) {                                             \
+    if (dim == 1) ny = 1;                                                                      \
+    const int64_t N = nx > ny ? nx : ny;                                                       \
+    memcpy(s, r, sizeof(T) * (size_t)(nx * ny));                                               \
+    zero_ring_##SFX(dim, nx, ny, s);                                                           \
+    if (dim == 1) {                                                                            \
+        T* cp = (T*)malloc(sizeof(T) * (size_t)N);                                             \
+        T* dp = (T*)malloc(sizeof(T) * (size_t)N);                                             \
+        thomas_line_##SFX(nx - 2, c1, 1, s, 1, cp, dp);                                         \
+        free(cp); free(dp);                                                                    \
+        return;                                                                                \
+    }                                                                                          \
+    _Pragma("omp parallel")                                                                    \
+    {                                                                                          \
+        T* cp = (T*)malloc(sizeof(T) * (size_t)N);                                             \
+        T* dp = (T*)malloc(sizeof(T) * (size_t)N);                                             \
+        _Pragma("omp for schedule(static)")                                                   \
+        for (int64_t j = 1; j < ny - 1; ++j)   /* x lines: (I − ½L_x) z = r */                  \
+            thomas_line_##SFX(nx - 2, c1 + j * (nx - 1), 1, s + j * nx, 1, cp, dp);            \
+        _Pragma("omp for schedule(static)")                                                   \
+        for (int64_t i = 1; i < nx - 1; ++i)   /* y lines: (I − ½L_y) w = z */                  \
+            thomas_line_##SFX(ny - 2, c2 + i, nx, s + i, nx, cp, dp);                          \
+        free(cp); free(dp);                                                                    \
+    }                                                                                          \
+}                                                                                              \
+                                                                                               \
+/* k implicit levels from (u^n, u^{n−1}): u^{n+1} = B⁻¹(2u^n) − u^{n−1}. */                     \
+void tswo_implicit_steps_##SFX(int dim, int64_t nx, int64_t ny, const T* c1, const T* c2,      \
+                               T* un, T* unm1, int64_t k) {                                    \
+    if (dim == 1) ny = 1;                                                                      \
+    const size_t n = (size_t)(nx * ny);                                                        \
+    T* r = (T*)malloc(sizeof(T) * n);                                                          \
+    T* w = (T*)malloc(sizeof(T) * n);                                                          \
+    for (int64_t s = 0; s < k; ++s) {                                                          \
+        for (size_t q = 0; q < n; ++q) r[q] = (T)2 * un[q];                                    \
+        tswo_implicit_solve_##SFX(dim, nx, ny, c1, c2, r, w);                                  \
+        for (size_t q = 0; q < n; ++q) {                                                       \
+            const T next = w[q] - unm1[q];                                                     \
+            unm1[q] = un[q];                                                                   \
+            un[q] = next;                                                                      \
+        }                                                                                      \
+        /* Dirichlet ring stays exactly 0 (w's ring is 0; the ring of u^{n−1} is 0) */         \
+    }                                                                                          \
+    free(r); free(w);                                                                          \
+}                                                                                              \
+                                                                                               \
+/* R27: u¹ = B⁻¹u⁰ + fl(dt·u₁) */                                                                \
+void tswo_implicit_startup_##SFX(int dim, int64_t nx, int64_t ny, const T* c1, const T* c2,    \
+                                 const T* u0, const T* u1, double dt, T* out) {                \
+    if (dim == 1) ny = 1;                                                                      \
+    const size_t n = (size_t)(nx * ny);                                                        \
+    tswo_implicit_solve_##SFX(dim, nx, ny, c1, c2, u0, out);                                   \
+    if (u1) {                                                                                  \
+        const T dtT = (T)dt;                                                                   \
+        for (size_t q = 0; q < n; ++q) out[q] = out[q] + dtT * u1[q];                          \
+        zero_ring_##SFX(dim, nx, ny, out);                                                     \
+    }                                                                                          \
+}
+
+ORACLE_IMPLICIT(double, f64)
+ORACLE_IMPLICIT(float, f32)
