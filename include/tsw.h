@@ -217,6 +217,12 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                             (single-rank 2D, δ-line / constant / profile kinds; allocates two more
                             levels; results are bitwise those of K = 1).  Default 1. */
 #define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil, 3..16 (default 4) */
+#define TSW_OPT_SCHEME 8   /* 0 (default): explicit leapfrog (north_star).  1: the paper's implicit method
+                              (§3.3, reading R26): factorised three-level Crank–Nicolson
+                              (I − ½L_x)(I − ½L_y)(u^{n+1} + u^{n−1}) = 2u^n, start u¹ = B⁻¹u⁰ + dt·u₁ (R27),
+                              line solves by cyclic reduction in shared memory (2D) or Thomas (1D);
+                              unconditionally stable (no CFL check).  Single rank, δ-line / constant /
+                              profile kinds, ≤ 227 KB/(4·sizeof(T)) unknowns per line. */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
 
 /* Live per-kernel timing of the stencil (S2/S3) launches recorded since TSW_OPT_TIME_KERNELS was

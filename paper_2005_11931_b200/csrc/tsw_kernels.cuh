@@ -1512,6 +1512,184 @@ __global__ void k_coeff_norms(const CoeffNormArgs a, unsigned long long* __restr
 }
 
 // ------------------------------------------------------------------------------------------
+// NEXT 3: the paper's 2D method (§3.3 P:1140 "implicit finite difference scheme and the
+// cyclic reduction method"; Table 1) — reading R26: factorised three-level CN
+//   (I − ½L_x)(I − ½L_y)(u^{n+1} + u^{n−1}) = 2u^n,   start (R27) u¹ = B⁻¹u⁰ + dt·u₁.
+// Line solves by cyclic reduction (Hockney–Golub) with the whole line resident in shared memory:
+// one CTA per line, a/b/c/d arrays of N = 2^q − 1 ≥ m entries (identity padding).
+// ------------------------------------------------------------------------------------------
+struct CrArgs {
+    const void* src;   // right-hand side lines (rows of a [B][rows][pitch] array, view row 1 = first)
+    void* dst;         // solution lines (may alias src)
+    const void* cf;    // DIR 0: c1 [B][cpitch] x faces;  DIR 1: c2 [B][cpitch] one value per line
+    int64_t pitch, mstride, cpitch;
+    int64_t m;         // unknowns per line (line length − 2)
+    int32_t q;         // N = 2^q − 1 ≥ m
+    int32_t row0;      // first line (array row) to solve; lines row0 .. row0 + nlines − 1
+    int32_t nlines;
+    int32_t line_coef0;  // DIR 1: coefficient index of line row0 (the original column index)
+    double scale;      // rhs = scale · src
+};
+
+template <typename T, int DIR>
+__global__ void __launch_bounds__(512) k_cr_rows(const CrArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int N = (1 << a.q) - 1;
+    T* A = reinterpret_cast<T*>(smem_raw);
+    T* Bd = A + N;
+    T* C = Bd + N;
+    T* D = C + N;
+    const int line = blockIdx.x;
+    const int b = blockIdx.y;
+    const int64_t row = a.row0 + line;
+    const T* src = static_cast<const T*>(a.src) + b * a.mstride + row * a.pitch;
+    T* dst = static_cast<T*>(a.dst) + b * a.mstride + row * a.pitch;
+    const T* cf = static_cast<const T*>(a.cf) + b * a.cpitch;
+    const T half = (T)0.5, one = (T)1, sc = (T)a.scale;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        if (i < a.m) {
+            T cl, cr;
+            if (DIR == 0) {
+                cl = cf[i];       // face (i+1) − 1/2 of line position i+1
+                cr = cf[i + 1];   // face (i+1) + 1/2
+            } else {
+                cl = cr = cf[a.line_coef0 + line];
+            }
+            A[i] = (i == 0) ? (T)0 : -(half * cl);
+            C[i] = (i == a.m - 1) ? (T)0 : -(half * cr);
+            Bd[i] = one + half * (cl + cr);
+            D[i] = sc * src[i + 1];
+        } else {
+            A[i] = (T)0;
+            C[i] = (T)0;
+            Bd[i] = one;
+            D[i] = (T)0;
+        }
+    }
+    // forward reduction: level l updates i = k·2^l − 1 from i ± 2^{l−1}
+    for (int l = 1; l < a.q; ++l) {
+        __syncthreads();
+        const int h = 1 << (l - 1), s = 1 << l;
+        for (int k = 1 + threadIdx.x; k * s - 1 < N; k += blockDim.x) {
+            const int i = k * s - 1;
+            const T al = -A[i] / Bd[i - h];
+            const T ga = -C[i] / Bd[i + h];
+            const T na = al * A[i - h];
+            const T nc = ga * C[i + h];
+            const T nb = Bd[i] + al * C[i - h] + ga * A[i + h];
+            const T nd = D[i] + al * D[i - h] + ga * D[i + h];
+            A[i] = na;
+            C[i] = nc;
+            Bd[i] = nb;
+            D[i] = nd;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int r = (1 << (a.q - 1)) - 1;
+        D[r] = D[r] / Bd[r];
+    }
+    // back substitution: level l solves i = h − 1 + k·2^l (h = 2^{l−1}) from i ± h
+    for (int l = a.q - 1; l >= 1; --l) {
+        __syncthreads();
+        const int h = 1 << (l - 1), s = 1 << l;
+        for (int k = threadIdx.x; h - 1 + k * s < N; k += blockDim.x) {
+            const int i = h - 1 + k * s;
+            const T xl = (i - h >= 0) ? D[i - h] : (T)0;
+            const T xr = (i + h < N) ? D[i + h] : (T)0;
+            D[i] = (D[i] - A[i] * xl - C[i] * xr) / Bd[i];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.m; i += blockDim.x) dst[i + 1] = D[i];
+    if (threadIdx.x == 0) {
+        dst[0] = (T)0;
+        dst[a.m + 1] = (T)0;
+    }
+}
+
+// Tiled transpose of the storage rows 1..ny (global rows 0..ny−1) × columns 0..nx−1 of every
+// member: out[b][i][j] = in[b][1 + j][i] (out row i = original column i, pitch pt).
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ in, T* __restrict__ out, int64_t nx, int64_t ny, int64_t pitch,
+                            int64_t mstride, int64_t pt, int64_t tstride) {
+    __shared__ T tile[32][33];
+    const int b = blockIdx.z;
+    const int64_t i0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
+    const T* ib = in + b * mstride;
+    T* ob = out + b * tstride;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + r, i = i0 + threadIdx.x;
+        tile[r][threadIdx.x] = (j < ny && i < nx) ? ib[(1 + j) * pitch + i] : (T)0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, j = j0 + threadIdx.x;
+        if (i < nx && j < pt) ob[i * pt + j] = tile[threadIdx.x][r];
+    }
+}
+
+// Transpose back the y-solved w and finish the level on the interior nodes, in place in `prev`:
+//   MODE 0: u^{n+1} = w − u^{n−1}   (prev holds u^{n−1});   MODE 1: u¹ = w + dt·u₁ (prev holds u₁).
+template <typename T, int MODE>
+__global__ void k_transpose_finish(const T* __restrict__ wt, T* __restrict__ prev, int64_t nx, int64_t ny,
+                                   int64_t pitch, int64_t mstride, int64_t pt, int64_t tstride, T dtT) {
+    __shared__ T tile[32][33];
+    const int b = blockIdx.z;
+    const int64_t i0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
+    const T* wb = wt + b * tstride;
+    T* pb = prev + b * mstride;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, j = j0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < nx && j < ny) ? wb[i * pt + j] : (T)0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + r, i = i0 + threadIdx.x;
+        if (j >= 1 && j <= ny - 2 && i >= 1 && i <= nx - 2) {
+            T* p = pb + (1 + j) * pitch + i;
+            const T w = tile[threadIdx.x][r];
+            *p = (MODE == 0) ? r_sub(w, *p) : r_add(w, r_mul(dtT, *p));
+        }
+    }
+}
+
+// 1D implicit level: one thread per member runs the Thomas algorithm on its line (three-level CN
+// (I − ½L_x)(u^{n+1} + u^{n−1}) = 2u^n).  MODE 0: rhs 2u^n, result w − u^{n−1};  MODE 1: rhs u⁰,
+// result w + dt·u₁ (R27).  The result is written in place over `prev`.  cp/dp: [B][pitch] scratch.
+template <typename T, int MODE>
+__global__ void k_implicit_1d(const T* __restrict__ un, T* __restrict__ prev, const T* __restrict__ c1, int64_t nx,
+                              int64_t pitch, int64_t cpitch, T* __restrict__ cp, T* __restrict__ dp, int B, T dtT) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const T* u = un + b * pitch;
+    T* p = prev + b * pitch;
+    const T* c = c1 + b * cpitch;
+    T* cq = cp + b * pitch;
+    T* dq = dp + b * pitch;
+    const T half = (T)0.5;
+    const int64_t m = nx - 2;
+    for (int64_t i = 1; i <= m; ++i) {
+        const T cl = c[i - 1], cr = c[i];
+        const T a = -r_mul(half, cl), bb = r_add((T)1, r_mul(half, r_add(cl, cr))), cc = -r_mul(half, cr);
+        const T d = (MODE == 0) ? r_mul((T)2, u[i]) : u[i];
+        if (i == 1) {
+            cq[i] = cc / bb;
+            dq[i] = d / bb;
+        } else {
+            const T den = r_sub(bb, r_mul(a, cq[i - 1]));
+            cq[i] = cc / den;
+            dq[i] = r_sub(d, r_mul(a, dq[i - 1])) / den;
+        }
+    }
+    T x = dq[m];
+    for (int64_t i = m; i >= 1; --i) {
+        if (i < m) x = r_sub(dq[i], r_mul(cq[i], x));
+        p[i] = (MODE == 0) ? r_sub(x, p[i]) : r_add(x, r_mul(dtT, p[i]));
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // plumbing kernels
 // ------------------------------------------------------------------------------------------
 // Force the Dirichlet nodes of the slab (global rows 0 / ny−1, columns 0 / nx−1) and the padding

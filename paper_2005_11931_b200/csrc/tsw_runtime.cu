@@ -182,6 +182,10 @@ struct tsw_ctx {
     int kernel_opt = 0;   // 0: CTA-wide TMA bulk-copy pipeline (default), 1: register-prefetch kernel
     int depth_opt = 4;    // TMA ring stages per CTA (sweep: 4 best at 32768-wide rows)
     int tblock = 1;       // levels per HBM pass of the temporally blocked stencil (1 = off)
+    int scheme = 0;       // 0 explicit leapfrog (north_star); 1 implicit factorised CN (NEXT 3, R26)
+    void* imp_s1 = nullptr;   // implicit: x-solve output (field layout)
+    void* imp_t = nullptr;    // implicit: transposed field [B][nx][pt]
+    int64_t imp_pt = 0;       // its pitch (≥ ny, multiple of 32)
     int tb_depth = 4;     // its input ring stages
     int tb_occ[2][9] = {};  // [f64][K] resident CTAs per SM (cached)
     int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
@@ -261,6 +265,101 @@ int choose_rows_per_item(int64_t rows, int64_t strips, int64_t batch, int64_t G,
         }
     }
     return bestR;
+}
+
+
+// ---- NEXT 3: implicit factorised three-level CN (R26/R27) --------------------------------------
+int cr_levels(int64_t m) {
+    int q = 1;
+    while (((int64_t(1) << q) - 1) < m) ++q;
+    return q;
+}
+
+template <typename T>
+tsw_status implicit_level_t(tsw_ctx* c, bool start) {
+    const T dtT = (T)c->dt;
+    if (c->g.dim == 1) {
+        T* cp = static_cast<T*>(c->imp_s1);
+        T* dp = static_cast<T*>(c->imp_t);
+        const int threads = 32;
+        const unsigned blocks = unsigned((c->g.batch + threads - 1) / threads);
+        if (start)
+            k_implicit_1d<T, 1><<<blocks, threads, 0, c->stream>>>(static_cast<const T*>(c->buf[c->ic]), static_cast<T*>(c->buf[c->ip]),
+                                                                 static_cast<const T*>(c->c1), c->g.nx, c->pitch, c->cstride1, cp, dp,
+                                                                 c->g.batch, dtT);
+        else
+            k_implicit_1d<T, 0><<<blocks, threads, 0, c->stream>>>(static_cast<const T*>(c->buf[c->ic]), static_cast<T*>(c->buf[c->ip]),
+                                                                 static_cast<const T*>(c->c1), c->g.nx, c->pitch, c->cstride1, cp, dp,
+                                                                 c->g.batch, dtT);
+        CKL();
+        c->launches++;
+        std::swap(c->ic, c->ip);
+        c->n++;
+        return TSW_OK;
+    }
+    const int64_t nx = c->g.nx, ny = c->g.ny;
+    // (1) x lines: (I − ½L_x) z = scale·u  on the interior rows (view rows 2 .. ny−1)
+    CrArgs ax;
+    ax.src = c->buf[c->ic];
+    ax.dst = c->imp_s1;
+    ax.cf = c->c1;
+    ax.pitch = c->pitch;
+    ax.mstride = c->mstride;
+    ax.cpitch = c->cstride1;
+    ax.m = nx - 2;
+    ax.q = cr_levels(ax.m);
+    ax.row0 = 2;
+    ax.nlines = int32_t(ny - 2);
+    ax.line_coef0 = 0;
+    ax.scale = start ? 1.0 : 2.0;
+    const size_t smx = size_t(4) * ((size_t(1) << ax.q) - 1) * sizeof(T);
+    CK(cudaFuncSetAttribute(k_cr_rows<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smx)));
+    k_cr_rows<T, 0><<<dim3(unsigned(ax.nlines), unsigned(c->g.batch)), 512, smx, c->stream>>>(ax);
+    CKL();
+    // (2) transpose z
+    const dim3 tb(32, 8);
+    const dim3 tg(unsigned((nx + 31) / 32), unsigned((c->imp_pt + 31) / 32), unsigned(c->g.batch));
+    const int64_t tstride = nx * c->imp_pt;
+    k_transpose<T><<<tg, tb, 0, c->stream>>>(static_cast<const T*>(c->imp_s1), static_cast<T*>(c->imp_t), nx, ny,
+                                             c->pitch, c->mstride, c->imp_pt, tstride);
+    CKL();
+    // (3) y lines (rows of the transpose = interior columns 1..nx−2): (I − ½L_y) w = z, c2 per column
+    CrArgs ay;
+    ay.src = static_cast<const T*>(c->imp_t) - 0;
+    ay.dst = c->imp_t;
+    ay.cf = c->c2;
+    ay.pitch = c->imp_pt;
+    ay.mstride = tstride;
+    ay.cpitch = c->cstride2;
+    ay.m = ny - 2;
+    ay.q = cr_levels(ay.m);
+    ay.row0 = 1;
+    ay.nlines = int32_t(nx - 2);
+    ay.line_coef0 = 1;
+    ay.scale = 1.0;
+    const size_t smy = size_t(4) * ((size_t(1) << ay.q) - 1) * sizeof(T);
+    CK(cudaFuncSetAttribute(k_cr_rows<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smy)));
+    k_cr_rows<T, 1><<<dim3(unsigned(ay.nlines), unsigned(c->g.batch)), 512, smy, c->stream>>>(ay);
+    CKL();
+    // (4) transpose back and finish the level in place over u^{n−1} (or u₁ at the start)
+    const dim3 fg(unsigned((nx + 31) / 32), unsigned((ny + 31) / 32), unsigned(c->g.batch));
+    if (start)
+        k_transpose_finish<T, 1><<<fg, tb, 0, c->stream>>>(static_cast<const T*>(c->imp_t), static_cast<T*>(c->buf[c->ip]), nx, ny,
+                                                           c->pitch, c->mstride, c->imp_pt, tstride, dtT);
+    else
+        k_transpose_finish<T, 0><<<fg, tb, 0, c->stream>>>(static_cast<const T*>(c->imp_t), static_cast<T*>(c->buf[c->ip]), nx, ny,
+                                                           c->pitch, c->mstride, c->imp_pt, tstride, dtT);
+    CKL();
+    c->launches += 4;
+    std::swap(c->ic, c->ip);
+    c->n++;
+    return TSW_OK;
+}
+
+tsw_status implicit_level(tsw_ctx* c) {
+    if (c->mode != MODE_LINE)
+        return fail(TSW_ERR_ARG, "the implicit scheme needs x-only coefficients (δ-line, constant or profile kinds)");
+    return is_f64(c) ? implicit_level_t<double>(c, c->n == 0) : implicit_level_t<float>(c, c->n == 0);
 }
 
 // Resident CTAs per SM of the TMA stencil at the ctx's ring depth (cached; 0 on error).
@@ -744,7 +843,7 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     if (!c->have_coeff) return fail(TSW_ERR_STATE, "set coefficients (tsw_set_coeff / tsw_set_coeff_faces) first");
     if (!(dt > 0.0) || !std::isfinite(dt)) return fail(TSW_ERR_ARG, "dt must be finite and > 0 (got %g)", dt);
     if (!a) return fail(TSW_ERR_ARG, "u0 / un is NULL");
-    if (!(flags & TSW_ALLOW_UNSTABLE) && !(dt <= c->dt_max))
+    if (!(flags & TSW_ALLOW_UNSTABLE) && c->scheme == 0 && !(dt <= c->dt_max))
         return fail(TSW_ERR_CFL, "dt = %.17g exceeds the Gershgorin leapfrog bound 2/sqrt(rho_G) = %.17g (R16)", dt,
                     c->dt_max);
     const bool shared = (flags & TSW_INIT_SHARED) != 0;
@@ -886,6 +985,13 @@ tsw_status step_pair_graph(tsw_ctx* c) {
 
 tsw_status do_steps(tsw_ctx* c, int64_t k) {
     if (k <= 0) return TSW_OK;
+    if (c->scheme == 1) {
+        for (int64_t s = 0; s < k; ++s) {
+            tsw_status st = implicit_level(c);
+            if (st) return st;
+        }
+        return TSW_OK;
+    }
     if (c->g.dim == 1) return is_f64(c) ? step1d_t<double>(c, k) : step1d_t<float>(c, k);
     tsw_status st;
     if (c->g.nranks > 1) {
@@ -1033,6 +1139,8 @@ void tsw_destroy(tsw_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     for (int k = 0; k < 4; ++k) dfree_guarded(c->buf[k], c->fshift);
+    dfree_guarded(c->imp_s1, c->fshift);
+    if (c->imp_t) cudaFree(c->imp_t);
     dfree_guarded(c->h1, c->cshift_h);
     dfree_guarded(c->h2, c->cshift_h);
     dfree_guarded(c->c1, c->cshift);
@@ -1793,6 +1901,31 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
             }
         }
         c->tblock = int(value);
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_SCHEME) {
+        if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "scheme must be 0 (leapfrog) or 1 (implicit)");
+        if (value == 1) {
+            if (c->g.nranks != 1) return fail(TSW_ERR_ARG, "the implicit scheme is single-rank");
+            const int64_t lim = (227 * 1024) / (4 * int64_t(c->esz));
+            if (c->g.dim == 2 && (c->g.nx - 2 > lim || c->g.ny - 2 > lim))
+                return fail(TSW_ERR_ARG, "implicit line solves keep a line in shared memory: at most %lld unknowns per line",
+                            (long long)lim);
+            tsw_status st = set_dev(c);
+            if (st) return st;
+            const size_t fbytes = size_t(c->g.batch) * c->mstride * c->esz;
+            if (!c->imp_s1) {
+                cudaError_t e = dmalloc_guarded(&c->imp_s1, fbytes, c->fshift, c->stream);
+                if (e != cudaSuccess) return fail(TSW_ERR_OOM, "implicit scratch: %s", cudaGetErrorString(e));
+            }
+            if (!c->imp_t) {
+                c->imp_pt = round_up(c->g.dim == 2 ? c->g.ny : c->pitch, 32);
+                const size_t tbytes = size_t(c->g.batch) * size_t(c->g.dim == 2 ? c->g.nx : 1) * c->imp_pt * c->esz;
+                CK(cudaMalloc(&c->imp_t, tbytes));
+                CK(cudaMemsetAsync(c->imp_t, 0, tbytes, c->stream));
+            }
+        }
+        c->scheme = int(value);
         return TSW_OK;
     }
     if (key == TSW_OPT_TB_DEPTH) {

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-for w in config5 config3; do
-timeout 900 python bench.py --workload $w --no-cpu-baseline --steps 500 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; echo "$w exit=$?"; cat gpurun_out/bench_$w.json | python -c "import json,sys; d=json.load(sys.stdin); print(d['config']['workload'], d['value'], d['roofline']['frac'], d.get('also',{}).get('value'), d.get('per_step_kernel',{}).get('value'), d['e2e']['value'])"; tail -2 gpurun_out/bench_$w.err
-done
+timeout 1200 python -m pytest tests/test_implicit_gpu.py -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_imp.log 2>&1; echo pytest_exit=$?
+grep -E "passed|failed|^E  |FAILED" gpurun_out/pytest_imp.log | head -20
