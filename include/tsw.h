@@ -220,9 +220,16 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
 #define TSW_OPT_SCHEME 8   /* 0 (default): explicit leapfrog (north_star).  1: the paper's implicit method
                               (§3.3, reading R26): factorised three-level Crank–Nicolson
                               (I − ½L_x)(I − ½L_y)(u^{n+1} + u^{n−1}) = 2u^n, start u¹ = B⁻¹u⁰ + dt·u₁ (R27),
-                              line solves by cyclic reduction in shared memory (2D) or Thomas (1D);
-                              unconditionally stable (no CFL check).  Single rank, δ-line / constant /
-                              profile kinds, ≤ 227 KB/(4·sizeof(T)) unknowns per line. */
+                              line solves (2D) by the scan solvers of TSW_OPT_IMPLICIT_SOLVER, (1D)
+                              Thomas; unconditionally stable (no CFL check).  Single rank, δ-line /
+                              constant / profile kinds (x-only coefficients), ≤ 8192 unknowns per line. */
+#define TSW_OPT_IMPLICIT_SOLVER 9 /* 2D line solves of the implicit scheme.  0 (default): scans (reading
+                              R28) — x lines share one matrix, whose LU is applied as two affine scans
+                              per row; y lines are Toeplitz per column and solved by the closed form
+                              T⁻¹ = κ⁻¹[(I − ρS)(I − ρSᵀ) + ρ²e₁e₁ᵀ]⁻¹ (exponential scans + a rank-one
+                              correction), in place, 5 words of HBM traffic per node and level.
+                              1: cyclic reduction per line in shared memory with tiled transposes
+                              (the paper's solver), ≤ 227 KB/(4·sizeof(T)) unknowns per line. */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
 
 /* Live per-kernel timing of the stencil (S2/S3) launches recorded since TSW_OPT_TIME_KERNELS was

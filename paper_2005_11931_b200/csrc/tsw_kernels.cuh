@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <stdint.h>
 
 #include <type_traits>
@@ -1687,6 +1688,726 @@ __global__ void k_implicit_1d(const T* __restrict__ un, T* __restrict__ prev, co
         if (i < m) x = r_sub(dq[i], r_mul(cq[i], x));
         p[i] = (MODE == 0) ? r_sub(x, p[i]) : r_add(x, r_mul(dtT, p[i]));
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// Implicit scheme, scan solvers (NEXT 3, R28).  Both factors of B = (I − ½L_x)(I − ½L_y) have
+// coefficients that depend on x only (δ-line / profile kinds), which the line solvers exploit:
+//  * x lines: one tridiagonal matrix shared by every row.  Its LU (l_p, 1/u_p, e_p = c_p/u_p) is
+//    computed once (k_imp_xfactor); each row then needs the two first-order recurrences
+//    y_p = d_p − l_p y_{p−1} and x_p = y_p/u_p − e_p x_{p+1}, run as affine scans across a CTA
+//    (warp shuffles inside a 32-position sub-block, sub-blocks in sequence per warp, warp totals
+//    through shared memory) — coalesced, in place along the row, no transposes (k_imp_x).
+//  * y lines: column i is Toeplitz, T = tridiag(−γ/2, 1 + γ, −γ/2) with γ = c2(i), and
+//    T = κ[(I − ρS)(I − ρSᵀ) + ρ² e₁e₁ᵀ] (κρ = γ/2, κ(1 + ρ²) = 1 + γ, 0 ≤ ρ < 1), so
+//    T⁻¹r = (1/κ)[z − β z₁ P⁻¹e₁] with z = P⁻¹r = (L_j + R_j − ρ^{m+1−j}A₂)/(1 − ρ²),
+//    L_j = Σ_{i≤j} ρ^{j−i} r_i, R_j = Σ_{i>j} ρ^{i−j} r_i, A₂ = Σ ρ^{m+1−i} r_i,
+//    z₁ = (A₁ − ρ^m A₂)/(1 − ρ²), A₁ = Σ ρ^{i−1} r_i, β = ρ²/(1 + ρ²(1 − ρ^{2m})/(1 − ρ²)),
+//    P⁻¹e₁ = (ρ^{j−1} − ρ^{2m+1−j})/(1 − ρ²): exponential scans with a constant factor per column,
+//    done column-parallel in place (k_imp_y), fused with the three-level update.
+// All recurrences have |factor| < 1 (diagonal dominance), so the scans are stable.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+template <typename T>
+__device__ __forceinline__ T powi_T(T x, int n) {  // x^n, n ≥ 0, by squaring (0^0 = 1)
+    T r = (T)1;
+    while (n > 0) {
+        if (n & 1) r = r * x;
+        x = x * x;
+        n >>= 1;
+    }
+    return r;
+}
+
+// LU of the x-line matrix of member b (one thread per member): unknown p ↔ column p + 1,
+// a_p = −½c1[p], b_p = 1 + ½(c1[p] + c1[p+1]), c_p = −½c1[p+1]; in fp64, stored as T.  The pivots
+// u_p = θ_p/θ_{p−1} come from the continuants θ_p = b_p θ_{p−1} − a_p c_{p−1} θ_{p−2} (the leading
+// principal minors; growing solution of a three-term recurrence, hence stable), rescaled by exact
+// powers of two — one dependent FMA per step instead of a dependent division.
+template <typename T>
+__global__ void k_imp_xfactor(const T* __restrict__ c1, int64_t cpitch, T* __restrict__ tab, int64_t tpitch, int m,
+                              int B) {
+    // One CTA per member.  Thread 0 runs the serial continuant recurrence (one FMA per step) and
+    // records each pivot as a (numerator, denominator) pair at a common scale; all threads then
+    // form l_p, 1/u_p, e_p in parallel.  Shared memory: c (m + 1), num (m), den (m), fp64.
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* c = reinterpret_cast<double*>(smem_raw);
+    double* num = c + (m + 1);
+    double* den = num + m;
+    const int b = blockIdx.x;
+    for (int i = threadIdx.x; i <= m; i += blockDim.x) c[i] = (double)c1[b * cpitch + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double th2 = 1.0, th1 = 1.0;   // θ_{p−2}, θ_{p−1} (θ_{−1} = 1)
+        for (int p = 0; p < m; ++p) {
+            const double cl = c[p], cr = c[p + 1];
+            const double bb = 1.0 + 0.5 * (cl + cr);
+            // a_p c_{p−1} = (−½c[p])(−½c[p]) = ¼c[p]²
+            const double th = (p == 0) ? bb : fma(bb, th1, -(0.25 * cl * cl) * th2);
+            num[p] = th;
+            den[p] = th1;
+            th2 = th1;
+            th1 = th;
+            if ((p & 15) == 15) {  // exact rescale
+                const int e = ilogb(th1);
+                th1 = scalbn(th1, -e);
+                th2 = scalbn(th2, -e);
+            }
+        }
+    }
+    __syncthreads();
+    T* t = tab + b * 3 * tpitch;
+    for (int p = threadIdx.x; p < m; p += blockDim.x) {
+        const double u = num[p] / den[p];
+        const double cl = c[p], cr = c[p + 1];
+        const double l = (p > 0) ? (-0.5 * cl) * (den[p - 1] / num[p - 1]) : 0.0;
+        const double cc = (p < m - 1) ? -0.5 * cr : 0.0;
+        t[p] = (T)l;
+        t[tpitch + p] = (T)(1.0 / u);
+        t[2 * tpitch + p] = (T)(cc / u);
+    }
+}
+
+struct ImpXArgs {
+    const void* src;   // right-hand side field (view rows), scaled by `scale`
+    void* dst;         // x-solve output z (same layout)
+    const void* tab;   // [B][3][tpitch]: l, 1/u, e of unknown p (column p + 1)
+    int64_t pitch, mstride, tpitch;
+    int32_t nx;
+    int32_t row0;      // view row of the first line; lines row0 .. row0 + nrows − 1
+    int32_t nrows;
+    double scale;
+};
+
+constexpr int IMPX_THREADS = 512;
+constexpr int IMPX_WARPS = IMPX_THREADS / 32;
+
+// Affine inclusive scan inside a warp, forward (lane 0 → 31): (A, V) ← (A·A_up, V + A·V_up).
+template <typename T>
+__device__ __forceinline__ void warp_affine_fwd(T& A, T& V, int lane, int from = 1) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        if (off < from) continue;
+        const T Vu = __shfl_up_sync(0xffffffffu, V, off);
+        const T Au = __shfl_up_sync(0xffffffffu, A, off);
+        if (lane >= off) {
+            V = fmaT(A, Vu, V);
+            A = A * Au;
+        }
+    }
+}
+template <typename T>
+__device__ __forceinline__ void warp_affine_bwd(T& A, T& V, int lane, int from = 1) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        if (off < from) continue;
+        const T Vd = __shfl_down_sync(0xffffffffu, V, off);
+        const T Ad = __shfl_down_sync(0xffffffffu, A, off);
+        if (lane + off < 32) {
+            V = fmaT(A, Vd, V);
+            A = A * Ad;
+        }
+    }
+}
+
+// 32-byte vector accesses (sm_100: LDG/STG .256) for a thread's span of R consecutive columns.
+template <typename T>
+__device__ __forceinline__ void ld32(const T* p, T* v) {
+    if constexpr (sizeof(T) == 8)
+        asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+    else
+        asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                     : "l"(p));
+}
+template <typename T>
+__device__ __forceinline__ void st32(T* p, const T* v) {
+    if constexpr (sizeof(T) == 8)
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]) : "memory");
+    else
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                     "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                     : "memory");
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void load_span(const T* __restrict__ row, int c0, int nx, T (&v)[R]) {
+    constexpr int W = 32 / int(sizeof(T));  // elements per 32-byte access
+    if (c0 + R <= nx && R % W == 0) {
+#pragma unroll
+        for (int k = 0; k < R; k += W) ld32<T>(row + c0 + k, v + k);
+    } else {
+#pragma unroll
+        for (int k = 0; k < R; ++k) v[k] = (c0 + k < nx) ? row[c0 + k] : (T)0;
+    }
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void store_span(T* __restrict__ row, int c0, int lo, int hi, const T (&v)[R]) {
+    // columns [lo, hi) only
+    constexpr int W = 32 / int(sizeof(T));
+    if (c0 >= lo && c0 + R <= hi && R % W == 0) {
+#pragma unroll
+        for (int k = 0; k < R; k += W) st32<T>(row + c0 + k, v + k);
+    } else {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+            if (c0 + k >= lo && c0 + k < hi) row[c0 + k] = v[k];
+    }
+}
+
+// One CTA (blockDim.x = nthreads ≤ 1024, a multiple of 32) solves rows row0 + blockIdx.x +
+// k·gridDim.x of member blockIdx.y.  Thread t owns the R consecutive columns [tR, tR + R) — one
+// 32-byte access when R·sizeof(T) = 32 (column 0 and columns ≥ nx − 1 carry zero table entries,
+// so they stay out of the system) — and keeps their LU table entries in registers.  Per row and
+// direction: a sequential local recurrence over the span; a warp-level scan of the span totals in
+// which only the values move (the factors are products of LU entries — data-independent — so the
+// per-level factors are computed once per CTA and kept in shared memory); the warp totals are
+// scanned by one warp; then the fix-up.  Two barriers per row.
+constexpr int IMPX_MAXW = 32;
+
+template <typename T, int R>
+__global__ void __launch_bounds__(1024, 1) k_imp_x(const ImpXArgs a) {
+    __shared__ T fwv[IMPX_MAXW], bwv[IMPX_MAXW];          // warp totals (values) per row
+    __shared__ T fwc[IMPX_MAXW], bwc[IMPX_MAXW];          // per-warp carry-in (values) per row
+    __shared__ T fwa[IMPX_MAXW], bwa[IMPX_MAXW];          // warp-total factors (constant)
+    __shared__ T fxa[5][IMPX_MAXW], bxa[5][IMPX_MAXW];    // cross-warp scan level factors (constant)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* lvf = reinterpret_cast<T*>(smem_raw);               // [5][nthreads] intra-warp level factors, forward
+    T* lvb = lvf + 5 * blockDim.x;                          // backward
+    const int b = blockIdx.y;
+    const int nx = a.nx, m = nx - 2;
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int nwarps = nt >> 5;
+    const int c0 = t * R;
+    const int lane = t & 31, warp = t >> 5;
+    T tl[R], tiu[R], te[R];
+    T aexf, aexb;   // product of the span factors of the earlier (later) lanes in the warp
+    {
+        const T* tab = static_cast<const T*>(a.tab) + b * 3 * a.tpitch;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int c = c0 + k;
+            const bool ok = c >= 1 && c <= m;
+            tl[k] = ok ? -tab[c - 1] : (T)0;                 // stored negated: the recurrence factor
+            tiu[k] = ok ? tab[a.tpitch + c - 1] : (T)0;
+            te[k] = ok ? -tab[2 * a.tpitch + c - 1] : (T)0;  // negated
+        }
+        // constant factors of the scans
+        T Af = (T)1, Ab = (T)1;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            Af = Af * tl[k];
+            Ab = Ab * te[k];
+        }
+        int lv = 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1, ++lv) {
+            const T Au = __shfl_up_sync(0xffffffffu, Af, off);
+            const T Ad = __shfl_down_sync(0xffffffffu, Ab, off);
+            lvf[lv * nt + t] = (lane >= off) ? Af : (T)0;
+            lvb[lv * nt + t] = (lane + off < 32) ? Ab : (T)0;
+            if (lane >= off) Af = Af * Au;
+            if (lane + off < 32) Ab = Ab * Ad;
+        }
+        aexf = __shfl_up_sync(0xffffffffu, Af, 1);
+        aexb = __shfl_down_sync(0xffffffffu, Ab, 1);
+        if (lane == 0) aexf = (T)1;
+        if (lane == 31) aexb = (T)1;
+        if (lane == 31) fwa[warp] = Af;   // product over the warp's spans
+        if (lane == 0) bwa[warp] = Ab;
+        __syncthreads();
+        if (warp == 0) {   // level factors of the cross-warp scans (lane = warp index)
+            T A = (lane < nwarps) ? fwa[lane] : (T)1;
+            T B = (lane < nwarps) ? bwa[lane] : (T)1;
+            int l2 = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++l2) {
+                const T Au = __shfl_up_sync(0xffffffffu, A, off);
+                const T Bd = __shfl_down_sync(0xffffffffu, B, off);
+                fxa[l2][lane] = (lane >= off) ? A : (T)0;
+                bxa[l2][lane] = (lane + off < 32) ? B : (T)0;
+                if (lane >= off) A = A * Au;
+                if (lane + off < 32) B = B * Bd;
+            }
+        }
+        __syncthreads();
+    }
+    const T sc = (T)a.scale;
+    const T* srcb = static_cast<const T*>(a.src) + b * a.mstride;
+    T* dstb = static_cast<T*>(a.dst) + b * a.mstride;
+    int line = blockIdx.x;
+    T nxt[R];
+    if (line < a.nrows) load_span<T, R>(srcb + int64_t(a.row0 + line) * a.pitch, c0, nx, nxt);
+    for (; line < a.nrows; line += gridDim.x) {
+        T d[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) d[k] = sc * nxt[k];
+        const int nline = line + gridDim.x;
+        if (nline < a.nrows) load_span<T, R>(srcb + int64_t(a.row0 + nline) * a.pitch, c0, nx, nxt);
+        // forward y_c = d_c − l_c y_{c−1}: local (zero carry-in)
+        T v = (T)0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            v = fmaT(tl[k], v, d[k]);
+            d[k] = v;
+        }
+        {
+            int lv = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++lv) v = fmaT(lvf[lv * nt + t], __shfl_up_sync(0xffffffffu, v, off), v);
+        }
+        T vex = __shfl_up_sync(0xffffffffu, v, 1);
+        if (lane == 0) vex = (T)0;
+        if (lane == 31) fwv[warp] = v;
+        __syncthreads();
+        if (warp == 0) {   // exclusive scan of the warp totals
+            T V = (lane < nwarps) ? fwv[lane] : (T)0;
+            int l2 = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++l2) V = fmaT(fxa[l2][lane], __shfl_up_sync(0xffffffffu, V, off), V);
+            const T Vx = __shfl_up_sync(0xffffffffu, V, 1);
+            if (lane < nwarps) fwc[lane] = (lane == 0) ? (T)0 : Vx;
+        } else if (warp == 1 || nwarps == 1) {
+            // (backward carries are computed after the fix-up)
+        }
+        __syncthreads();
+        T cin = fmaT(aexf, fwc[warp], vex);
+        {
+            T pi = (T)1;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                pi = pi * tl[k];
+                d[k] = fmaT(pi, cin, d[k]);
+            }
+        }
+        // backward x_c = y_c/u_c − e_c x_{c+1}
+        v = (T)0;
+#pragma unroll
+        for (int k = R - 1; k >= 0; --k) {
+            v = fmaT(te[k], v, d[k] * tiu[k]);
+            d[k] = v;
+        }
+        {
+            int lv = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++lv) v = fmaT(lvb[lv * nt + t], __shfl_down_sync(0xffffffffu, v, off), v);
+        }
+        vex = __shfl_down_sync(0xffffffffu, v, 1);
+        if (lane == 31) vex = (T)0;
+        if (lane == 0) bwv[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            T V = (lane < nwarps) ? bwv[lane] : (T)0;
+            int l2 = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++l2) V = fmaT(bxa[l2][lane], __shfl_down_sync(0xffffffffu, V, off), V);
+            const T Vx = __shfl_down_sync(0xffffffffu, V, 1);
+            if (lane < nwarps) bwc[lane] = (lane == nwarps - 1) ? (T)0 : Vx;
+        }
+        __syncthreads();
+        cin = fmaT(aexb, bwc[warp], vex);
+        {
+            T pi = (T)1;
+#pragma unroll
+            for (int k = R - 1; k >= 0; --k) {
+                pi = pi * te[k];
+                d[k] = fmaT(pi, cin, d[k]);
+            }
+        }
+        store_span<T, R>(dstb + int64_t(a.row0 + line) * a.pitch, c0, 1, nx - 1, d);
+    }
+}
+
+struct ImpYArgs {
+    const void* z;     // x-solve output (field layout, view rows)
+    void* prev;        // u^{n−1} (MODE 0) or u₁ (MODE 1); overwritten by u^{n+1}
+    const void* cf;    // c2 [B][cpitch], one value per column
+    int64_t pitch, mstride, cpitch;
+    int32_t nx;
+    int32_t m;         // unknowns per column (ny − 2): global rows 1..m
+    int32_t seg;       // rows per segment (multiple of 8); 32 segments cover 1..m
+    double dt;
+};
+
+constexpr int IMPY_COLS = 16;
+constexpr int IMPY_SEGS = 32;
+constexpr int IMPY_THREADS = IMPY_COLS * IMPY_SEGS;
+
+// One CTA owns 16 interior columns × the full height, as 32 segments of `seg` rows (lanes 0–15 /
+// 16–31 of warp w: segments 2w / 2w+1).  Pass 1 reads z and forms per-segment and per-8-row
+// decayed sums; the cross-segment carries go through shared memory; pass 2 re-reads z (L2),
+// forms L_j, R_j and the boundary corrections and writes u^{n+1} over `prev`.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(IMPY_THREADS, 2) k_imp_y(const ImpYArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Fs = reinterpret_cast<T*>(smem_raw);      // [32][16] forward sums (decayed to last valid row)
+    T* Bs = Fs + IMPY_SEGS * IMPY_COLS;          // [32][16] backward sums (decayed to segment start)
+    T* subS = Bs + IMPY_SEGS * IMPY_COLS;        // [NS][512] per-8-row backward sums → suffix carries
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cl = lane & 15, sg = 2 * warp + (lane >> 4);
+    const int b = blockIdx.y;
+    const int64_t col = 1 + int64_t(blockIdx.x) * IMPY_COLS + cl;
+    const bool colok = col <= a.nx - 2;
+    const int m = a.m, seg = a.seg, NS = seg >> 3;
+    const int j0 = 1 + sg * seg;
+    // column constants (fp64, rounded once to T)
+    const double g = colok ? (double)static_cast<const T*>(a.cf)[b * a.cpitch + col] : 0.0;
+    const double sq = sqrt(1.0 + 2.0 * g);
+    const double rho_d = g / ((1.0 + g) + sq);
+    const double kap_d = 0.5 * ((1.0 + g) + sq);
+    const double omr = (1.0 + sq) / ((1.0 + g) + sq);  // 1 − ρ, without cancellation
+    const double i1_d = 1.0 / (omr * (1.0 + rho_d));    // 1/(1 − ρ²)
+    const T rho = (T)rho_d;
+    const T* zb = static_cast<const T*>(a.z) + b * a.mstride + col;
+    T* pb = static_cast<T*>(a.prev) + b * a.mstride + col;
+    // ---- pass 1 ----
+    T F = (T)0;
+    for (int t = 0; t < NS; ++t) {
+        T Bt = (T)0, pw = (T)1;
+        const int jt = j0 + 8 * t;
+        T zz[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zz[k] = (colok && jt + k <= m) ? zb[int64_t(1 + jt + k) * a.pitch] : (T)0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (jt + k <= m) F = fmaT(rho, F, zz[k]);
+            Bt = fmaT(pw, zz[k], Bt);
+            pw = pw * rho;
+        }
+        subS[t * IMPY_THREADS + threadIdx.x] = Bt;
+    }
+    const T rho8 = powi_T(rho, 8);
+    {
+        T Bsum = (T)0;
+        for (int t = NS - 1; t >= 0; --t) Bsum = fmaT(rho8, Bsum, subS[t * IMPY_THREADS + threadIdx.x]);
+        Fs[sg * IMPY_COLS + cl] = F;
+        Bs[sg * IMPY_COLS + cl] = Bsum;
+    }
+    __syncthreads();
+    const T rhoS = powi_T(rho, seg);
+    T Lin = (T)0;
+    for (int k = 0; k < sg; ++k) Lin = fmaT(rhoS, Lin, Fs[k * IMPY_COLS + cl]);
+    T Sbelow = (T)0;
+    for (int k = IMPY_SEGS - 1; k > sg; --k) Sbelow = fmaT(rhoS, Sbelow, Bs[k * IMPY_COLS + cl]);
+    T A1 = Sbelow;
+    for (int k = sg; k >= 0; --k) A1 = fmaT(rhoS, A1, Bs[k * IMPY_COLS + cl]);
+    // L_m: segments before the last non-empty one are full
+    const int klast = (m - 1) / seg;
+    T Lm = (T)0;
+    for (int k = 0; k < klast; ++k) Lm = fmaT(rhoS, Lm, Fs[k * IMPY_COLS + cl]);
+    Lm = fmaT(powi_T(rho, m - klast * seg), Lm, Fs[klast * IMPY_COLS + cl]);
+    const T A2 = rho * Lm;
+    const T rhom = powi_T(rho, m);
+    const T i1 = (T)i1_d;
+    const T z1 = (A1 - rhom * A2) * i1;
+    const T rr = rho * rho;
+    const T beta = rr / ((T)1 + rr * (((T)1 - rhom * rhom) * i1));
+    const T bz1 = beta * z1;
+    const T A2p = A2 - bz1 * rhom;
+    const T K = (T)(i1_d / kap_d);
+    // suffix carries per 8-row block: subS[t] ← Σ_{i > end of block t} ρ^{i − end − 1} z_i
+    {
+        T Sa = Sbelow;
+        for (int t = NS - 1; t >= 0; --t) {
+            const T tmp = subS[t * IMPY_THREADS + threadIdx.x];
+            subS[t * IMPY_THREADS + threadIdx.x] = Sa;
+            Sa = fmaT(rho8, Sa, tmp);
+        }
+    }
+    if (!colok || j0 > m) return;
+    // ---- pass 2 ----
+    const T dtT = (T)a.dt;
+    T L = Lin;
+    T pu = powi_T(rho, j0 - 1);
+    for (int t = 0; t < NS; ++t) {
+        const int jt = j0 + 8 * t;
+        if (jt > m) break;
+        T zz[8], Lc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zz[k] = (jt + k <= m) ? zb[int64_t(1 + jt + k) * a.pitch] : (T)0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            L = fmaT(rho, L, zz[k]);
+            Lc[k] = L - bz1 * pu;
+            pu = pu * rho;
+        }
+        T R = rho * subS[t * IMPY_THREADS + threadIdx.x];
+        const int e = jt + 7;
+        T pd = powi_T(rho, (m + 1 - e) > 1 ? (m + 1 - e) : 1);
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+            const int j = jt + k;
+            if (j <= m) {
+                const T x = K * ((Lc[k] + R) - pd * A2p);
+                T* q = pb + int64_t(1 + j) * a.pitch;
+                const T pv = *q;
+                *q = (MODE == 0) ? (x - pv) : fmaT(dtT, pv, x);
+                pd = pd * rho;
+            }
+            R = rho * (zz[k] + R);
+        }
+    }
+}
+
+// Resident variant of the y solve (thread-block cluster).  A cluster of CL ≤ 8 CTAs owns COLS =
+// 128 B / sizeof(T) interior columns (one 128-byte line per row) × the full height; CTA r of the
+// cluster owns rows [1 + r·SEGS·seg, 1 + (r+1)·SEGS·seg) as SEGS = 512 / COLS segments of ≤ SR
+// rows (lane = column + COLS × local segment).  Each thread stages its segment of z in shared
+// memory with cp.async and holds its rows of u^{n−1} in registers, so everything it reads from HBM
+// is in flight at once.  Segment sums → carries: warp shuffles across segments, warp totals
+// through shared memory, CTA totals across the cluster through distributed shared memory →
+// a forward walk (L_j, folded into the registers) and a backward walk (R_j) over the staged
+// segment → u^{n+1} over `prev`.  Forward factors are ρ^{valid rows} (empty / partial segments
+// compose exactly); backward factors ρ^{slots}.  HBM traffic: z, u^{n−1} once each, u^{n+1} once.
+constexpr int IMPYC_THREADS = 512;
+
+template <typename T>
+struct ImpYc {
+    static constexpr int COLS = 128 / int(sizeof(T));
+    static constexpr int SEGS = IMPYC_THREADS / COLS;  // segments per CTA
+    static constexpr int WARPS = IMPYC_THREADS / 32;
+    static constexpr int SPW = 32 / COLS;              // segments per warp
+    static constexpr int SR = 128 / int(sizeof(T));    // max rows per segment (registers)
+    static __host__ __device__ size_t smem_bytes(int seg) {
+        return (size_t(SEGS) * seg * COLS + 6 * size_t(WARPS) * COLS + 12 * COLS) * sizeof(T);
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* sdst, const T* gsrc, bool valid) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+    const int n = valid ? int(sizeof(T)) : 0;   // src-size 0 ⇒ zero fill
+    if constexpr (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc), "r"(n) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gsrc), "r"(n) : "memory");
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
+    using G = ImpYc<T>;
+    constexpr int COLS = G::COLS, SR = G::SR, SEGS = G::SEGS, WARPS = G::WARPS;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = int(cluster.num_blocks());
+    const int rk = int(cluster.block_rank());
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int seg = a.seg;
+    T* zs = reinterpret_cast<T*>(smem_raw);                 // [SEGS][seg][COLS]
+    T* wF = zs + size_t(SEGS) * seg * COLS;                 // [WARPS][COLS] warp totals: forward value
+    T* wFA = wF + WARPS * COLS;                             //   forward factor
+    T* wB = wFA + WARPS * COLS;                             //   backward value
+    T* wBA = wB + WARPS * COLS;                             //   backward factor
+    T* wY = wBA + WARPS * COLS;                             // [WARPS][COLS] carry into each warp (forward)
+    T* wX = wY + WARPS * COLS;                              //   (backward)
+    T* ctot = wX + WARPS * COLS;                            // [4][COLS] this CTA's totals (read by the cluster)
+    T* ccon = ctot + 4 * COLS;                              // [8][COLS] column constants
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int cl = lane % COLS, sl = lane / COLS;
+    const int sg = warp * G::SPW + sl;
+    const int b = blockIdx.z;
+    const int64_t colbase = 1 + int64_t(blockIdx.x) * COLS;
+    const int64_t col = colbase + cl;
+    const bool colok = col <= a.nx - 2;
+    const int m = a.m;
+    const int cta0 = 1 + rk * SEGS * seg;
+    const int j0 = cta0 + sg * seg;
+    int nvalid = m - j0 + 1;
+    nvalid = nvalid < 0 ? 0 : (nvalid > seg ? seg : nvalid);
+    const int nv_ld = colok ? nvalid : 0;
+    T* zrow = zs + size_t(sg) * seg * COLS + cl;
+    // designated lanes: forward (column lane) and backward scans over warps / cluster ranks
+    const bool isF = (warp == 0 && lane < COLS);
+    const bool isB = (COLS == 32) ? (warp == 1) : (warp == 0 && lane >= COLS);
+    const int cc = (COLS == 32) ? lane : (lane % COLS);
+    // ---- issue every HBM read of this thread ----
+    T pv[SR];
+    {
+        const T* zq = static_cast<const T*>(a.z) + b * a.mstride + col + int64_t(1 + j0) * a.pitch;
+        const T* pq = static_cast<const T*>(a.prev) + b * a.mstride + col + int64_t(1 + j0) * a.pitch;
+#pragma unroll
+        for (int k = 0; k < SR; ++k) {
+            if (k < seg) cp_async_elem(zrow + k * COLS, zq, k < nv_ld);
+            pv[k] = (k < nv_ld) ? *pq : (T)0;
+            zq += a.pitch;
+            pq += a.pitch;
+        }
+    }
+    // ---- column constants (once per column) ----
+    if (isF) {
+        const int64_t cf = colbase + cc;
+        const double g = (cf <= a.nx - 2) ? (double)static_cast<const T*>(a.cf)[b * a.cpitch + cf] : 0.0;
+        const double sq = sqrt(1.0 + 2.0 * g);
+        const double rho_d = g / ((1.0 + g) + sq);
+        const double kap_d = 0.5 * ((1.0 + g) + sq);
+        const double omr = (1.0 + sq) / ((1.0 + g) + sq);  // 1 − ρ without cancellation
+        const double i1_d = 1.0 / (omr * (1.0 + rho_d));    // 1/(1 − ρ²)
+        const T rho = (T)rho_d;
+        ccon[0 * COLS + cc] = rho;
+        ccon[1 * COLS + cc] = powi_T(rho, seg);
+        ccon[2 * COLS + cc] = (T)(i1_d / kap_d);   // K
+        ccon[3 * COLS + cc] = (T)i1_d;
+    }
+    __syncthreads();
+    const T rho = ccon[cl], rhoS = ccon[COLS + cl];
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    // ---- segment sums: F (forward, to the last valid row), B (backward, from the segment start) ----
+    T F = (T)0, Bsum = (T)0, pw = (T)1;
+    if (nvalid == SR) {
+#pragma unroll
+        for (int k = 0; k < SR; ++k) {
+            const T z = zrow[k * COLS];
+            F = fmaT(rho, F, z);
+            Bsum = fmaT(pw, z, Bsum);
+            pw = pw * rho;
+        }
+    } else {
+        for (int k = 0; k < nvalid; ++k) {
+            const T z = zrow[k * COLS];
+            F = fmaT(rho, F, z);
+            Bsum = fmaT(pw, z, Bsum);
+            pw = pw * rho;
+        }
+    }
+    T Af = pw, Vf = F;        // forward factor ρ^{nvalid}
+    T Ab = rhoS, Vb = Bsum;   // backward factor ρ^{seg}
+    T vfx = (T)0, afx = (T)1, vbx = (T)0, abx = (T)1;
+    if constexpr (G::SPW > 1) {
+        warp_affine_fwd(Af, Vf, lane, COLS);
+        warp_affine_bwd(Ab, Vb, lane, COLS);
+        vfx = __shfl_up_sync(0xffffffffu, Vf, COLS);
+        afx = __shfl_up_sync(0xffffffffu, Af, COLS);
+        vbx = __shfl_down_sync(0xffffffffu, Vb, COLS);
+        abx = __shfl_down_sync(0xffffffffu, Ab, COLS);
+        if (sl == 0) {
+            vfx = (T)0;
+            afx = (T)1;
+        }
+        if (sl == G::SPW - 1) {
+            vbx = (T)0;
+            abx = (T)1;
+        }
+    }
+    if (sl == G::SPW - 1) {
+        wF[warp * COLS + cl] = Vf;
+        wFA[warp * COLS + cl] = Af;
+    }
+    if (sl == 0) {
+        wB[warp * COLS + cl] = Vb;
+        wBA[warp * COLS + cl] = Ab;
+    }
+    __syncthreads();
+    // ---- CTA totals ----
+    if (isF) {
+        T Ft = (T)0, AFt = (T)1;
+        for (int k = 0; k < WARPS; ++k) {
+            Ft = fmaT(wFA[k * COLS + cc], Ft, wF[k * COLS + cc]);
+            AFt = AFt * wFA[k * COLS + cc];
+        }
+        ctot[cc] = Ft;
+        ctot[COLS + cc] = AFt;
+    }
+    if (isB) {
+        T Bt = (T)0, ABt = (T)1;
+        for (int k = WARPS - 1; k >= 0; --k) {
+            Bt = fmaT(wBA[k * COLS + cc], Bt, wB[k * COLS + cc]);
+            ABt = ABt * wBA[k * COLS + cc];
+        }
+        ctot[2 * COLS + cc] = Bt;
+        ctot[3 * COLS + cc] = ABt;
+    }
+    cluster.sync();
+    // ---- carries across the cluster (distributed shared memory), then into each warp ----
+    if (isF || isB) {
+        T Lcl = (T)0, Lm = (T)0, Scl = (T)0, A1 = (T)0;
+        for (int r = 0; r < CL; ++r) {
+            const T* ot = cluster.map_shared_rank(ctot, r);
+            const T f = ot[cc], af = ot[COLS + cc];
+            if (r < rk) Lcl = fmaT(af, Lcl, f);
+            Lm = fmaT(af, Lm, f);
+        }
+        for (int r = CL - 1; r >= 0; --r) {
+            const T* ot = cluster.map_shared_rank(ctot, r);
+            const T bb = ot[2 * COLS + cc], ab = ot[3 * COLS + cc];
+            if (r > rk) Scl = fmaT(ab, Scl, bb);
+            A1 = fmaT(ab, A1, bb);
+        }
+        if (isF) {
+            T Y = Lcl;
+            for (int k = 0; k < WARPS; ++k) {
+                wY[k * COLS + cc] = Y;
+                Y = fmaT(wFA[k * COLS + cc], Y, wF[k * COLS + cc]);
+            }
+            // column-global constants of the closed form
+            const T rh = ccon[cc], i1 = ccon[3 * COLS + cc];
+            const T A2 = rh * Lm;
+            const T rhom = powi_T(rh, m);
+            const T z1 = (A1 - rhom * A2) * i1;
+            const T rr = rh * rh;
+            const T beta = rr / ((T)1 + rr * (((T)1 - rhom * rhom) * i1));
+            const T bz1 = beta * z1;
+            ccon[4 * COLS + cc] = bz1;
+            ccon[5 * COLS + cc] = A2 - bz1 * rhom;   // A2'
+        }
+        if (isB) {
+            T X = Scl;
+            for (int k = WARPS - 1; k >= 0; --k) {
+                wX[k * COLS + cc] = X;
+                X = fmaT(wBA[k * COLS + cc], X, wB[k * COLS + cc]);
+            }
+        }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");   // this CTA's totals are no longer read
+    __syncthreads();
+    if (nv_ld > 0) {
+        const T Lin = fmaT(afx, wY[warp * COLS + cl], vfx);
+        const T Sbelow = fmaT(abx, wX[warp * COLS + cl], vbx);
+        const T K = ccon[2 * COLS + cl], bz1 = ccon[4 * COLS + cl], A2p = ccon[5 * COLS + cl];
+        const T dtT = (T)a.dt;
+        T pu = powi_T(rhoS, rk * SEGS + sg);                 // ρ^{j0−1} (all earlier segments are full)
+        T pd = powi_T(rho, m + 1 - (j0 + nvalid - 1));       // ρ^{m+1−e}, e = last valid row
+        T L = Lin, R = rho * Sbelow;
+        T* pq = static_cast<T*>(a.prev) + b * a.mstride + col + int64_t(j0 + nvalid) * a.pitch;  // last valid row
+        if (nvalid == SR) {
+#pragma unroll
+            for (int k = 0; k < SR; ++k) {   // forward walk: pv_j ← K·(L_j − βz₁ρ^{j−1}) ∓ prev_j
+                L = fmaT(rho, L, zrow[k * COLS]);
+                const T lc = K * fmaT(-bz1, pu, L);
+                pv[k] = (MODE == 0) ? (lc - pv[k]) : fmaT(dtT, pv[k], lc);
+                pu = pu * rho;
+            }
+#pragma unroll
+            for (int k = SR - 1; k >= 0; --k) {   // backward walk: u^{n+1}_j = pv_j + K·(R_j − ρ^{m+1−j} A₂')
+                *pq = fmaT(K, fmaT(-pd, A2p, R), pv[k]);
+                pq -= a.pitch;
+                pd = pd * rho;
+                R = rho * (zrow[k * COLS] + R);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < SR; ++k) {
+                if (k < nvalid) {
+                    L = fmaT(rho, L, zrow[k * COLS]);
+                    const T lc = K * fmaT(-bz1, pu, L);
+                    pv[k] = (MODE == 0) ? (lc - pv[k]) : fmaT(dtT, pv[k], lc);
+                    pu = pu * rho;
+                }
+            }
+#pragma unroll
+            for (int k = SR - 1; k >= 0; --k) {
+                if (k < nvalid) {
+                    *pq = fmaT(K, fmaT(-pd, A2p, R), pv[k]);
+                    pq -= a.pitch;
+                    pd = pd * rho;
+                    R = rho * (zrow[k * COLS] + R);
+                }
+            }
+        }
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------------------

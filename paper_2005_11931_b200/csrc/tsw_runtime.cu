@@ -104,6 +104,7 @@ int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
 // row's padding; for the first/last row of the array those bytes lie outside it (their values
 // are never used and never written).
 constexpr size_t GUARD = 16384;
+constexpr int IMP_SCAN_MAX = 8192;  // unknowns per line of the implicit scan solvers
 // `shift` bytes: the returned pointer is a VIEW that many bytes into the array (row-structured
 // arrays of slabs with G ghost rows per side are addressed so that storage row 1 is the first owned
 // row; ghost rows sit at rows 0, −1, …, 2 − G).
@@ -186,6 +187,10 @@ struct tsw_ctx {
     void* imp_s1 = nullptr;   // implicit: x-solve output (field layout)
     void* imp_t = nullptr;    // implicit: transposed field [B][nx][pt]
     int64_t imp_pt = 0;       // its pitch (≥ ny, multiple of 32)
+    int imp_solver = 0;       // 0: scan solvers (R28, default); 1: cyclic reduction (the paper's)
+    void* imp_tab = nullptr;  // x-line LU tables [B][3][imp_tpitch] (scan solver)
+    int64_t imp_tpitch = 0;
+    bool imp_fact_valid = false;
     int tb_depth = 4;     // its input ring stages
     int tb_occ[2][9] = {};  // [f64][K] resident CTAs per SM (cached)
     int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
@@ -275,6 +280,113 @@ int cr_levels(int64_t m) {
     return q;
 }
 
+// Scan solvers (R28): k_imp_x (rows, shared LU) → z in imp_s1; k_imp_y (columns, Toeplitz closed
+// form) fused with the three-level update over buf[ip].  5 words of HBM traffic per node.
+template <typename T, int R>
+tsw_status launch_imp_x(tsw_ctx* c, const ImpXArgs& ax) {
+    const int threads = int(round_up((c->g.nx + R - 1) / R, 32));
+    if (threads > 1024) return fail(TSW_ERR_ARG, "implicit x solver: row too long");
+    const size_t smem = size_t(10) * threads * sizeof(T);
+    CK(cudaFuncSetAttribute(k_imp_x<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_imp_x<T, R>, threads, smem));
+    if (occ < 1) return fail(TSW_ERR_ARG, "implicit x solver does not fit on an SM");
+    const int64_t want = (int64_t(occ) * c->sm_count + c->g.batch - 1) / c->g.batch;
+    const unsigned gx = unsigned(std::max<int64_t>(1, std::min<int64_t>(ax.nrows, want)));
+    k_imp_x<T, R><<<dim3(gx, unsigned(c->g.batch)), threads, smem, c->stream>>>(ax);
+    CKL();
+    return TSW_OK;
+}
+
+template <typename T>
+tsw_status implicit_level_scan_t(tsw_ctx* c, bool start) {
+    const int64_t nx = c->g.nx, ny = c->g.ny;
+    const int m = int(nx - 2), my = int(ny - 2);
+    if (!c->imp_fact_valid) {
+        const size_t fsm = size_t(3 * m + 1) * sizeof(double);
+        CK(cudaFuncSetAttribute(k_imp_xfactor<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm)));
+        k_imp_xfactor<T><<<unsigned(c->g.batch), 256, fsm, c->stream>>>(
+            static_cast<const T*>(c->c1), c->cstride1, static_cast<T*>(c->imp_tab), c->imp_tpitch, m, c->g.batch);
+        CKL();
+        c->launches++;
+        c->imp_fact_valid = true;
+    }
+    ImpXArgs ax;
+    ax.src = c->buf[c->ic];
+    ax.dst = c->imp_s1;
+    ax.tab = c->imp_tab;
+    ax.pitch = c->pitch;
+    ax.mstride = c->mstride;
+    ax.tpitch = c->imp_tpitch;
+    ax.nx = int32_t(nx);
+    ax.row0 = 2;  // view row of global row 1
+    ax.nrows = my;
+    ax.scale = start ? 1.0 : 2.0;
+    tsw_status st;
+    constexpr int W = 32 / int(sizeof(T));  // one 32-byte access per thread
+    if (nx <= 1024 * W) st = launch_imp_x<T, W>(c, ax);
+    else st = launch_imp_x<T, 2 * W>(c, ax);
+    if (st) return st;
+    ImpYArgs ay;
+    ay.z = c->imp_s1;
+    ay.prev = c->buf[c->ip];
+    ay.cf = c->c2;
+    ay.pitch = c->pitch;
+    ay.mstride = c->mstride;
+    ay.cpitch = c->cstride2;
+    ay.nx = int32_t(nx);
+    ay.m = my;
+    ay.dt = c->dt;
+    {   // cluster-resident variant: a cluster of ≤ 8 CTAs holds the columns' full height on chip
+        using G = ImpYc<T>;
+        const int CL = (my + G::SEGS * G::SR - 1) / (G::SEGS * G::SR);
+        if (CL <= 8) {
+            const int segc = (my + CL * G::SEGS - 1) / (CL * G::SEGS);
+            const size_t smc = G::smem_bytes(segc);
+            ay.seg = segc;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(unsigned((m + G::COLS - 1) / G::COLS), unsigned(CL), unsigned(c->g.batch));
+            cfg.blockDim = dim3(IMPYC_THREADS, 1, 1);
+            cfg.dynamicSmemBytes = smc;
+            cfg.stream = c->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 1;
+            attr[0].val.clusterDim.y = unsigned(CL);
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (start) {
+                CK(cudaFuncSetAttribute(k_imp_yc<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smc)));
+                CK(cudaLaunchKernelEx(&cfg, k_imp_yc<T, 1>, ay));
+            } else {
+                CK(cudaFuncSetAttribute(k_imp_yc<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smc)));
+                CK(cudaLaunchKernelEx(&cfg, k_imp_yc<T, 0>, ay));
+            }
+            CKL();
+            c->launches += 2;
+            std::swap(c->ic, c->ip);
+            c->n++;
+            return TSW_OK;
+        }
+    }
+    ay.seg = int32_t(round_up((my + IMPY_SEGS - 1) / IMPY_SEGS, 8));
+    const size_t smem = (2 * size_t(IMPY_SEGS) * IMPY_COLS + size_t(ay.seg / 8) * IMPY_THREADS) * sizeof(T);
+    const dim3 gy(unsigned((m + IMPY_COLS - 1) / IMPY_COLS), unsigned(c->g.batch));
+    if (start) {
+        CK(cudaFuncSetAttribute(k_imp_y<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_imp_y<T, 1><<<gy, IMPY_THREADS, smem, c->stream>>>(ay);
+    } else {
+        CK(cudaFuncSetAttribute(k_imp_y<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_imp_y<T, 0><<<gy, IMPY_THREADS, smem, c->stream>>>(ay);
+    }
+    CKL();
+    c->launches += 2;
+    std::swap(c->ic, c->ip);
+    c->n++;
+    return TSW_OK;
+}
+
 template <typename T>
 tsw_status implicit_level_t(tsw_ctx* c, bool start) {
     const T dtT = (T)c->dt;
@@ -298,6 +410,7 @@ tsw_status implicit_level_t(tsw_ctx* c, bool start) {
         return TSW_OK;
     }
     const int64_t nx = c->g.nx, ny = c->g.ny;
+    if (c->imp_solver == 0) return implicit_level_scan_t<T>(c, start);
     // (1) x lines: (I − ½L_x) z = scale·u  on the interior rows (view rows 2 .. ny−1)
     CrArgs ax;
     ax.src = c->buf[c->ic];
@@ -737,6 +850,7 @@ tsw_status prescale_all(tsw_ctx* c) {
         }
     }
     c->launches += (c->g.dim == 2) ? 2 : 1;
+    c->imp_fact_valid = false;
     return TSW_OK;
 }
 
@@ -1141,6 +1255,7 @@ void tsw_destroy(tsw_ctx* c) {
     for (int k = 0; k < 4; ++k) dfree_guarded(c->buf[k], c->fshift);
     dfree_guarded(c->imp_s1, c->fshift);
     if (c->imp_t) cudaFree(c->imp_t);
+    if (c->imp_tab) cudaFree(c->imp_tab);
     dfree_guarded(c->h1, c->cshift_h);
     dfree_guarded(c->h2, c->cshift_h);
     dfree_guarded(c->c1, c->cshift);
@@ -1907,10 +2022,8 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "scheme must be 0 (leapfrog) or 1 (implicit)");
         if (value == 1) {
             if (c->g.nranks != 1) return fail(TSW_ERR_ARG, "the implicit scheme is single-rank");
-            const int64_t lim = (227 * 1024) / (4 * int64_t(c->esz));
-            if (c->g.dim == 2 && (c->g.nx - 2 > lim || c->g.ny - 2 > lim))
-                return fail(TSW_ERR_ARG, "implicit line solves keep a line in shared memory: at most %lld unknowns per line",
-                            (long long)lim);
+            if (c->g.dim == 2 && (c->g.nx - 2 > IMP_SCAN_MAX || c->g.ny - 2 > IMP_SCAN_MAX))
+                return fail(TSW_ERR_ARG, "implicit line solves: at most %d unknowns per line", IMP_SCAN_MAX);
             tsw_status st = set_dev(c);
             if (st) return st;
             const size_t fbytes = size_t(c->g.batch) * c->mstride * c->esz;
@@ -1924,8 +2037,25 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
                 CK(cudaMalloc(&c->imp_t, tbytes));
                 CK(cudaMemsetAsync(c->imp_t, 0, tbytes, c->stream));
             }
+            if (!c->imp_tab && c->g.dim == 2) {
+                c->imp_tpitch = round_up(c->g.nx, 32);
+                CK(cudaMalloc(&c->imp_tab, size_t(c->g.batch) * 3 * c->imp_tpitch * c->esz));
+                c->imp_fact_valid = false;
+            }
         }
         c->scheme = int(value);
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_IMPLICIT_SOLVER) {
+        if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "implicit solver must be 0 (scans) or 1 (cyclic reduction)");
+        if (value == 1 && c->g.dim == 2) {
+            int64_t lim = 1;  // largest 2^q − 1 whose four line arrays fit in 227 KB
+            while ((2 * lim + 1) * 4 * int64_t(c->esz) <= 227 * 1024) lim = 2 * lim + 1;
+            if (c->g.nx - 2 > lim || c->g.ny - 2 > lim)
+                return fail(TSW_ERR_ARG, "cyclic reduction keeps a line in shared memory: at most %lld unknowns per line",
+                            (long long)lim);
+        }
+        c->imp_solver = int(value);
         return TSW_OK;
     }
     if (key == TSW_OPT_TB_DEPTH) {

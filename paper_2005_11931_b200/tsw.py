@@ -31,6 +31,7 @@ TSW_OPT_GRAPHS = 5
 TSW_OPT_TBLOCK = 6
 TSW_OPT_TB_DEPTH = 7
 TSW_OPT_SCHEME = 8
+TSW_OPT_IMPLICIT_SOLVER = 9
 
 STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STATE", 4: "TSW_ERR_CUDA",
                 5: "TSW_ERR_NCCL", 6: "TSW_ERR_OOM", 7: "TSW_ERR_UNSTABLE"}
