@@ -2172,7 +2172,7 @@ struct ImpYc {
     static constexpr int SPW = 32 / COLS;              // segments per warp
     static constexpr int SR = 128 / int(sizeof(T));    // max rows per segment (registers)
     static __host__ __device__ size_t smem_bytes(int seg) {
-        return (size_t(SEGS) * seg * COLS + 6 * size_t(WARPS) * COLS + 12 * COLS) * sizeof(T);
+        return (size_t(SEGS) * seg * COLS + 4 * size_t(WARPS) * COLS + 12 * COLS) * sizeof(T);
     }
 };
 
@@ -2186,10 +2186,37 @@ __device__ __forceinline__ void cp_async_elem(T* sdst, const T* gsrc, bool valid
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gsrc), "r"(n) : "memory");
 }
 
+// Half-warp (16-lane) inclusive affine scans: forward (lane k combines lanes ≤ k), backward.
+template <typename T>
+__device__ __forceinline__ void half_affine_fwd(T& A, T& V, int k) {
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) {
+        const T Vu = __shfl_up_sync(0xffffffffu, V, off, 16);
+        const T Au = __shfl_up_sync(0xffffffffu, A, off, 16);
+        if (k >= off) {
+            V = fmaT(A, Vu, V);
+            A = A * Au;
+        }
+    }
+}
+template <typename T>
+__device__ __forceinline__ void half_affine_bwd(T& A, T& V, int k) {
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) {
+        const T Vd = __shfl_down_sync(0xffffffffu, V, off, 16);
+        const T Ad = __shfl_down_sync(0xffffffffu, A, off, 16);
+        if (k + off < 16) {
+            V = fmaT(A, Vd, V);
+            A = A * Ad;
+        }
+    }
+}
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
     using G = ImpYc<T>;
     constexpr int COLS = G::COLS, SR = G::SR, SEGS = G::SEGS, WARPS = G::WARPS;
+    static_assert(WARPS == 16, "one half-warp lane per warp of the CTA");
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = int(cluster.num_blocks());
@@ -2198,12 +2225,10 @@ __global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
     const int seg = a.seg;
     T* zs = reinterpret_cast<T*>(smem_raw);                 // [SEGS][seg][COLS]
     T* wF = zs + size_t(SEGS) * seg * COLS;                 // [WARPS][COLS] warp totals: forward value
-    T* wFA = wF + WARPS * COLS;                             //   forward factor
+    T* wFA = wF + WARPS * COLS;                             //   forward factor (→ carry factor into the warp)
     T* wB = wFA + WARPS * COLS;                             //   backward value
     T* wBA = wB + WARPS * COLS;                             //   backward factor
-    T* wY = wBA + WARPS * COLS;                             // [WARPS][COLS] carry into each warp (forward)
-    T* wX = wY + WARPS * COLS;                              //   (backward)
-    T* ctot = wX + WARPS * COLS;                            // [4][COLS] this CTA's totals (read by the cluster)
+    T* ctot = wBA + WARPS * COLS;                           // [4][COLS] this CTA's totals (read by the cluster)
     T* ccon = ctot + 4 * COLS;                              // [8][COLS] column constants
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int cl = lane % COLS, sl = lane / COLS;
@@ -2213,48 +2238,38 @@ __global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
     const int64_t col = colbase + cl;
     const bool colok = col <= a.nx - 2;
     const int m = a.m;
-    const int cta0 = 1 + rk * SEGS * seg;
-    const int j0 = cta0 + sg * seg;
+    const int j0 = 1 + (rk * SEGS + sg) * seg;
     int nvalid = m - j0 + 1;
     nvalid = nvalid < 0 ? 0 : (nvalid > seg ? seg : nvalid);
     const int nv_ld = colok ? nvalid : 0;
     T* zrow = zs + size_t(sg) * seg * COLS + cl;
-    // designated lanes: forward (column lane) and backward scans over warps / cluster ranks
-    const bool isF = (warp == 0 && lane < COLS);
-    const bool isB = (COLS == 32) ? (warp == 1) : (warp == 0 && lane >= COLS);
-    const int cc = (COLS == 32) ? lane : (lane % COLS);
-    // ---- issue every HBM read of this thread ----
-    T pv[SR];
+    // ---- stage this thread's segment of z (u^{n−1} is read just before pass 2) ----
     {
         const T* zq = static_cast<const T*>(a.z) + b * a.mstride + col + int64_t(1 + j0) * a.pitch;
-        const T* pq = static_cast<const T*>(a.prev) + b * a.mstride + col + int64_t(1 + j0) * a.pitch;
 #pragma unroll
         for (int k = 0; k < SR; ++k) {
             if (k < seg) cp_async_elem(zrow + k * COLS, zq, k < nv_ld);
-            pv[k] = (k < nv_ld) ? *pq : (T)0;
             zq += a.pitch;
-            pq += a.pitch;
         }
     }
     // ---- column constants (once per column) ----
-    if (isF) {
-        const int64_t cf = colbase + cc;
+    if (t < COLS) {
+        const int64_t cf = colbase + t;
         const double g = (cf <= a.nx - 2) ? (double)static_cast<const T*>(a.cf)[b * a.cpitch + cf] : 0.0;
         const double sq = sqrt(1.0 + 2.0 * g);
         const double rho_d = g / ((1.0 + g) + sq);
         const double kap_d = 0.5 * ((1.0 + g) + sq);
         const double omr = (1.0 + sq) / ((1.0 + g) + sq);  // 1 − ρ without cancellation
         const double i1_d = 1.0 / (omr * (1.0 + rho_d));    // 1/(1 − ρ²)
-        const T rho = (T)rho_d;
-        ccon[0 * COLS + cc] = rho;
-        ccon[1 * COLS + cc] = powi_T(rho, seg);
-        ccon[2 * COLS + cc] = (T)(i1_d / kap_d);   // K
-        ccon[3 * COLS + cc] = (T)i1_d;
+        ccon[t] = (T)rho_d;
+        ccon[1 * COLS + t] = (T)(i1_d / kap_d);   // K
+        ccon[2 * COLS + t] = (T)i1_d;
     }
     __syncthreads();
-    const T rho = ccon[cl], rhoS = ccon[COLS + cl];
+    const T rho = ccon[cl];
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    // ---- segment sums: F (forward, to the last valid row), B (backward, from the segment start) ----
+    // ---- segment sums: F (forward, to the last valid row), B (backward, from the segment start);
+    //      both carry factors are ρ^{nvalid} (everything after a partial segment is zero) ----
     T F = (T)0, Bsum = (T)0, pw = (T)1;
     if (nvalid == SR) {
 #pragma unroll
@@ -2272,8 +2287,7 @@ __global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
             pw = pw * rho;
         }
     }
-    T Af = pw, Vf = F;        // forward factor ρ^{nvalid}
-    T Ab = rhoS, Vb = Bsum;   // backward factor ρ^{seg}
+    T Af = pw, Vf = F, Ab = pw, Vb = Bsum;
     T vfx = (T)0, afx = (T)1, vbx = (T)0, abx = (T)1;
     if constexpr (G::SPW > 1) {
         warp_affine_fwd(Af, Vf, lane, COLS);
@@ -2300,109 +2314,134 @@ __global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
         wBA[warp * COLS + cl] = Ab;
     }
     __syncthreads();
-    // ---- CTA totals ----
-    if (isF) {
-        T Ft = (T)0, AFt = (T)1;
-        for (int k = 0; k < WARPS; ++k) {
-            Ft = fmaT(wFA[k * COLS + cc], Ft, wF[k * COLS + cc]);
-            AFt = AFt * wFA[k * COLS + cc];
+    // ---- scans over the 16 warps.  Jobs (column, direction) per half-warp; a backward scan runs
+    //      as a forward scan over reversed elements, so both halves issue identical shuffles ----
+    constexpr int NQ = (COLS == 16) ? 1 : 2;   // rounds
+    const int h = lane >> 4, k = lane & 15;
+    T exA[NQ], exV[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int jc = (COLS == 16) ? warp : 2 * warp + h;   // column of this job
+        const int dir = (COLS == 16) ? h : q;
+        const int e = dir == 0 ? k : 15 - k;                  // warp index of this lane's element
+        T A = dir == 0 ? wFA[e * COLS + jc] : wBA[e * COLS + jc];
+        T V = dir == 0 ? wF[e * COLS + jc] : wB[e * COLS + jc];
+        half_affine_fwd(A, V, k);
+        T Ax = __shfl_up_sync(0xffffffffu, A, 1, 16), Vx = __shfl_up_sync(0xffffffffu, V, 1, 16);
+        if (k == 0) {
+            Ax = (T)1;
+            Vx = (T)0;
         }
-        ctot[cc] = Ft;
-        ctot[COLS + cc] = AFt;
-    }
-    if (isB) {
-        T Bt = (T)0, ABt = (T)1;
-        for (int k = WARPS - 1; k >= 0; --k) {
-            Bt = fmaT(wBA[k * COLS + cc], Bt, wB[k * COLS + cc]);
-            ABt = ABt * wBA[k * COLS + cc];
+        exA[q] = Ax;
+        exV[q] = Vx;
+        if (k == 15) {
+            ctot[(2 * dir) * COLS + jc] = V;
+            ctot[(2 * dir + 1) * COLS + jc] = A;
         }
-        ctot[2 * COLS + cc] = Bt;
-        ctot[3 * COLS + cc] = ABt;
     }
     cluster.sync();
-    // ---- carries across the cluster (distributed shared memory), then into each warp ----
-    if (isF || isB) {
-        T Lcl = (T)0, Lm = (T)0, Scl = (T)0, A1 = (T)0;
-        for (int r = 0; r < CL; ++r) {
-            const T* ot = cluster.map_shared_rank(ctot, r);
-            const T f = ot[cc], af = ot[COLS + cc];
-            if (r < rk) Lcl = fmaT(af, Lcl, f);
-            Lm = fmaT(af, Lm, f);
-        }
-        for (int r = CL - 1; r >= 0; --r) {
-            const T* ot = cluster.map_shared_rank(ctot, r);
-            const T bb = ot[2 * COLS + cc], ab = ot[3 * COLS + cc];
-            if (r > rk) Scl = fmaT(ab, Scl, bb);
-            A1 = fmaT(ab, A1, bb);
-        }
-        if (isF) {
-            T Y = Lcl;
-            for (int k = 0; k < WARPS; ++k) {
-                wY[k * COLS + cc] = Y;
-                Y = fmaT(wFA[k * COLS + cc], Y, wF[k * COLS + cc]);
-            }
-            // column-global constants of the closed form
-            const T rh = ccon[cc], i1 = ccon[3 * COLS + cc];
-            const T A2 = rh * Lm;
-            const T rhom = powi_T(rh, m);
-            const T z1 = (A1 - rhom * A2) * i1;
-            const T rr = rh * rh;
-            const T beta = rr / ((T)1 + rr * (((T)1 - rhom * rhom) * i1));
-            const T bz1 = beta * z1;
-            ccon[4 * COLS + cc] = bz1;
-            ccon[5 * COLS + cc] = A2 - bz1 * rhom;   // A2'
-        }
-        if (isB) {
-            T X = Scl;
-            for (int k = WARPS - 1; k >= 0; --k) {
-                wX[k * COLS + cc] = X;
-                X = fmaT(wBA[k * COLS + cc], X, wB[k * COLS + cc]);
-            }
-        }
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");   // this CTA's totals are no longer read
-    __syncthreads();
-    if (nv_ld > 0) {
-        const T Lin = fmaT(afx, wY[warp * COLS + cl], vfx);
-        const T Sbelow = fmaT(abx, wX[warp * COLS + cl], vbx);
-        const T K = ccon[2 * COLS + cl], bz1 = ccon[4 * COLS + cl], A2p = ccon[5 * COLS + cl];
-        const T dtT = (T)a.dt;
-        T pu = powi_T(rhoS, rk * SEGS + sg);                 // ρ^{j0−1} (all earlier segments are full)
-        T pd = powi_T(rho, m + 1 - (j0 + nvalid - 1));       // ρ^{m+1−e}, e = last valid row
-        T L = Lin, R = rho * Sbelow;
-        T* pq = static_cast<T*>(a.prev) + b * a.mstride + col + int64_t(j0 + nvalid) * a.pitch;  // last valid row
-        if (nvalid == SR) {
+    // ---- scans over the cluster's CTAs (distributed shared memory, one rank per lane) ----
 #pragma unroll
-            for (int k = 0; k < SR; ++k) {   // forward walk: pv_j ← K·(L_j − βz₁ρ^{j−1}) ∓ prev_j
-                L = fmaT(rho, L, zrow[k * COLS]);
-                const T lc = K * fmaT(-bz1, pu, L);
-                pv[k] = (MODE == 0) ? (lc - pv[k]) : fmaT(dtT, pv[k], lc);
-                pu = pu * rho;
-            }
-#pragma unroll
-            for (int k = SR - 1; k >= 0; --k) {   // backward walk: u^{n+1}_j = pv_j + K·(R_j − ρ^{m+1−j} A₂')
-                *pq = fmaT(K, fmaT(-pd, A2p, R), pv[k]);
-                pq -= a.pitch;
-                pd = pd * rho;
-                R = rho * (zrow[k * COLS] + R);
+    for (int q = 0; q < NQ; ++q) {
+        const int jc = (COLS == 16) ? warp : 2 * warp + h;
+        const int dir = (COLS == 16) ? h : q;
+        const int e = dir == 0 ? k : 15 - k;
+        T A = (T)1, V = (T)0;
+        if (k < CL) {
+            const int r = dir == 0 ? k : CL - 1 - k;
+            const T* ot = cluster.map_shared_rank(ctot, r);
+            V = ot[(2 * dir) * COLS + jc];
+            A = ot[(2 * dir + 1) * COLS + jc];
+        }
+        half_affine_fwd(A, V, k);
+        const int kr = dir == 0 ? rk : CL - 1 - rk;           // lane of this CTA's rank
+        const int src = (h << 4) + (kr > 0 ? kr - 1 : 0);
+        T A2x = __shfl_sync(0xffffffffu, A, src), V2x = __shfl_sync(0xffffffffu, V, src);
+        if (kr == 0) {
+            A2x = (T)1;
+            V2x = (T)0;
+        }
+        const T Atot = __shfl_sync(0xffffffffu, A, (h << 4) + 15);
+        const T Vtot = __shfl_sync(0xffffffffu, V, (h << 4) + 15);
+        // carry into warp e (value and factor: everything before / after it in the column)
+        if (dir == 0) {
+            wF[e * COLS + jc] = fmaT(exA[q], V2x, exV[q]);
+            wFA[e * COLS + jc] = exA[q] * A2x;
+            if (k == 0) {
+                ccon[3 * COLS + jc] = Vtot;   // L_m
+                ccon[4 * COLS + jc] = Atot;   // ρ^m
             }
         } else {
+            wB[e * COLS + jc] = fmaT(exA[q], V2x, exV[q]);
+            wBA[e * COLS + jc] = exA[q] * A2x;
+            if (k == 0) ccon[5 * COLS + jc] = Vtot;   // A1 = Σ ρ^{i−1} z_i
+        }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");   // totals no longer read remotely
+    __syncthreads();
+    if (t < COLS) {   // column-global constants of the closed form
+        const T rh = ccon[t], i1 = ccon[2 * COLS + t];
+        const T Lm = ccon[3 * COLS + t], rhom = ccon[4 * COLS + t], A1 = ccon[5 * COLS + t];
+        const T A2 = rh * Lm;
+        const T z1 = (A1 - rhom * A2) * i1;
+        const T rr = rh * rh;
+        const T beta = rr / ((T)1 + rr * (((T)1 - rhom * rhom) * i1));
+        const T bz1 = beta * z1;
+        ccon[6 * COLS + t] = bz1;
+        ccon[7 * COLS + t] = A2 - bz1 * rhom;   // A2'
+    }
+    __syncthreads();
+    if (nv_ld > 0) {
+        // pass 2 in 8-row blocks, bottom block first: a forward pre-walk records L and ρ^{j−1} at
+        // each block start; each block then reads its u^{n−1}, walks forward (L_j) and backward (R_j)
+        constexpr int NBLK = SR / 8;
+        const T K = ccon[COLS + cl], bz1 = ccon[6 * COLS + cl], A2p = ccon[7 * COLS + cl];
+        const T dtT = (T)a.dt;
+        T Lb[NBLK], pub[NBLK];
+        {
+            T L = fmaT(afx, wF[warp * COLS + cl], vfx);   // L_{j0−1}
+            T pu = afx * wFA[warp * COLS + cl];           // ρ^{j0−1}
 #pragma unroll
-            for (int k = 0; k < SR; ++k) {
-                if (k < nvalid) {
-                    L = fmaT(rho, L, zrow[k * COLS]);
-                    const T lc = K * fmaT(-bz1, pu, L);
-                    pv[k] = (MODE == 0) ? (lc - pv[k]) : fmaT(dtT, pv[k], lc);
-                    pu = pu * rho;
+            for (int q = 0; q < NBLK; ++q) {
+                Lb[q] = L;
+                pub[q] = pu;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    if (8 * q + kk < nvalid) {
+                        L = fmaT(rho, L, zrow[(8 * q + kk) * COLS]);
+                        pu = pu * rho;
+                    }
                 }
             }
+        }
+        T R = rho * fmaT(abx, wB[warp * COLS + cl], vbx);   // R at the last valid row
+        T pd = rho * (abx * wBA[warp * COLS + cl]);         // ρ^{m+1−e}, e = last valid row
+        const T* pbase = static_cast<const T*>(a.prev) + b * a.mstride + col + int64_t(1 + j0) * a.pitch;
 #pragma unroll
-            for (int k = SR - 1; k >= 0; --k) {
-                if (k < nvalid) {
-                    *pq = fmaT(K, fmaT(-pd, A2p, R), pv[k]);
-                    pq -= a.pitch;
-                    pd = pd * rho;
-                    R = rho * (zrow[k * COLS] + R);
+        for (int q = NBLK - 1; q >= 0; --q) {
+            if (8 * q < nvalid) {
+                T w[8];
+                const T* pq = pbase + int64_t(8 * q) * a.pitch;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) w[kk] = (8 * q + kk < nvalid) ? pq[int64_t(kk) * a.pitch] : (T)0;
+                T L = Lb[q], pu = pub[q];
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {   // w_j ← K·(L_j − βz₁ρ^{j−1}) ∓ prev_j
+                    if (8 * q + kk < nvalid) {
+                        L = fmaT(rho, L, zrow[(8 * q + kk) * COLS]);
+                        const T lc = K * fmaT(-bz1, pu, L);
+                        w[kk] = (MODE == 0) ? (lc - w[kk]) : fmaT(dtT, w[kk], lc);
+                        pu = pu * rho;
+                    }
+                }
+                T* po = const_cast<T*>(pq);
+#pragma unroll
+                for (int kk = 7; kk >= 0; --kk) {   // u^{n+1}_j = w_j + K·(R_j − ρ^{m+1−j} A₂')
+                    if (8 * q + kk < nvalid) {
+                        po[int64_t(kk) * a.pitch] = fmaT(K, fmaT(-pd, A2p, R), w[kk]);
+                        pd = pd * rho;
+                        R = rho * (zrow[(8 * q + kk) * COLS] + R);
+                    }
                 }
             }
         }
