@@ -206,8 +206,10 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
 
 /* Options: TSW_OPT_ROWS_PER_ITEM — rows per warp work item of the 2D stencil (≥ 1; 0 = auto);
  *          TSW_OPT_KERNEL / TSW_OPT_DEPTH — stencil variant and its ring depth;
- *          TSW_OPT_TIME_KERNELS — 1: bracket every stencil launch with CUDA events on the ctx
- *          stream (for tsw_kernel_stats), 0: off; setting it resets the statistics. */
+ *          TSW_OPT_TIME_KERNELS — 1: bracket every stencil launch (leapfrog) or every y-line
+ *          solve launch k_imp_yc (implicit scan solver, the dominant kernel of a level) with CUDA
+ *          events on the ctx stream (for tsw_kernel_stats), 0: off; setting it resets the
+ *          statistics. */
 #define TSW_OPT_ROWS_PER_ITEM 1
 #define TSW_OPT_TIME_KERNELS 2
 #define TSW_OPT_KERNEL 3 /* 0: CTA-wide TMA bulk-copy row pipeline (default); 1: register-prefetch kernel */
@@ -232,8 +234,9 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               (the paper's solver), ≤ 227 KB/(4·sizeof(T)) unknowns per line. */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
 
-/* Live per-kernel timing of the stencil (S2/S3) launches recorded since TSW_OPT_TIME_KERNELS was
- * set: total device milliseconds, number of launches, and interior point-updates they performed.
+/* Live per-kernel timing of the launches TSW_OPT_TIME_KERNELS brackets (stencil S2/S3, or the
+ * implicit y solve) since it was set: total device milliseconds, number of launches, and interior
+ * point-updates they performed.
  * Synchronises.  Any pointer may be NULL. */
 tsw_status tsw_kernel_stats(tsw_ctx* ctx, double* total_ms, int64_t* launches, int64_t* updates);
 

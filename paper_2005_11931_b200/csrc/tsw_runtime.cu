@@ -356,6 +356,12 @@ tsw_status implicit_level_scan_t(tsw_ctx* c, bool start) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (c->timing) {   // live timing of the dominant implicit kernel
+                tsw_status st2 = timing_events(c, &e0, &e1);
+                if (st2) return st2;
+                CK(cudaEventRecord(e0, c->stream));
+            }
             if (start) {
                 CK(cudaFuncSetAttribute(k_imp_yc<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smc)));
                 CK(cudaLaunchKernelEx(&cfg, k_imp_yc<T, 1>, ay));
@@ -364,6 +370,11 @@ tsw_status implicit_level_scan_t(tsw_ctx* c, bool start) {
                 CK(cudaLaunchKernelEx(&cfg, k_imp_yc<T, 0>, ay));
             }
             CKL();
+            if (c->timing) {
+                CK(cudaEventRecord(e1, c->stream));
+                c->timed_launches++;
+                c->timed_updates += int64_t(m) * my * c->g.batch;
+            }
             c->launches += 2;
             std::swap(c->ic, c->ip);
             c->n++;
