@@ -558,22 +558,23 @@ struct TbState {
     bool colint[V];
 };
 
-template <typename T, int K, int PH>
-__device__ __forceinline__ void tb_row(TbState<T, K>& S, T* __restrict__ cen, int e0, int rowlo, int rowhi, int R,
-                                       const T (&nw)[2], const T (&pv_new)[2], T dtT, T (&lastk)[2]) {
+// One input row of the wavefront.  `cr` / `cw`: this thread's element in the centre-row buffers
+// of the previous / current row parity (level m at offset m·2·WEP).  MASKED: force the Dirichlet
+// rows/columns to +0 (only items whose dependency cone touches them need it).
+template <typename T, int K, int PH, bool MASKED>
+__device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
+                                       int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2]) {
     constexpr int V = 2;
     constexpr int WEP = TbGeom<T, K>::WE + 2 * TbPad<T>::P;
     constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
-    const int par = R & 1;
     // level 0
 #pragma unroll
     for (int k = 0; k < V; ++k) S.w[0][O][k] = nw[k];
-    sts_v2(cen + par * WEP + e0, nw);
+    sts_v2(cw, nw);
 #pragma unroll
     for (int m = 1; m <= K; ++m) {
         // level m−1 after its update: rows (r−1, r, r+1) in slots (C, N, O); level m−2: row r in C
-        const bool rowok = unsigned(R - m - rowlo) <= unsigned(rowhi - rowlo);
-        const T* ce = cen + ((m - 1) * 2 + (par ^ 1)) * WEP + e0;
+        const T* ce = cr + (m - 1) * 2 * WEP;
         const T left = ce[-1];
         const T right = ce[V];
         // canonical tree with shared face fluxes:
@@ -585,6 +586,8 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, T* __restrict__ cen, in
         const T F1 = r_mul(S.c1r[0], r_sub(u1, u0));
         const T F2 = r_mul(S.c1r[1], r_sub(right, u1));
         T nv[V];
+        bool rowok = true;
+        if (MASKED) rowok = unsigned(R - m - rowlo) <= unsigned(rowhi - rowlo);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const T cu = S.w[m - 1][N][k];
@@ -600,12 +603,17 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, T* __restrict__ cen, in
             const T lap = r_add(lapx, r_sub(gu, gd));
             const T pr = (m == 1) ? S.pm1[k] : S.w[(m >= 2) ? m - 2 : 0][C][k];
             const T v = r_add(r_sub(r_mul((T)2, cu), pr), lap);
-            nv[k] = (rowok && S.colint[k]) ? v : (T)0;
+            if (MASKED) {
+                const bool ok = rowok & S.colint[k];
+                nv[k] = ok ? v : (T)0;
+            } else {
+                nv[k] = v;
+            }
         }
         if (m < K) {
 #pragma unroll
             for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
-            sts_v2(cen + (m * 2 + par) * WEP + e0, nv);
+            sts_v2(cw + m * 2 * WEP, nv);
         } else {
 #pragma unroll
             for (int k = 0; k < V; ++k) lastk[k] = nv[k];
@@ -699,8 +707,12 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
             S.c2v[k] = S.colint[k] ? __ldg(c2b + gcol) : (T)0;
         }
         const bool out_cols = (e0 >= H) && (e0 < H + WO) && (cs - H + e0 < a.pitch);
-        T* ok = a.out_k + b * a.mstride + gc0;
-        T* okm1 = a.out_km1 + b * a.mstride + gc0;
+        // running output pointers: row ro = R − K of the current input row R = in_lo + i
+        T* okp = a.out_k + b * a.mstride + gc0 + int64_t(in_lo - K) * a.pitch;
+        T* okm1p = a.out_km1 + b * a.mstride + gc0 + int64_t(in_lo - K) * a.pitch;
+        // Dirichlet masking is only needed where the item's dependency cone (rows in_lo − K ..
+        // s1 + K − 1, the extended strip's columns) touches a boundary row/column or the grid edge
+        const bool masked = !((in_lo - K >= rowlo) && (s1 + K - 1 <= rowhi) && (cs - H >= 1) && (cs - H + WE <= a.nx - 1));
 #pragma unroll
         for (int m = 0; m < K; ++m)
 #pragma unroll
@@ -718,8 +730,9 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
         const int L = s1 + K - in_lo;
 
         // one input row: barrier, refill, stage read, wavefront (phase PH), output
-        auto row = [&](auto ph, int i) {
+        auto row = [&](auto ph, auto msk, int i) {
             constexpr int PH = decltype(ph)::value;
+            constexpr bool MASKED = decltype(msk)::value;
             const int R = in_lo + i;
             __syncthreads();  // the previous rows' stages and centre rows are consumed / published
             // refill the consumed stages two at a time (their shared-memory reads completed before
@@ -746,7 +759,10 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
                 for (int k = 0; k < V; ++k) nw[k] = pv_new[k] = (T)0;
             }
             T lastk[V];
-            tb_row<T, K, PH>(S, cen, e0, rowlo, rowhi, R, nw, pv_new, a.dtT, lastk);
+            const int par = R & 1;
+            T* cw = cen + par * WEP + e0;
+            const T* cr = cen + (par ^ 1) * WEP + e0;
+            tb_row<T, K, PH, MASKED>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
                 // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH
@@ -754,18 +770,26 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
                 T o2[V];
 #pragma unroll
                 for (int k = 0; k < V; ++k) o2[k] = S.w[K - 1][NS][k];
-                stg_v2(ok + int64_t(ro) * a.pitch, lastk);
-                stg_v2(okm1 + int64_t(ro) * a.pitch, o2);
+                stg_v2(okp, lastk);
+                stg_v2(okm1p, o2);
             }
+            okp += a.pitch;
+            okm1p += a.pitch;
         };
-        int i = 0;
-        for (; i + 3 <= L; i += 3) {
-            row(std::integral_constant<int, 0>{}, i);
-            row(std::integral_constant<int, 1>{}, i + 1);
-            row(std::integral_constant<int, 2>{}, i + 2);
-        }
-        if (i < L) row(std::integral_constant<int, 0>{}, i++);
-        if (i < L) row(std::integral_constant<int, 1>{}, i++);
+        auto run_rows = [&](auto msk) {
+            int i = 0;
+            for (; i + 3 <= L; i += 3) {
+                row(std::integral_constant<int, 0>{}, msk, i);
+                row(std::integral_constant<int, 1>{}, msk, i + 1);
+                row(std::integral_constant<int, 2>{}, msk, i + 2);
+            }
+            if (i < L) row(std::integral_constant<int, 0>{}, msk, i++);
+            if (i < L) row(std::integral_constant<int, 1>{}, msk, i++);
+        };
+        if (masked)
+            run_rows(std::integral_constant<bool, true>{});
+        else
+            run_rows(std::integral_constant<bool, false>{});
     }
 }
 
