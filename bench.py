@@ -7,8 +7,8 @@ GPU (global grid 32768 × 4096·N, dx = dy = 0.0025, ε = 0.05, dt = 4e−4), de
 data (SURVEY §8(d) data-independence guard), fp64 by default.  One "step" = one pass of the
 hot path over the slab: the leapfrog stencil (S3), the NCCL ghost-row exchange at N > 1 (S4),
 and the discrete-energy reduction every `--energy-every` steps (S5).  By default the stencil is
-temporally blocked (`--tblock 5`: 5 levels per HBM pass, K-deep ghost rows exchanged every 5
-levels on slabs); `--tblock 1` times the one-level-per-pass kernel.  Inputs (2 × 1.07 GB per
+temporally blocked (K levels per HBM pass — 4 in fp64, 8 in fp32 by default — with K-deep ghost
+rows exchanged every K levels on slabs); `--tblock 1` times the one-level-per-pass kernel.  Inputs (2 × 1.07 GB per
 GPU in fp64) exceed the 126 MB L2, so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f64|f32] [--impl tsw|reference]
@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "2D stencil Gpoint-updates/s & HBM GB/s vs 8 TB/s peak, at 1/2/4/8 B200"
 UNIT = "Gpt/s"
 ESZ = {"f64": 8, "f32": 4}
+TB_DEFAULT = {"f64": 4, "f32": 8}   # levels per HBM pass (sweep optimum on B200, profiles/r01)
 
 
 def host_cores() -> int:
@@ -364,8 +365,9 @@ def main():
                     help="config4: the weak-scaling unit (default, the BASELINE metric's scaling "
                          "workload); config5: 65-member eps family x 2048^2; config3: 4096^2 delta line; "
                          "table1: the paper's implicit method on its Table 1 set-up (4096^2, dt 0.05)")
-    ap.add_argument("--tblock", type=int, default=5,
-                    help="levels per HBM pass of the temporally blocked stencil (1 = per-step TMA kernel)")
+    ap.add_argument("--tblock", type=int, default=0,
+                    help="levels per HBM pass of the temporally blocked stencil (1 = per-step TMA kernel; "
+                         "0 = per dtype: 4 for f64, 8 for f32 — the sweep optimum, tools/sweep.py)")
     args = ap.parse_args()
 
     from paper_2005_11931_b200 import inputs, parallel
@@ -390,7 +392,7 @@ def main():
         parallel.init_process_group("nccl")
     dev = torch.device("cuda", local)
 
-    def run(dtype: str, full: bool):
+    def run(dtype: str, full: bool, tblock: int):
         npdt = np.float64 if dtype == "f64" else np.float32
         stream = torch.cuda.Stream(device=dev)
         s = tsw.Solver.from_config(cfg, dtype, rank=rank, nranks=world, device=local, stream=stream.cuda_stream)
@@ -478,15 +480,15 @@ def main():
         torch.cuda.empty_cache()
         return res
 
-    tblock = args.tblock  # slabs exchange K ghost rows of both levels every K levels
-    main_res = run(args.dtype, True)
+    # slabs exchange K ghost rows of both levels every K levels
+    tblock = args.tblock or TB_DEFAULT[args.dtype]
+    main_res = run(args.dtype, True, tblock)
     other = "f32" if args.dtype == "f64" else "f64"
-    also = None if args.no_also else run(other, False)
+    tblock_other = args.tblock or TB_DEFAULT[other]
+    also = None if args.no_also else run(other, False, tblock_other)
     per_step = None
     if tblock > 1 and not args.no_also:
-        tb_saved, tblock = tblock, 1
-        per_step = run(args.dtype, False)  # the one-level-per-pass kernel on the same workload
-        tblock = tb_saved
+        per_step = run(args.dtype, False, 1)  # the one-level-per-pass kernel on the same workload
 
     if rank == 0:
         peak, peak_src = measured_peak()
@@ -532,8 +534,9 @@ def main():
             line["e2e"] = main_res["e2e"]
         if also:
             e2 = ESZ[other]
-            ach2 = also["kernel_updates_per_launch"] / (also["kernel_avg_ms"] * 1e-3) * words * e2 / 1e9
-            line["also"] = {"dtype": other, "value": also["value"], "unit": UNIT,
+            words2 = 3.0 if tblock_other == 1 else 4.0 / tblock_other
+            ach2 = also["kernel_updates_per_launch"] / (also["kernel_avg_ms"] * 1e-3) * words2 * e2 / 1e9
+            line["also"] = {"dtype": other, "value": also["value"], "unit": UNIT, "temporal_blocking": tblock_other,
                             "ms_per_step": also["ms"] / args.steps, "roofline_frac": ach2 / peak, "achieved_gbs": ach2}
         if per_step:
             ach1 = per_step["kernel_updates_per_launch"] * 3 * esz / (per_step["kernel_avg_ms"] * 1e-3) / 1e9

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 200 python tools/sweep.py --dtype f64 --steps 20 --depths 4 --tblocks 5 --tbdepths 4 > gpurun_out/sweep_plain.log 2>&1; echo plain=$?
-tail -3 gpurun_out/sweep_plain.log
-timeout 400 ncu --set full --import-source on --clock-control none -k regex:"k_step2d_tb" --launch-skip 3 -c 1 -o gpurun_out/prof_tb5_v3 -f python tools/sweep.py --dtype f64 --steps 20 --depths 4 --tblocks 5 --tbdepths 4 > gpurun_out/ncu_tb.log 2>&1; echo ncu=$?
+timeout 200 python tools/sweep.py --dtype f32 --steps 20 --depths 4 --tblocks 8 --tbdepths 4 > gpurun_out/sweep_plain.log 2>&1; echo plain=$?
+timeout 400 ncu --set full --import-source on --clock-control none -k regex:"k_step2d_tb" --launch-skip 3 -c 1 -o gpurun_out/prof_tb8_f32 -f python tools/sweep.py --dtype f32 --steps 20 --depths 4 --tblocks 8 --tbdepths 4 > gpurun_out/ncu_tb.log 2>&1; echo ncu=$?

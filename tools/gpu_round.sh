@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_tblock_gpu.py tests/test_parity_gpu.py -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_tb.log 2>&1; echo pytest_exit=$?
-tail -2 gpurun_out/pytest_tb.log
-timeout 300 python tools/sweep.py --dtype f64 --steps 200 --depths 4 --tblocks 4,5,6 --tbdepths 4 > gpurun_out/sweep64.log 2>&1; echo s64=$?
-timeout 300 python tools/sweep.py --dtype f32 --steps 200 --depths 4 --tblocks 5,6,8 --tbdepths 4 > gpurun_out/sweep32.log 2>&1; echo s32=$?
-grep '"tb"' gpurun_out/sweep64.log gpurun_out/sweep32.log | cut -c1-200
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench=$?
+timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_short.json 2>&1; echo short=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo ncu=$?
