@@ -232,7 +232,16 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               correction), in place, 5 words of HBM traffic per node and level.
                               1: cyclic reduction per line in shared memory with tiled transposes
                               (the paper's solver), ≤ 227 KB/(4·sizeof(T)) unknowns per line. */
+#define TSW_OPT_GUARD_CHECK 10 /* 1: fill the 16 KB guard zones before and after every device array the ctx
+                              holds so far (fields, scratch, faces, coefficients) with 0xFF bytes (NaN in
+                              both precisions, so a stray read shows up in results too); synchronises.
+                              A debugging aid: tsw_check_guards then counts guard bytes that changed. */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
+
+/* Out-of-bounds write check: *bad_bytes = number of guard bytes (TSW_OPT_GUARD_CHECK) that no
+ * longer hold 0xFF — any nonzero count is a kernel writing outside its array; *checked_bytes (may
+ * be NULL) = guard bytes inspected.  Synchronises. */
+tsw_status tsw_check_guards(tsw_ctx* ctx, int64_t* bad_bytes, int64_t* checked_bytes);
 
 /* Live per-kernel timing of the launches TSW_OPT_TIME_KERNELS brackets (stencil S2/S3, or the
  * implicit y solve) since it was set: total device milliseconds, number of launches, and interior

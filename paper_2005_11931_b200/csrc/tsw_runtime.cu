@@ -14,6 +14,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <map>
+#include <mutex>
 
 using namespace tsw;
 
@@ -111,16 +113,34 @@ constexpr int IMP_SCAN_MAX = 8192;  // unknowns per line of the implicit scan so
 // Zeroed on `stream` — never on the legacy default stream: the ctx streams are non-blocking, so a
 // legacy-stream memset would not be ordered before the ctx's own work (with another ctx keeping the
 // GPU busy it could land in the middle of it).
+// Registry of guarded allocations (raw pointer → payload bytes) for the out-of-bounds write
+// check (TSW_OPT_GUARD_CHECK / tsw_check_guards).
+std::mutex& guard_mu() {
+    static std::mutex m;
+    return m;
+}
+std::map<char*, size_t>& guard_reg() {
+    static std::map<char*, size_t> r;
+    return r;
+}
 cudaError_t dmalloc_guarded(void** p, size_t bytes, size_t shift, cudaStream_t stream) {
     void* raw = nullptr;
     cudaError_t e = cudaMalloc(&raw, bytes + 2 * GUARD);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(raw, 0, bytes + 2 * GUARD, stream);
     *p = static_cast<char*>(raw) + GUARD + shift;
+    std::lock_guard<std::mutex> lk(guard_mu());
+    guard_reg()[static_cast<char*>(raw)] = bytes;
     return e;
 }
 void dfree_guarded(void* p, size_t shift = 0) {
-    if (p) cudaFree(static_cast<char*>(p) - GUARD - shift);
+    if (!p) return;
+    char* raw = static_cast<char*>(p) - GUARD - shift;
+    {
+        std::lock_guard<std::mutex> lk(guard_mu());
+        guard_reg().erase(raw);
+    }
+    cudaFree(raw);
 }
 
 }  // namespace
@@ -1996,6 +2016,8 @@ tsw_status tsw_sync(tsw_ctx* c) {
 
 int64_t tsw_launch_count(const tsw_ctx* c) { return c ? c->launches : 0; }
 
+tsw_status guard_fill(tsw_ctx* c);
+
 tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
     if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
     drop_graphs(c);  // captured launches bake in the kernel variant and its shape
@@ -2057,6 +2079,12 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         c->scheme = int(value);
         return TSW_OK;
     }
+    if (key == TSW_OPT_GUARD_CHECK) {
+        if (value != 1) return fail(TSW_ERR_ARG, "guard check: value must be 1");
+        tsw_status st = set_dev(c);
+        if (st) return st;
+        return guard_fill(c);
+    }
     if (key == TSW_OPT_IMPLICIT_SOLVER) {
         if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "implicit solver must be 0 (scans) or 1 (cyclic reduction)");
         if (value == 1 && c->g.dim == 2) {
@@ -2099,6 +2127,58 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     return fail(TSW_ERR_ARG, "unknown option %d", key);
+}
+
+// ---- out-of-bounds write check ----------------------------------------------------------------
+namespace {
+// (raw pointer, payload bytes) of every guarded array the ctx holds
+std::vector<std::pair<char*, size_t>> ctx_guarded(tsw_ctx* c) {
+    std::vector<std::pair<char*, size_t>> out;
+    auto add = [&](void* p, size_t shift) {
+        if (!p) return;
+        char* raw = static_cast<char*>(p) - GUARD - shift;
+        std::lock_guard<std::mutex> lk(guard_mu());
+        auto it = guard_reg().find(raw);
+        if (it != guard_reg().end()) out.emplace_back(raw, it->second);
+    };
+    for (int k = 0; k < 4; ++k) add(c->buf[k], c->fshift);
+    add(c->imp_s1, c->fshift);
+    add(c->h1, c->cshift_h);
+    add(c->h2, c->cshift_h);
+    add(c->c1, c->cshift);
+    add(c->c2, c->cshift);
+    return out;
+}
+}  // namespace
+
+tsw_status guard_fill(tsw_ctx* c) {
+    for (auto& g : ctx_guarded(c)) {
+        CK(cudaMemsetAsync(g.first, 0xFF, GUARD, c->stream));
+        CK(cudaMemsetAsync(g.first + GUARD + g.second, 0xFF, GUARD, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return TSW_OK;
+}
+
+tsw_status tsw_check_guards(tsw_ctx* c, int64_t* bad_bytes, int64_t* checked_bytes) {
+    if (!c || !bad_bytes) return fail(TSW_ERR_ARG, "NULL argument");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<unsigned char> h(GUARD);
+    int64_t bad = 0, checked = 0;
+    for (auto& g : ctx_guarded(c)) {
+        checked += 2 * int64_t(GUARD);
+        for (int side = 0; side < 2; ++side) {
+            CK(cudaMemcpyAsync(h.data(), side ? g.first + GUARD + g.second : g.first, GUARD, cudaMemcpyDeviceToHost,
+                               c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            for (unsigned char v : h) bad += (v != 0xFF);
+        }
+    }
+    *bad_bytes = bad;
+    if (checked_bytes) *checked_bytes = checked;
+    return TSW_OK;
 }
 
 tsw_status tsw_kernel_stats(tsw_ctx* c, double* total_ms, int64_t* launches, int64_t* updates) {

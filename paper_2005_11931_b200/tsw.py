@@ -32,6 +32,7 @@ TSW_OPT_TBLOCK = 6
 TSW_OPT_TB_DEPTH = 7
 TSW_OPT_SCHEME = 8
 TSW_OPT_IMPLICIT_SOLVER = 9
+TSW_OPT_GUARD_CHECK = 10
 
 STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STATE", 4: "TSW_ERR_CUDA",
                 5: "TSW_ERR_NCCL", 6: "TSW_ERR_OOM", 7: "TSW_ERR_UNSTABLE"}
@@ -39,7 +40,7 @@ STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STA
 # every symbol include/tsw.h declares (tests check the library exports all of them)
 EXPORTS = ["tsw_create", "tsw_destroy", "tsw_set_coeff", "tsw_set_coeff_faces", "tsw_set_coeff_profile", "tsw_read_faces", "tsw_set_initial", "tsw_step",
            "tsw_group_step", "tsw_energy", "tsw_wave2", "tsw_read", "tsw_family_l2", "tsw_field_norms", "tsw_coeff_norms", "tsw_set_state", "tsw_info", "tsw_sync",
-           "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
+           "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_check_guards", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
            "tsw_version"]
 
 
@@ -105,6 +106,7 @@ def load(path: Optional[str] = None):
         "tsw_launch_count": (i64, [vp]),
         "tsw_set_option": (i32, [vp, i32, i64]),
         "tsw_kernel_stats": (i32, [vp, ctypes.POINTER(d), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "tsw_check_guards": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "tsw_nccl_unique_id": (i32, [vp]),
         "tsw_nccl_init": (i32, [vp, vp]),
         "tsw_last_error": (ctypes.c_char_p, [vp]),
@@ -303,6 +305,13 @@ def tsw_kernel_stats(ctx) -> Tuple[float, int, int]:
     return ms.value, n.value, u.value
 
 
+def tsw_check_guards(ctx) -> Tuple[int, int]:
+    """(guard bytes changed since TSW_OPT_GUARD_CHECK filled them, guard bytes inspected)."""
+    n, m = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().tsw_check_guards(ctx, ctypes.byref(n), ctypes.byref(m)), ctx)
+    return n.value, m.value
+
+
 def tsw_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load().tsw_nccl_unique_id(buf))
@@ -419,3 +428,6 @@ class Solver:
 
     def kernel_stats(self):
         return tsw_kernel_stats(self.ctx)
+
+    def check_guards(self) -> Tuple[int, int]:
+        return tsw_check_guards(self.ctx)

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench=$?
-timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_short.json 2>&1; echo short=$?
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo ncu=$?
+timeout 600 python -m pytest tests/test_guards_gpu.py -q --timeout 120 -p no:cacheprovider > gpurun_out/pytest_guard.log 2>&1; echo pytest_exit=$?
+tail -15 gpurun_out/pytest_guard.log
