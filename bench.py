@@ -365,6 +365,8 @@ def main():
                     help="config4: the weak-scaling unit (default, the BASELINE metric's scaling "
                          "workload); config5: 65-member eps family x 2048^2; config3: 4096^2 delta line; "
                          "table1: the paper's implicit method on its Table 1 set-up (4096^2, dt 0.05)")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+                    help="ghost rows of the row slabs at N > 1: peer stores fused into the stencil (default) or NCCL")
     ap.add_argument("--tblock", type=int, default=0,
                     help="levels per HBM pass of the temporally blocked stencil (1 = per-step TMA kernel; "
                          "0 = per dtype: 4 for f64, 8 for f32 — the sweep optimum, tools/sweep.py)")
@@ -392,6 +394,8 @@ def main():
         parallel.init_process_group("nccl")
     dev = torch.device("cuda", local)
 
+    halo_used, halo_note = ["nccl"], []
+
     def run(dtype: str, full: bool, tblock: int):
         npdt = np.float64 if dtype == "f64" else np.float32
         stream = torch.cuda.Stream(device=dev)
@@ -400,7 +404,23 @@ def main():
             s.set_option(tsw.TSW_OPT_ROWS_PER_ITEM, args.rows_per_item)
         if tblock > 1:
             s.set_option(tsw.TSW_OPT_TBLOCK, tblock)
-        parallel.nccl_bootstrap(s)
+        parallel.nccl_bootstrap(s)            # the communicator serves the reductions (energy)
+        if world > 1 and args.halo == "peer":
+            # ghost rows by peer stores from the stencil itself (fused halo push over NVLink);
+            # every rank must agree, so a failure anywhere falls back to NCCL halos everywhere
+            ok = True
+            try:
+                parallel.peer_bootstrap(s)
+            except Exception as e:  # noqa: BLE001 — reported in the JSON line
+                ok = False
+                halo_note.append(f"peer halos unavailable on rank {rank}: {e}")
+            flag = torch.tensor([1.0 if ok else 0.0], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if flag.item() < 1.0:
+                s.set_option(tsw.TSW_OPT_HALO, 0)
+                halo_used[0] = "nccl"
+            else:
+                halo_used[0] = "peer"
         r0, r1 = parallel.slab(cfg.ny, rank, world)
         u0_host = torch.from_numpy(inputs.uniform_dense_rows(cfg.nx, cfg.ny, r0, r1 - r0).astype(npdt)).pin_memory()
         # (config 5: every member starts from the same field — TSW_INIT_SHARED)
@@ -475,6 +495,8 @@ def main():
             nbo = out_host.numel() * out_host.element_size()
             res["e2e"] = {"value": updates / el / 1e9, "unit": UNIT, "h2d_bytes_per_step": nb / args.steps,
                           "d2h_bytes_per_step": nbo / args.steps}
+        if world > 1:
+            dist.barrier()   # every rank's streams are done (peer halos write into neighbours' buffers)
         s.close()
         del u0_dev
         torch.cuda.empty_cache()
@@ -512,7 +534,10 @@ def main():
                        "eps": cfg.eps[0] if cfg.batch == 1 else [min(cfg.eps), max(cfg.eps)],
                        "energy_every": args.energy_every,
                        "temporal_blocking": tblock,
-                       "parallelism": f"row-slab x{world} (NCCL ghost rows)" if world > 1 else "single GPU",
+                       "parallelism": (f"row-slab x{world} (" + ("peer-store ghost rows fused into the stencil, NVLink"
+                                                                  if halo_used[0] == "peer" else "NCCL ghost rows") + ")")
+                       if world > 1 else "single GPU",
+                       "halo_notes": halo_note or None,
                        "l2": "inputs exceed L2 (2 levels x %.2f GB per GPU), no flush" %
                              ((cfg.nx * (cfg.ny // world) * esz * cfg.batch) / 1e9)},
             "hbm_gbs_effective": main_res["value"] * words * esz,

@@ -232,11 +232,45 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               correction), in place, 5 words of HBM traffic per node and level.
                               1: cyclic reduction per line in shared memory with tiled transposes
                               (the paper's solver), ≤ 227 KB/(4·sizeof(T)) unknowns per line. */
+#define TSW_OPT_HALO 11     /* ghost rows of 2D slabs.  0 (default): NCCL send/recv (tsw_nccl_init).
+                              1: peer stores — the temporally blocked stencil writes its first / last K
+                              owned rows straight into the neighbours' ghost rows through mapped peer
+                              pointers (NVLink), one-level steps and initial ghosts are pushed by a copy
+                              kernel; ordering by epochs: before halo operation e each rank's stream
+                              runs a one-thread waiter until both neighbours have published e − 1 into
+                              its mailbox (bounded: a ~20 s timeout sets an error word that tsw_read /
+                              tsw_energy report), and afterwards publishes e.  Neighbours are mapped
+                              with tsw_peer_export / tsw_peer_import (processes, CUDA IPC — one GPU per
+                              rank) or tsw_peer_attach (ctxs of one process, stepped together by
+                              tsw_group_step on one shared stream, epoch by epoch, so no waiter ever
+                              spins), after TSW_OPT_TBLOCK and before tsw_set_initial.  tsw_set_initial
+                              / tsw_set_state are one epoch; the ghost rows are pushed by the first
+                              stepping call.  tsw_energy / tsw_field_norms return this slab's share
+                              and are collective: every rank calls them in the same order (after a
+                              step). */
 #define TSW_OPT_GUARD_CHECK 10 /* 1: fill the 16 KB guard zones before and after every device array the ctx
                               holds so far (fields, scratch, faces, coefficients) with 0xFF bytes (NaN in
                               both precisions, so a stray read shows up in results too); synchronises.
                               A debugging aid: tsw_check_guards then counts guard bytes that changed. */
 tsw_status tsw_set_option(tsw_ctx* ctx, int32_t key, int64_t value);
+
+/* Peer halo plumbing (TSW_OPT_HALO = 1).  tsw_peer_export writes an opaque blob
+ * (*len bytes; call with out = NULL to get the size) holding CUDA IPC handles of this ctx's field
+ * buffers and mailbox; the neighbour passes it to tsw_peer_import(ctx, side, …) with side 0 for
+ * rank − 1 and 1 for rank + 1 (the same blob bytes, any transport — e.g. an all-gather).  For ctxs
+ * of one process, tsw_peer_attach(ctx, side, neighbour_ctx) maps directly.  Shapes must agree. */
+tsw_status tsw_peer_export(tsw_ctx* ctx, void* out, size_t cap, size_t* len);
+tsw_status tsw_peer_import(tsw_ctx* ctx, int32_t side, const void* blob, size_t len);
+tsw_status tsw_peer_attach(tsw_ctx* ctx, int32_t side, tsw_ctx* neighbour);
+/* Peer halos, host-driven lock step: issue exactly ONE halo operation (epoch) of the next
+ * min(nsteps, …) levels — the ghost push, one level or one temporally blocked pass — and report
+ * the levels it advanced in *consumed (0 for a ghost push).  Ranks sharing a GPU can then be
+ * stepped operation by operation with a host barrier in between, so no waiter ever spins. */
+tsw_status tsw_step_op(tsw_ctx* ctx, int64_t nsteps, int64_t* consumed);
+
+/* Diagnostics: out4 = {halo epochs issued, mailbox from rank − 1, mailbox from rank + 1, wait
+ * timeout word} (the mailboxes read on a private stream; −1 without peer halos). */
+tsw_status tsw_peer_state(tsw_ctx* ctx, int64_t* out4);
 
 /* Out-of-bounds write check: *bad_bytes = number of guard bytes (TSW_OPT_GUARD_CHECK) that no
  * longer hold 0xFF — any nonzero count is a kernel writing outside its array; *checked_bytes (may

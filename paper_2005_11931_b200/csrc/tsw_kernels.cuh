@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <stdint.h>
+#include <climits>
 
 #include <type_traits>
 
@@ -525,6 +526,15 @@ struct TbArgs {
     int32_t rows_per_item, chunks;
     int64_t strips, items;
     T dtT;
+    // fused halo push (peer mode): output rows ro ≤ push_top are also stored into the
+    // upper neighbour's lower ghost rows, rows ro ≥ push_bot into the lower neighbour's upper ghost
+    // rows, through mapped peer pointers shifted so that the row index is this slab's
+    T* pu_k = nullptr;
+    T* pu_km1 = nullptr;
+    T* pd_k = nullptr;
+    T* pd_km1 = nullptr;
+    int64_t pu_mstride = 0, pd_mstride = 0;
+    int32_t push_top = 0, push_bot = INT32_MAX;
 };
 
 // centre-row buffers are padded by one 16-byte vector on each side (zeros), so the left/right
@@ -626,7 +636,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
 // The producer is thread 0: after every second input row it refills the two stages consumed by
 // the previous rows (every thread has passed the per-row barrier, so they are free) with the next
 // stages of its stream (needs a ring of ≥ 3 stages).
-template <typename T, int K>
+template <typename T, int K, bool PEER = false>
 __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
@@ -772,6 +782,18 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
                 for (int k = 0; k < V; ++k) o2[k] = S.w[K - 1][NS][k];
                 stg_v2(okp, lastk);
                 stg_v2(okm1p, o2);
+                if constexpr (PEER) {
+                    if (ro <= a.push_top) {   // peer stores over NVLink (rare rows)
+                        const int64_t off = int64_t(ro) * a.pitch + gc0;
+                        stg_v2(a.pu_k + b * a.pu_mstride + off, lastk);
+                        stg_v2(a.pu_km1 + b * a.pu_mstride + off, o2);
+                    }
+                    if (ro >= a.push_bot) {
+                        const int64_t off = int64_t(ro) * a.pitch + gc0;
+                        stg_v2(a.pd_k + b * a.pd_mstride + off, lastk);
+                        stg_v2(a.pd_km1 + b * a.pd_mstride + off, o2);
+                    }
+                }
             }
             okp += a.pitch;
             okm1p += a.pitch;
@@ -2471,6 +2493,80 @@ __global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
         }
     }
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// Peer halos (peer mode): ghost rows are written by the producing rank straight
+// into its neighbours' buffers through mapped peer pointers (NVLink), instead of NCCL messages.
+// k_push_rows copies rows that are already computed (start-up level, initial state, remainder
+// levels); the temporally blocked stencil pushes its boundary rows itself (TbArgs::pu_* / pd_*).
+// k_peer_signal publishes "epoch e done" into the neighbours' mailboxes after a fence;
+// k_peer_wait makes the receiving stream wait for its local mailbox.
+// ------------------------------------------------------------------------------------------
+template <typename T>
+struct PushArgs {
+    const T* src;      // this slab's buffer (view: storage row 1 = first owned row)
+    T* pu;             // upper neighbour's buffer, shifted: this slab's row r ↦ its row r + ny_up (or null)
+    T* pd;             // lower neighbour's buffer, shifted: row r ↦ its row r − ny_local (or null)
+    int64_t pitch, mstride, pu_mstride, pd_mstride;
+    int64_t nx, ny_local;
+    int32_t nrows, batch;
+};
+
+template <typename T>
+__global__ void k_push_rows(const PushArgs<T> a) {
+    const int64_t per = int64_t(a.nrows) * a.nx;                 // elements per direction and member
+    const int64_t total = per * 2 * a.batch;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e % a.nx;
+        const int64_t rest = e / a.nx;
+        const int64_t k = rest % a.nrows;
+        const int64_t dirb = rest / a.nrows;
+        const int dir = int(dirb & 1);
+        const int64_t b = dirb >> 1;
+        if (dir == 0) {
+            if (!a.pu) continue;
+            const int64_t r = 1 + k;                                  // first owned rows go up
+            a.pu[b * a.pu_mstride + r * a.pitch + i] = a.src[b * a.mstride + r * a.pitch + i];
+        } else {
+            if (!a.pd) continue;
+            const int64_t r = a.ny_local - a.nrows + 1 + k;           // last owned rows go down
+            a.pd[b * a.pd_mstride + r * a.pitch + i] = a.src[b * a.mstride + r * a.pitch + i];
+        }
+    }
+}
+
+// Wait until the mailbox slots of the existing neighbours reach `target` (acquire), bounded:
+// after ~20 s the error word is set and the kernel returns (the host reports it).  On one GPU the
+// ranks of a process share one stream and are issued epoch by epoch, so the wait is always
+// already satisfied there; across GPUs it is the rank's own stream that waits.
+__global__ void k_peer_wait(const unsigned int* mbox, int has_up, int has_dn, unsigned int target, unsigned int* err) {
+    if (threadIdx.x != 0) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int side = 0; side < 2; ++side) {
+        if (!(side == 0 ? has_up : has_dn)) continue;
+        for (;;) {
+            unsigned int v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mbox + side) : "memory");
+            if (int(v - target) >= 0) break;
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 20000000000ull) {
+                atomicExch(err, 1u);
+                return;
+            }
+            __nanosleep(256);
+        }
+    }
+}
+
+__global__ void k_peer_signal(unsigned int* up_slot, unsigned int* dn_slot, unsigned int epoch) {
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (up_slot) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(up_slot), "r"(epoch) : "memory");
+        if (dn_slot) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dn_slot), "r"(epoch) : "memory");
+    }
 }
 
 // ------------------------------------------------------------------------------------------

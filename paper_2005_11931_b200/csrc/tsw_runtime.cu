@@ -187,6 +187,15 @@ struct tsw_ctx {
     // state
     bool have_init = false;
     bool ghosts_valid = false;  // ghost rows of u^n hold the neighbours' rows
+    // peer halos (TSW_OPT_HALO = 1): neighbours' buffers mapped into this process
+    int halo_mode = 0;                  // 0: NCCL messages, 1: peer stores
+    void* peer_buf[2][4] = {};          // [0] upper neighbour (rank−1), [1] lower (rank+1): its buf[k] views
+    int64_t peer_ny[2] = {0, 0};        // its ny_local
+    int64_t peer_mstride[2] = {0, 0};
+    unsigned int* mbox = nullptr;       // my mailbox: [0] epoch of the upper neighbour, [1] of the lower
+    unsigned int* peer_slot[2] = {};    // where I publish my epoch: upper's mbox[1], lower's mbox[0]
+    unsigned int epoch = 0;             // halo operations issued
+    std::vector<void*> ipc_opened;      // cudaIpcOpenMemHandle mappings (closed on destroy)
     int gdepth[4] = {0, 0, 0, 0};  // ghost rows of each buffer that hold the neighbours' rows
     int64_t n = 0;
     double dt = 0.0;
@@ -595,6 +604,10 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
     return TSW_OK;
 }
 
+// neighbour on side 0 (rank − 1) / 1 (rank + 1); peer halos in use
+bool has_nb(const tsw_ctx* c, int side) { return side == 0 ? c->g.rank > 0 : c->g.rank < c->g.nranks - 1; }
+bool peer_mode(const tsw_ctx* c) { return c->g.nranks > 1 && c->g.dim == 2 && c->halo_mode == 1; }
+
 // ---- temporally blocked pass: K levels, (buf[ic], buf[ip]) → (buf[fk], buf[fkm1]) -----------
 template <typename T, int K>
 tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
@@ -602,11 +615,14 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi)
     using G = TbGeom<T, K>;
     const int depth = c->tb_depth;
     const size_t smem = tb_smem_bytes<T, K>(depth);
+    const bool peer = peer_mode(c);
     int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K];
     if (occ == 0) {
-        CK(cudaFuncSetAttribute(k_step2d_tb<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        CK(cudaFuncSetAttribute(k_step2d_tb<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K>, TB_NC * 32, smem));
+        for (auto fn : {k_step2d_tb<T, K, false>, k_step2d_tb<T, K, true>}) {
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K, false>, TB_NC * 32, smem));
         if (occ < 1) return fail(TSW_ERR_ARG, "temporally blocked stencil (K=%d) does not fit on an SM", K);
     }
     TbArgs<T> a;
@@ -629,6 +645,20 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi)
     a.smax = int32_t(c->ny_local) + ((c->g.rank < c->g.nranks - 1) ? c->G : 0);
     a.strips = (c->pitch + G::WO - 1) / G::WO;
     a.dtT = (T)c->dt;
+    if (peer) {   // fused halo push: the first / last K owned rows also go to the neighbours
+        if (has_nb(c, 0)) {
+            a.pu_k = static_cast<T*>(c->peer_buf[0][fk]) + c->peer_ny[0] * c->pitch;
+            a.pu_km1 = static_cast<T*>(c->peer_buf[0][fkm1]) + c->peer_ny[0] * c->pitch;
+            a.pu_mstride = c->peer_mstride[0];
+            a.push_top = K;
+        }
+        if (has_nb(c, 1)) {
+            a.pd_k = static_cast<T*>(c->peer_buf[1][fk]) - c->ny_local * c->pitch;
+            a.pd_km1 = static_cast<T*>(c->peer_buf[1][fkm1]) - c->ny_local * c->pitch;
+            a.pd_mstride = c->peer_mstride[1];
+            a.push_bot = int32_t(c->ny_local) - K + 1;
+        }
+    }
     const int64_t rows = s_hi - s_lo;
     const int64_t Gw = int64_t(occ) * c->sm_count;
     int R = c->rows_per_item_opt;
@@ -644,7 +674,10 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi)
         if (st) return st;
         CK(cudaEventRecord(e0, c->stream));
     }
-    k_step2d_tb<T, K><<<unsigned(blocks), TB_NC * 32, smem, c->stream>>>(a, depth);
+    if (peer)
+        k_step2d_tb<T, K, true><<<unsigned(blocks), TB_NC * 32, smem, c->stream>>>(a, depth);
+    else
+        k_step2d_tb<T, K, false><<<unsigned(blocks), TB_NC * 32, smem, c->stream>>>(a, depth);
     CKL();
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
@@ -669,6 +702,74 @@ tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1, int32_t s_lo, int32_
 }
 
 tsw_status exchange_nccl(tsw_ctx* c, void* field, cudaStream_t stream, int nrows);
+
+// ---- peer halos --------------------------------------------------------------------------------
+// Epochs: every halo operation (a pass, a level, an initial exchange, a ghost-reading diagnostic) is
+// issued by every rank in the same order and numbered e = 1, 2, … .  Before operation e a rank's
+// stream waits until each neighbour has published e − 1 (its writes into my ghost rows are done and
+// it no longer reads the ghost rows I am about to overwrite); afterwards it publishes e.
+bool peers_ready(const tsw_ctx* c) {
+    if (!c->mbox) return false;
+    for (int side = 0; side < 2; ++side)
+        if (has_nb(c, side) && (!c->peer_buf[side][0] || !c->peer_buf[side][1] || !c->peer_slot[side])) return false;
+    return true;
+}
+
+
+tsw_status peer_begin(tsw_ctx* c, cudaStream_t s) {
+    if (!peers_ready(c)) return fail(TSW_ERR_STATE, "peer halos: neighbours not attached (tsw_peer_import / tsw_peer_attach)");
+    ++c->epoch;
+    // mailbox layout: [0] from rank − 1, [1] from rank + 1, [2] wait-timeout error word
+    k_peer_wait<<<1, 32, 0, s>>>(c->mbox, has_nb(c, 0) ? 1 : 0, has_nb(c, 1) ? 1 : 0, c->epoch - 1, c->mbox + 2);
+    CKL();
+    c->launches++;
+    return TSW_OK;
+}
+
+tsw_status peer_end(tsw_ctx* c, cudaStream_t s) {
+    k_peer_signal<<<1, 32, 0, s>>>(has_nb(c, 0) ? c->peer_slot[0] : nullptr, has_nb(c, 1) ? c->peer_slot[1] : nullptr,
+                                   c->epoch);
+    CKL();
+    c->launches++;
+    return TSW_OK;
+}
+
+// Copy nrows boundary rows of buffer bi into the neighbours' ghost rows (peer stores).
+template <typename T>
+tsw_status push_rows_t(tsw_ctx* c, int bi, int nrows, cudaStream_t s) {
+    PushArgs<T> a;
+    a.src = static_cast<const T*>(c->buf[bi]);
+    a.pu = has_nb(c, 0) ? static_cast<T*>(c->peer_buf[0][bi]) + c->peer_ny[0] * c->pitch : nullptr;
+    a.pd = has_nb(c, 1) ? static_cast<T*>(c->peer_buf[1][bi]) - c->ny_local * c->pitch : nullptr;
+    if ((has_nb(c, 0) && !c->peer_buf[0][bi]) || (has_nb(c, 1) && !c->peer_buf[1][bi]))
+        return fail(TSW_ERR_STATE, "peer halos: the neighbour has no buffer %d", bi);
+    a.pitch = c->pitch;
+    a.mstride = c->mstride;
+    a.pu_mstride = c->peer_mstride[0];
+    a.pd_mstride = c->peer_mstride[1];
+    a.nx = c->g.nx;
+    a.ny_local = c->ny_local;
+    a.nrows = nrows;
+    a.batch = c->g.batch;
+    const int64_t total = int64_t(nrows) * c->g.nx * 2 * c->g.batch;
+    k_push_rows<T><<<unsigned(grid_for(total, 256, 2 * c->sm_count)), 256, 0, s>>>(a);
+    CKL();
+    c->launches++;
+    return TSW_OK;
+}
+// The waiter's timeout word (mailbox slot 2); call after the ctx stream has been synchronised.
+tsw_status peer_check(tsw_ctx* c) {
+    if (!peer_mode(c) || !c->mbox) return TSW_OK;
+    unsigned int e = 0;
+    CK(cudaMemcpyAsync(&e, c->mbox + 2, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (e) return fail(TSW_ERR_STATE, "peer halos: a wait for a neighbour timed out (epochs out of step)");
+    return TSW_OK;
+}
+
+tsw_status push_rows(tsw_ctx* c, int bi, int nrows, cudaStream_t s) {
+    return is_f64(c) ? push_rows_t<double>(c, bi, nrows, s) : push_rows_t<float>(c, bi, nrows, s);
+}
 
 void free_pair(const tsw_ctx* c, int* fk, int* fkm1) {
     int ids[2], nf = 0;
@@ -718,6 +819,12 @@ tsw_status tb_pass(tsw_ctx* c) {
     tsw_status st;
     if (c->g.nranks == 1) {
         if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
+    } else if (peer_mode(c)) {
+        // one launch; the kernel itself stores the boundary rows into the neighbours' ghost rows
+        if ((st = peer_begin(c, c->stream))) return st;
+        if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
+        if ((st = peer_end(c, c->stream))) return st;
+        c->gdepth[fk] = c->gdepth[fkm1] = K;
     } else {
         const TbSplit p = tb_split(c);
         if (p.split) {
@@ -996,9 +1103,13 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     drop_graphs(c);  // captured launches bake in dt
     c->ic = 0;
     c->ip = 1;
+    tsw_status st;
+    // peer halos: the buffers are re-initialised inside an epoch of their own, so no neighbour
+    // pushes into them meanwhile; the ghost push below waits for the neighbours' initialisation
+    if (peer_mode(c) && (st = peer_begin(c, c->stream))) return st;
     for (int k = 0; k < 4; ++k)
         if (c->buf[k]) CK(cudaMemsetAsync(static_cast<char*>(c->buf[k]) - c->fshift, 0, bytes, c->stream));
-    tsw_status st = load_field(c, c->buf[0], a, shared, on_device);
+    st = load_field(c, c->buf[0], a, shared, on_device);
     if (st) return st;
     if (b) {
         st = load_field(c, c->buf[1], b, shared, on_device);
@@ -1010,7 +1121,11 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     if ((st = prescale_all(c))) return st;
     c->ghosts_valid = false;
     for (int& d : c->gdepth) d = 0;
-    if (c->g.dim == 2 && c->g.nranks > 1 && c->comm) {
+    if (peer_mode(c)) {
+        // this slab's buffers are initialised; the neighbours' rows are pushed by the first
+        // operation that reads ghost rows (one epoch per call: see tsw_group_step)
+        if ((st = peer_end(c, c->stream))) return st;
+    } else if (c->g.dim == 2 && c->g.nranks > 1 && c->comm) {
         // ghost rows of both levels (the energy of (u^n, u^{n−1}) reads both; loopback groups
         // exchange in tsw_group_step instead)
         if ((st = exchange_nccl(c, c->buf[0], c->stream, c->G))) return st;
@@ -1077,9 +1192,36 @@ tsw_status step_slab_overlapped(tsw_ctx* c) {
     return TSW_OK;
 }
 
+// One slab level, peer mode: boundary rows, their push into the neighbours' ghost rows, then the
+// interior (the interior rows read no ghost rows, so the epoch is published before them).
+tsw_status step_slab_peer(tsw_ctx* c) {
+    const bool start = (c->n == 0);
+    tsw_status st;
+    if ((st = peer_begin(c, c->stream))) return st;
+    if ((st = launch_boundary_rows(c, start))) return st;
+    if ((st = push_rows(c, c->ip, 1, c->stream))) return st;
+    if ((st = peer_end(c, c->stream))) return st;
+    if ((st = launch_interior_rows(c, start))) return st;
+    std::swap(c->ic, c->ip);
+    c->gdepth[c->ic] = 1;
+    c->n++;
+    return TSW_OK;
+}
+
 // Make the K outermost ghost rows of both current levels valid before temporally blocked passes.
 tsw_status ensure_ghosts_nccl(tsw_ctx* c, int K) {
     tsw_status st;
+    if (peer_mode(c)) {
+        const bool need = c->gdepth[c->ic] < K || c->gdepth[c->ip] < K;  // identical on every rank
+        if (!need) return TSW_OK;
+        if ((st = peer_begin(c, c->stream))) return st;
+        for (int which : {c->ic, c->ip})
+            if (c->gdepth[which] < K) {
+                if ((st = push_rows(c, which, K, c->stream))) return st;
+                c->gdepth[which] = K;
+            }
+        return peer_end(c, c->stream);
+    }
     for (int which : {c->ic, c->ip})
         if (c->gdepth[which] < K) {
             if ((st = exchange_nccl(c, c->buf[which], c->stream, K))) return st;
@@ -1088,7 +1230,40 @@ tsw_status ensure_ghosts_nccl(tsw_ctx* c, int K) {
     return TSW_OK;
 }
 
+bool tb_usable(const tsw_ctx* c);
+
+// Peer halos: the halo operations of a stepping call, one epoch each.  The next operation follows
+// from the ctx state alone, so every rank of a group issues the same sequence.
+enum PeerOp { PEER_NONE = 0, PEER_ENSURE_1, PEER_ENSURE_K, PEER_LEVEL, PEER_PASS };
+PeerOp next_peer_op(const tsw_ctx* c, int64_t remaining) {
+    if (remaining <= 0) return PEER_NONE;
+    const int K = c->tblock;
+    const bool pass = tb_usable(c) && c->n > 0 && remaining >= K;
+    if (pass) {
+        if (c->gdepth[c->ic] < K || c->gdepth[c->ip] < K) return PEER_ENSURE_K;
+        return PEER_PASS;
+    }
+    if (c->gdepth[c->ic] < 1) return PEER_ENSURE_1;
+    return PEER_LEVEL;
+}
+tsw_status ensure_ghosts_nccl(tsw_ctx* c, int K);
+tsw_status step_slab_peer(tsw_ctx* c);
+tsw_status tb_pass(tsw_ctx* c);
+tsw_status run_peer_op(tsw_ctx* c, PeerOp op, int64_t* consumed) {
+    *consumed = 0;
+    switch (op) {
+        case PEER_ENSURE_1: return ensure_ghosts_nccl(c, 1);
+        case PEER_ENSURE_K: return ensure_ghosts_nccl(c, c->tblock);
+        case PEER_LEVEL: *consumed = 1; return step_slab_peer(c);
+        case PEER_PASS: *consumed = c->tblock; return tb_pass(c);
+        default: return TSW_OK;
+    }
+}
+
 bool tb_usable(const tsw_ctx* c) {
+    if (peer_mode(c))
+        for (int side = 0; side < 2; ++side)
+            if (has_nb(c, side) && (!c->peer_buf[side][2] || !c->peer_buf[side][3])) return false;
     return c->tblock > 1 && c->g.dim == 2 && c->mode == MODE_LINE && c->buf[2] && c->buf[3] &&
            c->tblock <= c->G + (c->g.nranks == 1 ? 1 << 20 : 0);
 }
@@ -1139,6 +1314,15 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
     }
     if (c->g.dim == 1) return is_f64(c) ? step1d_t<double>(c, k) : step1d_t<float>(c, k);
     tsw_status st;
+    if (c->g.nranks > 1 && peer_mode(c)) {
+        for (int64_t s = 0;;) {
+            const PeerOp op = next_peer_op(c, k - s);
+            if (op == PEER_NONE) return TSW_OK;
+            int64_t used = 0;
+            if ((st = run_peer_op(c, op, &used))) return st;
+            s += used;
+        }
+    }
     if (c->g.nranks > 1) {
         int64_t s = 0;
         if (c->n == 0) {
@@ -1283,6 +1467,8 @@ void tsw_destroy(tsw_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (c->mbox) cudaFree(c->mbox);
     for (int k = 0; k < 4; ++k) dfree_guarded(c->buf[k], c->fshift);
     dfree_guarded(c->imp_s1, c->fshift);
     if (c->imp_t) cudaFree(c->imp_t);
@@ -1554,11 +1740,22 @@ tsw_status tsw_step(tsw_ctx* c, int64_t nsteps) {
     if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
     if (nsteps < 0) return fail(TSW_ERR_ARG, "nsteps must be >= 0");
     if (!c->have_init) return fail(TSW_ERR_STATE, "tsw_set_initial / tsw_set_state first");
-    if (c->g.nranks > 1 && !c->comm)
-        return fail(TSW_ERR_STATE, "nranks > 1: call tsw_nccl_init (or step the slabs with tsw_group_step)");
+    if (c->g.nranks > 1 && c->g.dim == 2 && !c->comm && !peer_mode(c))
+        return fail(TSW_ERR_STATE, "nranks > 1: call tsw_nccl_init, enable peer halos, or step the slabs with tsw_group_step");
     tsw_status st = set_dev(c);
     if (st) return st;
     return do_steps(c, nsteps);
+}
+
+tsw_status tsw_step_op(tsw_ctx* c, int64_t nsteps, int64_t* consumed) {
+    if (!c || !consumed) return fail(TSW_ERR_ARG, "NULL argument");
+    *consumed = 0;
+    if (!c->have_init) return fail(TSW_ERR_STATE, "tsw_set_initial / tsw_set_state first");
+    if (!peer_mode(c)) return fail(TSW_ERR_STATE, "tsw_step_op drives peer halos (TSW_OPT_HALO = 1) only");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    const PeerOp op = next_peer_op(c, nsteps);
+    return run_peer_op(c, op, consumed);
 }
 
 tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
@@ -1577,6 +1774,18 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
     tsw_ctx* c0 = cs[0];
     tsw_status st = set_dev(c0);
     if (st) return st;
+    if (peer_mode(c0)) {
+        // peer halos: the members' halo operations are issued epoch by epoch on the shared stream
+        // (every rank's operation e before any rank's e + 1), so each wait is satisfied on arrival
+        for (int64_t s = 0;;) {
+            const PeerOp op = next_peer_op(c0, nsteps - s);
+            if (op == PEER_NONE) return TSW_OK;
+            int64_t used = 0;
+            for (int r = 0; r < n; ++r)
+                if ((st = run_peer_op(cs[r], op, &used))) return st;
+            s += used;
+        }
+    }
     bool need = false;
     for (int r = 0; r < n; ++r) need = need || !cs[r]->ghosts_valid;
     if (need) {
@@ -1667,6 +1876,9 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     if (!c->have_init || c->n < 1) return fail(TSW_ERR_STATE, "energy E^{n-1/2} needs n >= 1");
     tsw_status st = set_dev(c);
     if (st) return st;
+    // peer halos: a ghost-reading collective is an epoch of its own (no neighbour overwrites the
+    // ghost rows while they are read)
+    if (peer_mode(c) && (st = peer_begin(c, c->stream))) return st;
     int nparts = 0;
     if (c->g.dim == 2) {
         Energy2Args a;
@@ -1729,7 +1941,9 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     k_energy_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_partial, nparts, w, c->d_out);
     CKL();
     c->launches += 2;
-    if (c->g.nranks > 1 && c->comm)  // without a communicator (loopback group): this slab's share
+    if (peer_mode(c) && (st = peer_end(c, c->stream))) return st;
+    if (peer_mode(c) && (st = peer_check(c))) return st;
+    if (c->g.nranks > 1 && c->comm)  // without a communicator (loopback / peer group): this slab's share
         NK(nccl().AllReduce(c->d_out, c->d_out, size_t(c->g.batch), NCCL_F64, NCCL_SUM, c->comm, c->stream));
     CK(cudaMemcpyAsync(out_B, c->d_out, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1891,6 +2105,7 @@ tsw_status tsw_field_norms(tsw_ctx* c, double* out_B4) {
     if (!c->have_init) return fail(TSW_ERR_STATE, "no field");
     tsw_status st = set_dev(c);
     if (st) return st;
+    if (peer_mode(c) && (st = peer_begin(c, c->stream))) return st;   // reads ghost rows (see tsw_energy)
     NormArgs a;
     a.dim = c->g.dim;
     a.un = c->buf[c->ic];
@@ -1912,6 +2127,7 @@ tsw_status tsw_field_norms(tsw_ctx* c, double* out_B4) {
     k_norms_final<<<c->g.batch, 32, 0, c->stream>>>(c->d_partial, a.nblk, c->g.batch, d4);
     CKL();
     c->launches += 2;
+    if (peer_mode(c) && (st = peer_end(c, c->stream))) return st;
     if (c->g.nranks > 1 && c->comm) NK(nccl().AllReduce(d4, d4, size_t(4) * c->g.batch, NCCL_F64, NCCL_SUM, c->comm, c->stream));
     CK(cudaMemcpyAsync(out_B4, d4, sizeof(double) * 4 * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1991,7 +2207,10 @@ tsw_status tsw_read(tsw_ctx* c, int32_t which, void* dst, int32_t to_device) {
         char* d = static_cast<char*>(dst) + size_t(b) * rows * w;
         CK(cudaMemcpy2DAsync(d, w, s, size_t(c->pitch) * c->esz, w, rows, kind, c->stream));
     }
-    if (!to_device) CK(cudaStreamSynchronize(c->stream));
+    if (!to_device) {
+        CK(cudaStreamSynchronize(c->stream));
+        if ((st = peer_check(c))) return st;
+    }
     return TSW_OK;
 }
 
@@ -2079,6 +2298,21 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         c->scheme = int(value);
         return TSW_OK;
     }
+    if (key == TSW_OPT_HALO) {
+        if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "halo mode must be 0 (NCCL) or 1 (peer)");
+        if (value == 1) {
+            if (c->g.dim != 2) return fail(TSW_ERR_ARG, "peer halos are for 2D slabs");
+            tsw_status st = set_dev(c);
+            if (st) return st;
+            if (!c->mbox) {
+                CK(cudaMalloc(reinterpret_cast<void**>(&c->mbox), 256));
+                CK(cudaMemsetAsync(c->mbox, 0, 256, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+            }
+        }
+        c->halo_mode = int(value);
+        return TSW_OK;
+    }
     if (key == TSW_OPT_GUARD_CHECK) {
         if (value != 1) return fail(TSW_ERR_ARG, "guard check: value must be 1");
         tsw_status st = set_dev(c);
@@ -2127,6 +2361,114 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     return fail(TSW_ERR_ARG, "unknown option %d", key);
+}
+
+// ---- peer halo plumbing -------------------------------------------------------------------------
+namespace {
+struct PeerBlob {
+    uint32_t magic;
+    int32_t nbuf;   // bit k: buffer k exported
+    int64_t ny_local, fshift, mstride, pitch, esz, batch, nx;
+    cudaIpcMemHandle_t buf[4];
+    cudaIpcMemHandle_t mbox;
+};
+constexpr uint32_t PEER_MAGIC = 0x74737770u;  // "tswp"
+
+void set_peer(tsw_ctx* c, int side, void* const bufs[4], int64_t ny, int64_t mstride, unsigned int* mbox) {
+    for (int k = 0; k < 4; ++k) c->peer_buf[side][k] = bufs[k];
+    c->peer_ny[side] = ny;
+    c->peer_mstride[side] = mstride;
+    // the upper neighbour hears from me (its lower neighbour) in slot 1, the lower one in slot 0
+    c->peer_slot[side] = mbox + (side == 0 ? 1 : 0);
+}
+}  // namespace
+
+tsw_status tsw_peer_export(tsw_ctx* c, void* out, size_t cap, size_t* len) {
+    if (!c || !len) return fail(TSW_ERR_ARG, "NULL argument");
+    *len = sizeof(PeerBlob);
+    if (!out) return TSW_OK;
+    if (cap < sizeof(PeerBlob)) return fail(TSW_ERR_ARG, "buffer too small (%zu bytes needed)", sizeof(PeerBlob));
+    if (!c->mbox) return fail(TSW_ERR_STATE, "enable peer halos (TSW_OPT_HALO = 1) first");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    PeerBlob b;
+    memset(&b, 0, sizeof(b));
+    b.magic = PEER_MAGIC;
+    b.ny_local = c->ny_local;
+    b.fshift = int64_t(c->fshift);
+    b.mstride = c->mstride;
+    b.pitch = c->pitch;
+    b.esz = c->esz;
+    b.batch = c->g.batch;
+    b.nx = c->g.nx;
+    for (int k = 0; k < 4; ++k)
+        if (c->buf[k]) {
+            CK(cudaIpcGetMemHandle(&b.buf[k], static_cast<char*>(c->buf[k]) - GUARD - c->fshift));
+            b.nbuf |= 1 << k;
+        }
+    CK(cudaIpcGetMemHandle(&b.mbox, c->mbox));
+    memcpy(out, &b, sizeof(b));
+    return TSW_OK;
+}
+
+tsw_status tsw_peer_import(tsw_ctx* c, int32_t side, const void* blob, size_t len) {
+    if (!c || !blob) return fail(TSW_ERR_ARG, "NULL argument");
+    if (side != 0 && side != 1) return fail(TSW_ERR_ARG, "side must be 0 (rank−1) or 1 (rank+1)");
+    if (len < sizeof(PeerBlob)) return fail(TSW_ERR_ARG, "peer blob too short");
+    if (!has_nb(c, side)) return fail(TSW_ERR_ARG, "no neighbour on that side");
+    PeerBlob b;
+    memcpy(&b, blob, sizeof(b));
+    if (b.magic != PEER_MAGIC) return fail(TSW_ERR_ARG, "not a peer blob");
+    if (b.pitch != c->pitch || b.esz != int64_t(c->esz) || b.batch != c->g.batch || b.nx != c->g.nx)
+        return fail(TSW_ERR_ARG, "peer blob from a ctx of another shape");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    void* bufs[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int k = 0; k < 4; ++k)
+        if (b.nbuf & (1 << k)) {
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, b.buf[k], cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(p);
+            bufs[k] = static_cast<char*>(p) + GUARD + b.fshift;
+        }
+    void* pm = nullptr;
+    CK(cudaIpcOpenMemHandle(&pm, b.mbox, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(pm);
+    set_peer(c, side, bufs, b.ny_local, b.mstride, static_cast<unsigned int*>(pm));
+    return TSW_OK;
+}
+
+tsw_status tsw_peer_state(tsw_ctx* c, int64_t* out3) {
+    if (!c || !out3) return fail(TSW_ERR_ARG, "NULL argument");
+    out3[0] = c->epoch;
+    out3[1] = out3[2] = out3[3] = -1;
+    if (!c->mbox) return TSW_OK;
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    cudaStream_t s;   // a private stream: the ctx stream may be waiting on a neighbour
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    unsigned int h[3] = {0, 0, 0};
+    cudaError_t e = cudaMemcpyAsync(h, c->mbox, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return fail(TSW_ERR_CUDA, "mailbox read: %s", cudaGetErrorString(e));
+    out3[1] = h[0];
+    out3[2] = h[1];
+    out3[3] = h[2];
+    return TSW_OK;
+}
+
+tsw_status tsw_peer_attach(tsw_ctx* c, int32_t side, tsw_ctx* other) {
+    if (!c || !other) return fail(TSW_ERR_ARG, "NULL argument");
+    if (side != 0 && side != 1) return fail(TSW_ERR_ARG, "side must be 0 (rank−1) or 1 (rank+1)");
+    if (!has_nb(c, side)) return fail(TSW_ERR_ARG, "no neighbour on that side");
+    if (!other->mbox) return fail(TSW_ERR_STATE, "enable peer halos (TSW_OPT_HALO = 1) on the neighbour first");
+    if (other->pitch != c->pitch || other->esz != c->esz || other->g.batch != c->g.batch || other->g.nx != c->g.nx)
+        return fail(TSW_ERR_ARG, "neighbour ctx of another shape");
+    void* bufs[4];
+    for (int k = 0; k < 4; ++k) bufs[k] = other->buf[k];
+    set_peer(c, side, bufs, other->ny_local, other->mstride, other->mbox);
+    return TSW_OK;
 }
 
 // ---- out-of-bounds write check ----------------------------------------------------------------

@@ -46,3 +46,29 @@ def nccl_bootstrap(solver: "tsw.Solver") -> None:
     obj = [tsw.tsw_nccl_unique_id() if solver.rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     tsw.tsw_nccl_init(solver.ctx, obj[0])
+
+
+def peer_bootstrap(solver: "tsw.Solver") -> None:
+    """Peer halos (TSW_OPT_HALO = 1): every rank exports IPC handles of its buffers, an all-gather
+    distributes them, each rank maps its neighbours (rank ± 1).  Call after TSW_OPT_TBLOCK and
+    before set_initial; no NCCL communicator is needed for the halos."""
+    import torch.distributed as dist
+    if solver.nranks <= 1:
+        return
+    solver.set_option(tsw.TSW_OPT_HALO, 1)
+    blobs = [None] * solver.nranks
+    dist.all_gather_object(blobs, solver.peer_export())
+    neighbours = peer_neighbours(solver.rank, solver.nranks)
+    for side, r in neighbours:
+        solver.peer_import(side, blobs[r])
+    dist.barrier()
+
+
+def peer_neighbours(rank: int, nranks: int):
+    """(side, rank) of the slab neighbours: side 0 = rank − 1 (above), side 1 = rank + 1 (below)."""
+    out = []
+    if rank > 0:
+        out.append((0, rank - 1))
+    if rank < nranks - 1:
+        out.append((1, rank + 1))
+    return out

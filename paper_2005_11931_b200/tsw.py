@@ -33,6 +33,7 @@ TSW_OPT_TB_DEPTH = 7
 TSW_OPT_SCHEME = 8
 TSW_OPT_IMPLICIT_SOLVER = 9
 TSW_OPT_GUARD_CHECK = 10
+TSW_OPT_HALO = 11
 
 STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STATE", 4: "TSW_ERR_CUDA",
                 5: "TSW_ERR_NCCL", 6: "TSW_ERR_OOM", 7: "TSW_ERR_UNSTABLE"}
@@ -40,7 +41,7 @@ STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STA
 # every symbol include/tsw.h declares (tests check the library exports all of them)
 EXPORTS = ["tsw_create", "tsw_destroy", "tsw_set_coeff", "tsw_set_coeff_faces", "tsw_set_coeff_profile", "tsw_read_faces", "tsw_set_initial", "tsw_step",
            "tsw_group_step", "tsw_energy", "tsw_wave2", "tsw_read", "tsw_family_l2", "tsw_field_norms", "tsw_coeff_norms", "tsw_set_state", "tsw_info", "tsw_sync",
-           "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_check_guards", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
+           "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_check_guards", "tsw_peer_export", "tsw_peer_import", "tsw_peer_attach", "tsw_peer_state", "tsw_step_op", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
            "tsw_version"]
 
 
@@ -109,6 +110,11 @@ def load(path: Optional[str] = None):
         "tsw_check_guards": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "tsw_nccl_unique_id": (i32, [vp]),
         "tsw_nccl_init": (i32, [vp, vp]),
+        "tsw_peer_export": (i32, [vp, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+        "tsw_peer_import": (i32, [vp, i32, vp, ctypes.c_size_t]),
+        "tsw_peer_attach": (i32, [vp, i32, vp]),
+        "tsw_peer_state": (i32, [vp, ctypes.POINTER(i64)]),
+        "tsw_step_op": (i32, [vp, i64, ctypes.POINTER(i64)]),
         "tsw_last_error": (ctypes.c_char_p, [vp]),
         "tsw_version": (ctypes.c_char_p, []),
     }
@@ -323,6 +329,40 @@ def tsw_nccl_init(ctx, uid: bytes) -> None:
     _check(load().tsw_nccl_init(ctx, buf), ctx)
 
 
+def tsw_peer_export(ctx) -> bytes:
+    """Opaque blob with CUDA IPC handles of this ctx's field buffers and halo mailbox."""
+    n = ctypes.c_size_t()
+    _check(load().tsw_peer_export(ctx, None, 0, ctypes.byref(n)), ctx)
+    buf = ctypes.create_string_buffer(n.value)
+    _check(load().tsw_peer_export(ctx, buf, n.value, ctypes.byref(n)), ctx)
+    return buf.raw[:n.value]
+
+
+def tsw_peer_import(ctx, side: int, blob: bytes) -> None:
+    """Map the neighbour on `side` (0: rank − 1, 1: rank + 1) from its tsw_peer_export blob."""
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(load().tsw_peer_import(ctx, side, buf, len(blob)), ctx)
+
+
+def tsw_peer_state(ctx) -> Tuple[int, int, int, int]:
+    """(halo epochs issued, mailbox from rank − 1, mailbox from rank + 1, wait-timeout word)."""
+    out = (ctypes.c_int64 * 4)()
+    _check(load().tsw_peer_state(ctx, out), ctx)
+    return out[0], out[1], out[2], out[3]
+
+
+def tsw_step_op(ctx, nsteps: int) -> int:
+    """One peer-halo operation of the next `nsteps` levels; returns the levels it advanced."""
+    n = ctypes.c_int64()
+    _check(load().tsw_step_op(ctx, nsteps, ctypes.byref(n)), ctx)
+    return n.value
+
+
+def tsw_peer_attach(ctx, side: int, neighbour_ctx) -> None:
+    """Map a neighbour ctx of this process directly."""
+    _check(load().tsw_peer_attach(ctx, side, neighbour_ctx), ctx)
+
+
 # ---- convenience wrapper ------------------------------------------------------------------
 
 class Solver:
@@ -431,3 +471,12 @@ class Solver:
 
     def check_guards(self) -> Tuple[int, int]:
         return tsw_check_guards(self.ctx)
+
+    def peer_export(self) -> bytes:
+        return tsw_peer_export(self.ctx)
+
+    def peer_import(self, side: int, blob: bytes) -> None:
+        tsw_peer_import(self.ctx, side, blob)
+
+    def peer_attach(self, side: int, neighbour: "Solver") -> None:
+        tsw_peer_attach(self.ctx, side, neighbour.ctx)
