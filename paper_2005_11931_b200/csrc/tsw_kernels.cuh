@@ -544,18 +544,32 @@ struct TbPad {
     static constexpr int P = 16 / sizeof(T);
 };
 
+// Caching the upper y-flux for the next row saves 2 fp ops per update (identical operands, so the
+// tree is unchanged bit for bit).  fp32 keeps it in registers (2V per level); fp64 has no spare
+// registers and keeps it in shared memory (one 16-byte load + store per level and thread, each
+// thread touching only its own slots — no barrier).
+// fp64 y-flux cache in shared memory: measured 15 % slower on B200 (K = 4: 569 vs 657 Gpt/s,
+// interleaved A/B on one box) — the load sits in the dependency chain — so it is off by default
+#ifndef TSW_TB_YCACHE_SMEM
+#define TSW_TB_YCACHE_SMEM 0
+#endif
+template <typename T> struct TbYCache {
+    static constexpr bool on = sizeof(T) == 4;                             // registers
+    static constexpr bool smem = sizeof(T) == 8 && TSW_TB_YCACHE_SMEM;     // shared memory
+};
+
 template <typename T, int K>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
     return size_t(depth) * 2 * TbGeom<T, K>::WE * sizeof(T) +
-           size_t(K) * 2 * (TbGeom<T, K>::WE + 2 * TbPad<T>::P) * sizeof(T) + size_t(depth) * sizeof(uint64_t);
+           size_t(K) * 2 * (TbGeom<T, K>::WE + 2 * TbPad<T>::P) * sizeof(T) +
+           (size_t(depth) * sizeof(uint64_t) + 15) / 16 * 16 +
+           (TbYCache<T>::smem ? size_t(K + 1) * TbGeom<T, K>::NT * TbGeom<T, K>::V * sizeof(T) : 0);
 }
 
 // Per-thread state of one item's wavefront.  Window slots rotate with the row phase PH ∈ {0,1,2}:
 // before row i (phase PH = i mod 3) level m holds rows (r−1, r, r+1) in slots (PH, PH+1, PH+2) mod 3;
 // its new row overwrites slot PH, so no register moves are needed.
-// caching the upper y-flux for the next row saves 2 ops per update but costs 2V registers per
-// level: on for fp32 (spare registers), off for fp64 (it would spill at K = 5)
-template <typename T> struct TbYCache { static constexpr bool on = sizeof(T) == 4; };
+
 
 template <typename T, int K>
 struct TbState {
@@ -573,7 +587,8 @@ struct TbState {
 // rows/columns to +0 (only items whose dependency cone touches them need it).
 template <typename T, int K, int PH, bool MASKED>
 __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
-                                       int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2]) {
+                                       int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
+                                       T* __restrict__ yc) {
     constexpr int V = 2;
     constexpr int WEP = TbGeom<T, K>::WE + 2 * TbPad<T>::P;
     constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
@@ -598,14 +613,19 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
         T nv[V];
         bool rowok = true;
         if (MASKED) rowok = unsigned(R - m - rowlo) <= unsigned(rowhi - rowlo);
+        T gdv[V], guv[V];
+        if (TbYCache<T>::smem) lds_v2(yc + m * TbGeom<T, K>::NT * V, gdv);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const T cu = S.w[m - 1][N][k];
             const T gu = r_mul(S.c2v[k], r_sub(S.w[m - 1][O][k], cu));
+            guv[k] = gu;
             T gd;
             if (TbYCache<T>::on) {
                 gd = S.gup[m][k];
                 S.gup[m][k] = gu;
+            } else if (TbYCache<T>::smem) {
+                gd = gdv[k];
             } else {
                 gd = r_mul(S.c2v[k], r_sub(cu, S.w[m - 1][C][k]));
             }
@@ -620,6 +640,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
                 nv[k] = v;
             }
         }
+        if (TbYCache<T>::smem) sts_v2(yc + m * TbGeom<T, K>::NT * V, guv);
         if (m < K) {
 #pragma unroll
             for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
@@ -647,6 +668,10 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
     uint64_t* full = reinterpret_cast<uint64_t*>(cenp + size_t(K) * 2 * WEP);
     T* cen = cenp + PAD;
     const int tid = threadIdx.x;
+    // y-flux cache (fp64): [K+1][NT][V] after the mbarriers (16-byte aligned: depth is even or the
+    // barrier block is padded below)
+    T* ycache = reinterpret_cast<T*>(reinterpret_cast<char*>(full) + ((size_t(depth) * sizeof(uint64_t) + 15) / 16) * 16) +
+                tid * V;
     for (int e = tid; e < K * 2 * WEP; e += blockDim.x) cenp[e] = (T)0;  // pads stay 0
     if (tid == 0) {
         for (int k = 0; k < depth; ++k) mbar_init(&full[k], 1);
@@ -736,6 +761,11 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
             for (int m = 0; m <= (TbYCache<T>::on ? K : 0); ++m)
 #pragma unroll
                 for (int k = 0; k < V; ++k) S.gup[m][k] = (T)0;
+        if (TbYCache<T>::smem) {
+            const T z2[V] = {(T)0, (T)0};
+#pragma unroll
+            for (int m = 0; m <= K; ++m) sts_v2(ycache + m * G::NT * V, z2);
+        }
         const int nload = in_hi - in_lo;
         const int L = s1 + K - in_lo;
 
@@ -772,7 +802,7 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
             const int par = R & 1;
             T* cw = cen + par * WEP + e0;
             const T* cr = cen + (par ^ 1) * WEP + e0;
-            tb_row<T, K, PH, MASKED>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk);
+            tb_row<T, K, PH, MASKED>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
                 // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH

@@ -79,7 +79,7 @@ def load(path: Optional[str] = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("TSW_LIB") or LIB_PATH   # TSW_LIB: an alternative build (A/B timing)
     if not os.path.exists(path):
         raise RuntimeError(f"{path} is missing: build it with `python paper_2005_11931_b200/build.py` "
                            "(there is no CPU fallback)")
