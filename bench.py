@@ -52,12 +52,12 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(dtype: str, workload: str, tblock: int = 1):
-    """dram bytes per stencil launch from the committed ncu --set full summary, if any."""
+def ncu_traffic(dtype: str, workload: str, tblock: int = 1, kernel: str = ""):
+    """dram bytes per launch of the dominant kernel from the committed ncu summaries, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        e = t.get(dtype if tblock == 1 else f"{dtype}_tb{tblock}")
+        e = t.get(f"{dtype}_{kernel}" if kernel else (dtype if tblock == 1 else f"{dtype}_tb{tblock}"))
         if e and e.get("workload") == workload:
             return float(e["dram_bytes_per_launch"])
     except Exception:
@@ -319,7 +319,8 @@ def run_table1(args, rank: int, world: int, local: int):
                        "this_run_s_100_steps": ms / args.steps * 100 / 1e3},
             "hbm_gbs_effective": value * 5 * esz,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "k_imp_yc (y-line closed-form solve + three-level update)",
+                         "traffic": ncu_traffic(args.dtype, wl, kernel="imp_yc"),
+                         "kernel": "k_imp_yc (y-line closed-form solve + three-level update)",
                          "algorithmic_bytes_per_update": 3 * esz, "peak_source": peak_src, "kernel_avg_ms": kavg,
                          "level_algorithmic_bytes_per_node": 5 * esz,
                          "level_frac": value * 5 * esz / peak},
