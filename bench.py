@@ -88,6 +88,11 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
 
+    def wait_ready(self, timeout: float = 5.0):
+        t0 = time.time()
+        while self.proc and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
     def mark(self, start: bool):
         if start:
             self.t0 = time.time()
@@ -139,9 +144,21 @@ def cpu_baseline(cfg, dtype: str, budget_s: float = 15.0, rows: int = 1024):
         steps += k
         k *= 2
     upd = rows * (cfg.nx - 2) * steps
-    return {"value": upd / el / 1e9, "unit": UNIT, "cores": int(oracle.max_threads()), "kind": "oracle",
+    cores = int(oracle.max_threads())
+    # the same sample on one core (1-core and all-core rates), ≈ budget / 4
+    oracle.set_threads(1)
+    s1, e1, k = 0, 0.0, 2
+    while e1 < budget_s / 4 and s1 < 2000:
+        t = time.perf_counter()
+        v, u = oracle.leapfrog(2, c1, c2, v, u, k)
+        e1 += time.perf_counter() - t
+        s1 += k
+        k *= 2
+    oracle.set_threads(threads)
+    return {"value": upd / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1core": rows * (cfg.nx - 2) * s1 / e1 / 1e9,
             "sample": f"{rows} rows x {cfg.nx} cols of the per-GPU slab, {steps} leapfrog steps, {dtype}, "
-                      f"OpenMP over rows, {el:.1f} s"}
+                      f"OpenMP over rows, {el:.1f} s (1 core: {s1} steps, {e1:.1f} s)"}
 
 
 def run_reference(args, cfg, rank: int, world: int):
@@ -167,7 +184,7 @@ def run_reference(args, cfg, rank: int, world: int):
     val = upd / el / 1e9
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "impl": "reference",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": args.dtype, "impl": "reference",
             "data": "synthetic (dense uniform[-1,1], seed 0)",
             "config": {"workload": workload_name(cfg, world), "sample_rows": rows, "nx": cfg.nx},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": int(oracle.max_threads()), "kind": "oracle",
@@ -259,10 +276,10 @@ def run_table1(args, rank: int, world: int, local: int):
     u0_dev = u0_host.to(dev)
     torch.cuda.synchronize()
     s.set_initial(u0_dev, None, T1_DT)
+    clocks = ClockSampler(local)
     s.step(max(20, 3 * args.warmup))            # untimed spin-up (clocks ramp), then warm-up
     s.step(args.warmup)
-    clocks = ClockSampler(local)
-    time.sleep(0.2)
+    clocks.wait_ready()
     s.set_option(tsw.TSW_OPT_TIME_KERNELS, 1)
     l0 = s.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -340,6 +357,8 @@ def run_table1(args, rank: int, world: int, local: int):
 
 
 def workload_name(cfg, world: int) -> str:
+    if cfg.name.startswith("config4_strong"):
+        return f"config4_strong_{cfg.nx}x{cfg.ny}_over_{world}_gpus"
     if cfg.batch > 1:
         return f"config5_eps_family_{cfg.batch}x{cfg.nx}x{cfg.ny // world}_per_gpu"
     if cfg.name.startswith("config3"):
@@ -366,6 +385,8 @@ def main():
                     help="config4: the weak-scaling unit (default, the BASELINE metric's scaling "
                          "workload); config5: 65-member eps family x 2048^2; config3: 4096^2 delta line; "
                          "table1: the paper's implicit method on its Table 1 set-up (4096^2, dt 0.05)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: 32768 x rows-per-gpu per GPU (default); strong: the 32768^2 grid split over the GPUs (R22)")
     ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                     help="ghost rows of the row slabs at N > 1: peer stores fused into the stencil (default) or NCCL")
     ap.add_argument("--tblock", type=int, default=0,
@@ -382,7 +403,10 @@ def main():
     elif args.workload == "config3":
         cfg = inputs.config(3, ny=4096 * world)
     else:
-        cfg = inputs.weak_unit(world, rows_per_rank=args.rows_per_gpu, nx=args.nx)
+        if args.scaling == "strong":   # R22: the fixed 32768² grid split over the ranks
+            cfg = inputs.config(4, nx=args.nx, ny=args.nx, name=f"config4_strong_{args.nx}x{args.nx}")
+        else:
+            cfg = inputs.weak_unit(world, rows_per_rank=args.rows_per_gpu, nx=args.nx)
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
@@ -428,13 +452,14 @@ def main():
         u0_dev = u0_host.to(dev)
         torch.cuda.synchronize()
         s.set_initial(u0_dev, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
-        # untimed spin-up (clocks ramp) then the W warm-up steps
+        # untimed spin-up (clocks ramp) then the W warm-up steps; the clock sampler starts first
+        # and must have delivered a sample before the timed region begins
+        clocks = ClockSampler(local) if full else None
         s.step(max(50, 3 * args.warmup))
         s.step(args.warmup)
         s.energy()
-        clocks = ClockSampler(local) if full else None
         if clocks:
-            time.sleep(0.2)
+            clocks.wait_ready()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.set_option(tsw.TSW_OPT_TIME_KERNELS, 1)
         l0 = s.launches()
@@ -528,7 +553,7 @@ def main():
         line = {
             "metric": METRIC, "value": main_res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": main_res["ms"] / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (dense uniform[-1,1] u0, u1 = 0, seed 0; delta-line h_eps, eps = 0.05)",
             "config": {"workload": wl, "nx": cfg.nx, "ny_global": cfg.ny, "rows_per_gpu": cfg.ny // world,
                        "batch": cfg.batch, "dx": cfg.dx, "dt": cfg.dt,
