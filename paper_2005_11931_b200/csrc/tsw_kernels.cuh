@@ -1176,7 +1176,7 @@ struct Energy2Args {
     int64_t items_per_member;
 };
 
-template <typename T>
+template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* __restrict__ partial) {
     constexpr int V = Vec16<T>::N;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1201,26 +1201,31 @@ __global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* _
             xface[k] = (col + k <= a.nx - 2);
         }
         T c1l[V], c2l[V];
-        if (a.mode == MODE_LINE) {
+        if (MODE == MODE_LINE) {
             vload(C1 + col, c1l);
             vload(C2 + col, c2l);
         }
+        // lane 31 needs the first column of the next strip (its right neighbour): prefetched one
+        // row ahead together with the row itself, so no load sits on an iteration's critical path
+        const bool rok = (lane == 31) && (cs + 32 * V < a.pitch);
+        const int64_t rcol = cs + 32 * V;
         T ac[V], bc[V], an[V], bn[V];
         vload(A + s0 * a.pitch + col, ac);
         vload(Bv + s0 * a.pitch + col, bc);
+        T xr = rok ? A[s0 * a.pitch + rcol] : (T)0, yr = rok ? Bv[s0 * a.pitch + rcol] : (T)0;
         for (int s = s0; s < s1; ++s) {
             const int64_t g = a.r0 + s - 1;
             vload(A + (s + 1) * a.pitch + col, an);
             vload(Bv + (s + 1) * a.pitch + col, bn);
+            const T xn = rok ? A[(s + 1) * a.pitch + rcol] : (T)0, yn = rok ? Bv[(s + 1) * a.pitch + rcol] : (T)0;
             T ar = __shfl_down_sync(0xffffffffu, ac[0], 1);
             T br = __shfl_down_sync(0xffffffffu, bc[0], 1);
             if (lane == 31) {
-                const bool ok = cs + 32 * V < a.pitch;
-                ar = ok ? A[s * a.pitch + cs + 32 * V] : (T)0;
-                br = ok ? Bv[s * a.pitch + cs + 32 * V] : (T)0;
+                ar = xr;
+                br = yr;
             }
             T c1d[V], c2d[V];
-            if (a.mode == MODE_DENSE) {
+            if (MODE == MODE_DENSE) {
                 vload(C1 + s * a.pitch + col, c1d);
                 vload(C2 + (s + 1) * a.pitch + col, c2d);
             }
@@ -1236,14 +1241,16 @@ __global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* _
                 if (row_int && xface[k]) {
                     const double a1 = (double)((k == V - 1) ? ar : ac[k + 1]);
                     const double b1 = (double)((k == V - 1) ? br : bc[k + 1]);
-                    const double c = (a.mode == MODE_LINE) ? (double)c1l[k] : (double)c1d[k];
+                    const double c = (MODE == MODE_LINE) ? (double)c1l[k] : (double)c1d[k];
                     acc += (c * (a1 - a0)) * (b1 - b0);
                 }
                 if (yface && colint[k]) {
-                    const double c = (a.mode == MODE_LINE) ? (double)c2l[k] : (double)c2d[k];
+                    const double c = (MODE == MODE_LINE) ? (double)c2l[k] : (double)c2d[k];
                     acc += (c * ((double)an[k] - a0)) * ((double)bn[k] - b0);
                 }
             }
+            xr = xn;
+            yr = yn;
 #pragma unroll
             for (int k = 0; k < V; ++k) {
                 ac[k] = an[k];

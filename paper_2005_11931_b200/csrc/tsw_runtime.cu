@@ -1897,8 +1897,8 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
         a.rows = int32_t(c->ny_local);
         const int64_t cta_w = 8 * 32 * int64_t(16 / c->esz);
         a.cta_strips = (c->pitch + cta_w - 1) / cta_w;
-        // ≈ 4 CTAs per SM over the batch, ≤ nblk_red partials per member
-        int64_t chunks = (int64_t(4) * c->sm_count + a.cta_strips * c->g.batch - 1) / (a.cta_strips * c->g.batch);
+        // ≈ 8 CTAs per SM over the batch, ≤ nblk_red partials per member
+        int64_t chunks = (int64_t(8) * c->sm_count + a.cta_strips * c->g.batch - 1) / (a.cta_strips * c->g.batch);
         chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, std::max<int64_t>(1, c->nblk_red / a.cta_strips)));
         chunks = std::min<int64_t>(chunks, c->ny_local);
         a.rows_per_item = int32_t((c->ny_local + chunks - 1) / chunks);
@@ -1907,10 +1907,13 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
         if (a.items_per_member > c->nblk_red) return fail(TSW_ERR_ARG, "energy: too many partials (pitch too wide)");
         nparts = int(a.items_per_member);
         dim3 grid(unsigned(a.items_per_member), unsigned(c->g.batch));
-        if (is_f64(c))
-            k_energy2d<double><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
-        else
-            k_energy2d<float><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+        if (is_f64(c)) {
+            if (c->mode == MODE_LINE) k_energy2d<double, MODE_LINE><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+            else k_energy2d<double, MODE_DENSE><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+        } else {
+            if (c->mode == MODE_LINE) k_energy2d<float, MODE_LINE><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+            else k_energy2d<float, MODE_DENSE><<<grid, 256, 0, c->stream>>>(a, c->d_partial);
+        }
         CKL();
     } else {
         EnergyArgs a;
