@@ -696,6 +696,7 @@ tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1, int32_t s_lo, int32_
         case 4: return launch_tb_t<T, 4>(c, fk, fkm1, s_lo, s_hi);
         case 5: return launch_tb_t<T, 5>(c, fk, fkm1, s_lo, s_hi);
         case 6: return launch_tb_t<T, 6>(c, fk, fkm1, s_lo, s_hi);
+        case 7: return launch_tb_t<T, 7>(c, fk, fkm1, s_lo, s_hi);
         case 8: return launch_tb_t<T, 8>(c, fk, fkm1, s_lo, s_hi);
         default: return fail(TSW_ERR_ARG, "unsupported temporal blocking depth %d", K);
     }
@@ -2248,8 +2249,8 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     if (key == TSW_OPT_TBLOCK) {
-        if (!(value >= 1 && value <= 6) && value != 8)
-            return fail(TSW_ERR_ARG, "temporal blocking depth must be 1..6 or 8");
+        if (!(value >= 1 && value <= 8))
+            return fail(TSW_ERR_ARG, "temporal blocking depth must be 1..8");
         if (value > 1 && c->g.dim != 2) return fail(TSW_ERR_ARG, "temporal blocking needs a 2D grid");
         if (value > 1 && c->g.nranks > 1 && value > c->G)
             return fail(TSW_ERR_ARG, "temporal blocking depth %d exceeds the %d ghost rows of a slab", int(value), c->G);

@@ -25,7 +25,7 @@ def _run(cfg, dtype, K, nsteps, u0, rows_per_item=0, profile=None):
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("K", [2, 3, 4, 5, 6, 8])
+@pytest.mark.parametrize("K", [2, 3, 4, 5, 6, 7, 8])
 def test_tblock_bitwise_vs_oracle(dtype, K):
     cfg = inputs.config(3, nx=1300, ny=211, dx=0.01, dy=0.01, eps=[0.05, 0.3], amp=[1.0, 0.0], dt=2e-3)
     u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(NP[dtype])
