@@ -261,12 +261,21 @@ def _dense_rows(cfg):
     return lambda j0, rows, i0, cols: inputs.uniform_dense_rows(cfg.nx, cfg.ny, j0, rows)[:, i0:i0 + cols]
 
 
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_config4_weak_unit_sampled_windows(dtype):
-    """The bench workload (32768 × 4096 slab, dense data) in the bench's launch configuration:
-    sampled nodes against light-cone oracle windows, bitwise with the GPU's own faces."""
-    cfg = inputs.weak_unit(1)
+BENCH_K = {"f64": 4, "f32": 8}   # bench.py's default temporal-blocking depth per dtype
+
+
+@pytest.mark.parametrize("dtype,K,full", [("f64", 1, False), ("f32", 1, False), ("f64", BENCH_K["f64"], False),
+                                          ("f32", BENCH_K["f32"], False), ("f64", BENCH_K["f64"], True),
+                                          ("f32", BENCH_K["f32"], True)])
+def test_config4_weak_unit_sampled_windows(dtype, K, full):
+    """The bench workload (32768 × 4096 slab, dense data) in the bench's launch configuration
+    (temporally blocked, K per dtype; K = 1 too) and the full 32768² config-4 grid
+    (`bench.py --scaling strong`): sampled nodes against light-cone oracle windows, bitwise with
+    the GPU's own faces."""
+    cfg = inputs.config(4) if full else inputs.weak_unit(1)
     s = tsw.Solver.from_config(cfg, dtype)
+    if K > 1:
+        s.set_option(tsw.TSW_OPT_TBLOCK, K)
     u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(NP[dtype])
     s.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
     nsteps = 40
@@ -275,7 +284,8 @@ def test_config4_weak_unit_sampled_windows(dtype):
     rng = np.random.default_rng(5)
     V = 2 if dtype == "f64" else 4
     samples = [(0, 0), (1, 1), (cfg.ny - 2, cfg.nx - 2), (cfg.ny - 1, 100), (2048, cfg.nx // 2 - 1),
-               (2048, cfg.nx // 2), (17, 32 * V - 1), (17, 32 * V), (300, 64 * V - 1)]
+               (2048, cfg.nx // 2), (17, 32 * V - 1), (17, 32 * V), (300, 64 * V - 1),
+               (cfg.ny // 2, 503), (cfg.ny // 2, 504), (cfg.ny // 2, 505), (5, 1007), (cfg.ny - 3, 1008)]
     samples += [(int(rng.integers(0, cfg.ny)), int(rng.integers(0, cfg.nx))) for _ in range(40)]
     thin = tsw.Solver.from_config(inputs.weak_unit(1, rows_per_rank=8), dtype)
     line = thin.read_faces()[0][0, 0]
