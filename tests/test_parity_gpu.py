@@ -463,3 +463,34 @@ def test_boundary_forced_zero_and_velocity_start():
         z[0] = z[-1] = 0; z[:, 0] = z[:, -1] = 0
     ref = oracle.startup(2, c1, c2, z0, z1, cfg.dt)
     assert np.array_equal(g[0], ref)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_config5_and_config3_bench_launch_configuration(dtype):
+    """config 5 (65 × 2048² ε family) and config 3 (4096²) as bench.py runs them — temporally
+    blocked at the dtype's K: config 5 bitwise equal to the one-level launch on every member,
+    config 3 against the full oracle at 100 steps."""
+    K = BENCH_K[dtype]
+    cfg = inputs.config(5)
+    u0 = cfg.initial().astype(NP[dtype])
+    runs = []
+    for k in (1, K):
+        s = tsw.Solver.from_config(cfg, dtype)
+        if k > 1:
+            s.set_option(tsw.TSW_OPT_TBLOCK, k)
+        s.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+        s.step(3 * K + 1)
+        runs.append((s.read(0), s.energy()))
+        s.close()
+    assert np.array_equal(runs[0][0], runs[1][0])
+    np.testing.assert_allclose(runs[0][1], runs[1][1], rtol=1e-12)
+    del runs
+    cfg = inputs.config(3)
+    s = tsw.Solver.from_config(cfg, dtype)
+    s.set_option(tsw.TSW_OPT_TBLOCK, K)
+    u0 = cfg.initial().astype(NP[dtype])
+    s.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    s.step(100)
+    un, _, _, _ = oracle.run_member(cfg, 0, NP[dtype], nsteps=100, u0=u0)
+    assert rel_maxnorm(s.read(0)[0], un) <= TOL[dtype]
+    s.close()
