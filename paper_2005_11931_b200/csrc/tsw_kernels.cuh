@@ -30,6 +30,10 @@ __device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a
 __device__ __forceinline__ float r_add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float r_sub(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b); }
+// fl(2u − p) in one instruction: 2u is exact (a doubling), so the fused form rounds exactly like
+// the canonical r_sub(r_mul(2, u), p) — bit-identical (R19), one FP op fewer per update
+__device__ __forceinline__ double twice_minus(double u, double p) { return __fma_rn(2.0, u, -p); }
+__device__ __forceinline__ float twice_minus(float u, float p) { return __fmaf_rn(2.0f, u, -p); }
 
 template <typename T> struct Vec16;
 template <> struct Vec16<double> { using type = double2; static constexpr int N = 2; };
@@ -83,7 +87,7 @@ __device__ __forceinline__ T node_update(T u, T ul, T ur, T ud, T uu, T p, T c1l
         lap = r_add(lap, r_sub(r_mul(c2u, dyp), r_mul(c2d, dym)));
     }
     if (START) return r_add(r_add(u, r_mul(dtT, p)), r_mul((T)0.5, lap));
-    return r_add(r_sub(r_mul((T)2, u), p), lap);
+    return r_add(twice_minus(u, p), lap);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -632,7 +636,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
             const T lapx = (k == 0) ? r_sub(F1, F0) : r_sub(F2, F1);
             const T lap = r_add(lapx, r_sub(gu, gd));
             const T pr = (m == 1) ? S.pm1[k] : S.w[(m >= 2) ? m - 2 : 0][C][k];
-            const T v = r_add(r_sub(r_mul((T)2, cu), pr), lap);
+            const T v = r_add(twice_minus(cu, pr), lap);
             if (MASKED) {
                 const bool ok = rowok & S.colint[k];
                 nv[k] = ok ? v : (T)0;
