@@ -225,13 +225,16 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               line solves (2D) by the scan solvers of TSW_OPT_IMPLICIT_SOLVER, (1D)
                               Thomas; unconditionally stable (no CFL check).  Single rank, δ-line /
                               constant / profile kinds (x-only coefficients), ≤ 8192 unknowns per line. */
-#define TSW_OPT_IMPLICIT_SOLVER 9 /* 2D line solves of the implicit scheme.  0 (default): scans (reading
-                              R28) — x lines share one matrix, whose LU is applied as two affine scans
-                              per row; y lines are Toeplitz per column and solved by the closed form
+#define TSW_OPT_IMPLICIT_SOLVER 9 /* 2D line solves of the implicit scheme.  Scans (reading R28): x lines
+                              share one matrix, whose LU is applied as two affine scans per row; y
+                              lines are Toeplitz per column and solved by the closed form
                               T⁻¹ = κ⁻¹[(I − ρS)(I − ρSᵀ) + ρ²e₁e₁ᵀ]⁻¹ (exponential scans + a rank-one
-                              correction), in place, 5 words of HBM traffic per node and level.
+                              correction), fused with the three-level update.  The y solve runs either
+                              in thread-block clusters holding the columns on chip (3: 5 words per node
+                              and level) or as three barrier-free streaming kernels (2: z read twice).
+                              0 (default): auto — 2 for fp64 grids of ≥ 8 M nodes, else 3.
                               1: cyclic reduction per line in shared memory with tiled transposes
-                              (the paper's solver), ≤ 227 KB/(4·sizeof(T)) unknowns per line. */
+                              (the paper's solver), ≤ 4095 (fp64) / 8191 (fp32) unknowns per line. */
 #define TSW_OPT_HALO 11     /* ghost rows of 2D slabs.  0 (default): NCCL send/recv (tsw_nccl_init).
                               1: peer stores — the temporally blocked stencil writes its first / last K
                               owned rows straight into the neighbours' ghost rows through mapped peer

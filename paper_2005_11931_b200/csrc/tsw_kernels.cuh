@@ -2537,6 +2537,201 @@ __global__ void __launch_bounds__(IMPYC_THREADS, 2) k_imp_yc(const ImpYArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Implicit y solve, streaming variant (TSW_OPT_IMPLICIT_SOLVER = 2): the same closed form as
+// k_imp_yc in three barrier-free kernels — per-(column, segment) decayed sums; a per-column scan
+// of the segments (carries and the column constants of the closed form); the finish (L_j, R_j,
+// the boundary terms and the three-level update).  z is read twice (4 words + the small carry
+// arrays per node and level) but every kernel is a plain coalesced stream.
+// ------------------------------------------------------------------------------------------
+constexpr int IMPS_SEG = 16;   // rows per segment
+
+struct ImpSArgs {
+    const void* z;      // x-solve output (field layout)
+    void* prev;         // u^{n−1} / u₁ → u^{n+1}
+    const void* ycol;   // [B][4][ncolp]: ρ, K = 1/(κ(1−ρ²)), i1 = 1/(1−ρ²), spare   (columns 1..nx−2 at 0..)
+    void* cF;           // [B][nseg][ncolp]: forward sums → L_in
+    void* cB;           // [B][nseg][ncolp]: backward sums → S_below
+    void* ccon;         // [B][2][ncolp]: βz₁, A₂'
+    int64_t pitch, mstride, ncolp;
+    int32_t nx, m, nseg;
+    double dt;
+};
+
+// column constants from c2 (once per coefficients / dt)
+template <typename T>
+__global__ void k_imp_ycol(const T* __restrict__ c2, int64_t cpitch, T* __restrict__ ycol, int64_t ncolp, int nx, int B) {
+    const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int b = blockIdx.y;
+    if (i >= nx - 2 || b >= B) return;
+    const double g = (double)c2[b * cpitch + 1 + i];
+    const double sq = sqrt(1.0 + 2.0 * g);
+    const double rho = g / ((1.0 + g) + sq);
+    const double kap = 0.5 * ((1.0 + g) + sq);
+    const double omr = (1.0 + sq) / ((1.0 + g) + sq);
+    const double i1 = 1.0 / (omr * (1.0 + rho));
+    T* y = ycol + b * 4 * ncolp;
+    y[i] = (T)rho;
+    y[ncolp + i] = (T)(i1 / kap);
+    y[2 * ncolp + i] = (T)i1;
+}
+
+// pass 1: thread (column, segment) — F (forward, to the last valid row), B (backward, from the start)
+template <typename T>
+__global__ void __launch_bounds__(256) k_imp_ysum(const ImpSArgs a) {
+    const int64_t ci = blockIdx.x * 32 + threadIdx.x;   // column index 0.. (global column ci + 1)
+    const int sg = blockIdx.y * 8 + threadIdx.y;
+    const int b = blockIdx.z;
+    if (ci >= a.nx - 2 || sg >= a.nseg) return;
+    const T rho = static_cast<const T*>(a.ycol)[b * 4 * a.ncolp + ci];
+    const int j0 = 1 + sg * IMPS_SEG;
+    const int nv = min(IMPS_SEG, a.m - j0 + 1);
+    const T* zq = static_cast<const T*>(a.z) + b * a.mstride + (ci + 1) + int64_t(1 + j0) * a.pitch;
+    T zz[IMPS_SEG];
+#pragma unroll
+    for (int k = 0; k < IMPS_SEG; ++k) zz[k] = (k < nv) ? zq[int64_t(k) * a.pitch] : (T)0;
+    T F = (T)0, Bs = (T)0, pw = (T)1;
+#pragma unroll
+    for (int k = 0; k < IMPS_SEG; ++k) {
+        if (k < nv) {
+            F = fmaT(rho, F, zz[k]);
+            Bs = fmaT(pw, zz[k], Bs);
+            pw = pw * rho;
+        }
+    }
+    static_cast<T*>(a.cF)[(b * int64_t(a.nseg) + sg) * a.ncolp + ci] = F;
+    static_cast<T*>(a.cB)[(b * int64_t(a.nseg) + sg) * a.ncolp + ci] = Bs;
+}
+
+// pass 2: scans over the segments of each column (in place: F → L_in, B → S_below) and the
+// column-global constants βz₁, A₂'.  CTA = 32 columns × 32 groups; group g owns segments
+// [g·G, (g+1)·G): local scans, carries across the groups through shared memory, re-walk.
+constexpr int IMPS_GROUPS = 32;
+template <typename T, int GMAX>
+__global__ void __launch_bounds__(1024) k_imp_yscan(const ImpSArgs a) {
+    __shared__ T sF[IMPS_GROUPS][33], sB[IMPS_GROUPS][33], sP[IMPS_GROUPS][33];
+    __shared__ T sLm[32], sA1[32];
+    const int tx = threadIdx.x, grp = threadIdx.y;
+    const int64_t ci = blockIdx.x * 32 + tx;
+    const int b = blockIdx.y;
+    const bool ok = ci < a.nx - 2;
+    const int G = (a.nseg + IMPS_GROUPS - 1) / IMPS_GROUPS;   // segments per group (≤ GMAX)
+    const T* y = static_cast<const T*>(a.ycol) + b * 4 * a.ncolp;
+    const T rho = ok ? y[ci] : (T)0;
+    const T i1 = ok ? y[2 * a.ncolp + ci] : (T)1;
+    T* F = static_cast<T*>(a.cF) + b * int64_t(a.nseg) * a.ncolp + ci;
+    T* Bv = static_cast<T*>(a.cB) + b * int64_t(a.nseg) * a.ncolp + ci;
+    const T rS = powi_T(rho, IMPS_SEG);
+    const int nlast = a.m - (a.nseg - 1) * IMPS_SEG;
+    const T rL = powi_T(rho, nlast);
+    const int g0 = grp * G;
+    T f[GMAX], bb[GMAX];
+    T Lloc = (T)0, P = (T)1;
+#pragma unroll
+    for (int k = 0; k < GMAX; ++k) {
+        const int sg = g0 + k;
+        const bool v = ok && k < G && sg < a.nseg;
+        f[k] = v ? F[int64_t(sg) * a.ncolp] : (T)0;
+        bb[k] = v ? Bv[int64_t(sg) * a.ncolp] : (T)0;
+        if (v) {
+            const T fac = (sg == a.nseg - 1) ? rL : rS;
+            Lloc = fmaT(fac, Lloc, f[k]);
+            P = P * fac;
+        }
+    }
+    T Sloc = (T)0;
+#pragma unroll
+    for (int k = GMAX - 1; k >= 0; --k) {
+        const int sg = g0 + k;
+        if (ok && k < G && sg < a.nseg) Sloc = fmaT((sg == a.nseg - 1) ? rL : rS, Sloc, bb[k]);
+    }
+    sF[grp][tx] = Lloc;
+    sB[grp][tx] = Sloc;
+    sP[grp][tx] = P;
+    __syncthreads();
+    T L = (T)0;
+    for (int g = 0; g < grp; ++g) L = fmaT(sP[g][tx], L, sF[g][tx]);
+    T S = (T)0;
+    for (int g = IMPS_GROUPS - 1; g > grp; --g) S = fmaT(sP[g][tx], S, sB[g][tx]);
+    if (grp == IMPS_GROUPS - 1) sLm[tx] = fmaT(P, L, Lloc);   // L_m: everything composed
+    if (grp == 0) sA1[tx] = fmaT(P, S, Sloc);                  // A₁
+    // re-walk with the true carries
+#pragma unroll
+    for (int k = 0; k < GMAX; ++k) {
+        const int sg = g0 + k;
+        if (ok && k < G && sg < a.nseg) {
+            F[int64_t(sg) * a.ncolp] = L;
+            L = fmaT((sg == a.nseg - 1) ? rL : rS, L, f[k]);
+        }
+    }
+#pragma unroll
+    for (int k = GMAX - 1; k >= 0; --k) {
+        const int sg = g0 + k;
+        if (ok && k < G && sg < a.nseg) {
+            Bv[int64_t(sg) * a.ncolp] = S;
+            S = fmaT((sg == a.nseg - 1) ? rL : rS, S, bb[k]);
+        }
+    }
+    __syncthreads();
+    if (grp == 0 && ok) {
+        const T Lm = sLm[tx], A1 = sA1[tx];
+        const T A2 = rho * Lm;
+        const T rhom = powi_T(rho, a.m);
+        const T z1 = (A1 - rhom * A2) * i1;
+        const T rr = rho * rho;
+        const T beta = rr / ((T)1 + rr * (((T)1 - rhom * rhom) * i1));
+        const T bz1 = beta * z1;
+        T* cc = static_cast<T*>(a.ccon) + b * 2 * a.ncolp;
+        cc[ci] = bz1;
+        cc[a.ncolp + ci] = A2 - bz1 * rhom;
+    }
+}
+
+// pass 3: thread (column, segment) — u^{n+1}_j = K·(L_j + R_j − βz₁ρ^{j−1} − ρ^{m+1−j}A₂') ∓ prev_j
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_imp_yfin(const ImpSArgs a) {
+    const int64_t ci = blockIdx.x * 32 + threadIdx.x;
+    const int sg = blockIdx.y * 8 + threadIdx.y;
+    const int b = blockIdx.z;
+    if (ci >= a.nx - 2 || sg >= a.nseg) return;
+    const int j0 = 1 + sg * IMPS_SEG;
+    const int nv = min(IMPS_SEG, a.m - j0 + 1);
+    const T* zq = static_cast<const T*>(a.z) + b * a.mstride + (ci + 1) + int64_t(1 + j0) * a.pitch;
+    T* pq = static_cast<T*>(a.prev) + b * a.mstride + (ci + 1) + int64_t(1 + j0) * a.pitch;
+    T zz[IMPS_SEG], w[IMPS_SEG];
+#pragma unroll
+    for (int k = 0; k < IMPS_SEG; ++k) {
+        zz[k] = (k < nv) ? zq[int64_t(k) * a.pitch] : (T)0;
+        w[k] = (k < nv) ? pq[int64_t(k) * a.pitch] : (T)0;
+    }
+    const T* y = static_cast<const T*>(a.ycol) + b * 4 * a.ncolp;
+    const T rho = y[ci], K = y[a.ncolp + ci];
+    const T* cc = static_cast<const T*>(a.ccon) + b * 2 * a.ncolp;
+    const T bz1 = cc[ci], A2p = cc[a.ncolp + ci];
+    T L = static_cast<const T*>(a.cF)[(b * int64_t(a.nseg) + sg) * a.ncolp + ci];
+    T R = rho * static_cast<const T*>(a.cB)[(b * int64_t(a.nseg) + sg) * a.ncolp + ci];
+    T pu = powi_T(rho, j0 - 1);
+    T pd = powi_T(rho, a.m + 1 - (j0 + nv - 1));
+    const T dtT = (T)a.dt;
+#pragma unroll
+    for (int k = 0; k < IMPS_SEG; ++k) {
+        if (k < nv) {
+            L = fmaT(rho, L, zz[k]);
+            const T lc = K * fmaT(-bz1, pu, L);
+            w[k] = (MODE == 0) ? (lc - w[k]) : fmaT(dtT, w[k], lc);
+            pu = pu * rho;
+        }
+    }
+#pragma unroll
+    for (int k = IMPS_SEG - 1; k >= 0; --k) {
+        if (k < nv) {
+            pq[int64_t(k) * a.pitch] = fmaT(K, fmaT(-pd, A2p, R), w[k]);
+            pd = pd * rho;
+            R = rho * (zz[k] + R);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // Peer halos (peer mode): ghost rows are written by the producing rank straight
 // into its neighbours' buffers through mapped peer pointers (NVLink), instead of NCCL messages.
 // k_push_rows copies rows that are already computed (start-up level, initial state, remainder

@@ -216,10 +216,15 @@ struct tsw_ctx {
     void* imp_s1 = nullptr;   // implicit: x-solve output (field layout)
     void* imp_t = nullptr;    // implicit: transposed field [B][nx][pt]
     int64_t imp_pt = 0;       // its pitch (≥ ny, multiple of 32)
-    int imp_solver = 0;       // 0: scan solvers (R28, default); 1: cyclic reduction (the paper's)
+    int imp_solver = 0;       // 0 auto, 1 cyclic reduction (the paper's), 2 streaming scans, 3 cluster scans (R28)
     void* imp_tab = nullptr;  // x-line LU tables [B][3][imp_tpitch] (scan solver)
     int64_t imp_tpitch = 0;
     bool imp_fact_valid = false;
+    void* imp_ycol = nullptr;   // streaming y solve (solver 2): column constants [B][4][ncolp]
+    void* imp_cF = nullptr;     //   segment sums / carries [B][nseg][ncolp]
+    void* imp_cB = nullptr;
+    void* imp_ccon = nullptr;   //   βz₁, A₂' [B][2][ncolp]
+    bool imp_ycol_stale = true;
     int tb_depth = 4;     // its input ring stages
     int tb_occ[2][9] = {};  // [f64][K] resident CTAs per SM (cached)
     int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
@@ -356,6 +361,68 @@ tsw_status implicit_level_scan_t(tsw_ctx* c, bool start) {
     if (nx <= 1024 * W) st = launch_imp_x<T, W>(c, ax);
     else st = launch_imp_x<T, 2 * W>(c, ax);
     if (st) return st;
+    // solver 0 (auto): the streaming y solve for large fp64 grids (where the cluster kernel is
+    // latency-bound), the cluster solve otherwise (measured)
+    const int solver = (c->imp_solver == 0) ? ((is_f64(c) && int64_t(m) * my >= (int64_t(8) << 20)) ? 2 : 3)
+                                            : c->imp_solver;
+    if (solver == 2) {   // streaming y solve: three barrier-free kernels
+        const int64_t ncolp = round_up(nx, 32);
+        const int nseg = (my + IMPS_SEG - 1) / IMPS_SEG;
+        if (!c->imp_ycol) {
+            const size_t B = size_t(c->g.batch);
+            CK(cudaMalloc(&c->imp_ycol, B * 4 * ncolp * sizeof(T)));
+            CK(cudaMalloc(&c->imp_cF, B * nseg * ncolp * sizeof(T)));
+            CK(cudaMalloc(&c->imp_cB, B * nseg * ncolp * sizeof(T)));
+            CK(cudaMalloc(&c->imp_ccon, B * 2 * ncolp * sizeof(T)));
+            c->imp_fact_valid = false;
+        }
+        if (!c->imp_fact_valid || c->imp_ycol_stale) {
+            k_imp_ycol<T><<<dim3(unsigned((m + 255) / 256), unsigned(c->g.batch)), 256, 0, c->stream>>>(
+                static_cast<const T*>(c->c2), c->cstride2, static_cast<T*>(c->imp_ycol), ncolp, int(nx), c->g.batch);
+            CKL();
+            c->launches++;
+            c->imp_ycol_stale = false;
+        }
+        ImpSArgs as;
+        as.z = c->imp_s1;
+        as.prev = c->buf[c->ip];
+        as.ycol = c->imp_ycol;
+        as.cF = c->imp_cF;
+        as.cB = c->imp_cB;
+        as.ccon = c->imp_ccon;
+        as.pitch = c->pitch;
+        as.mstride = c->mstride;
+        as.ncolp = ncolp;
+        as.nx = int32_t(nx);
+        as.m = my;
+        as.nseg = nseg;
+        as.dt = c->dt;
+        const dim3 g2(unsigned((m + 31) / 32), unsigned((nseg + 7) / 8), unsigned(c->g.batch));
+        k_imp_ysum<T><<<g2, dim3(32, 8), 0, c->stream>>>(as);
+        CKL();
+        const dim3 gs(unsigned((m + 31) / 32), unsigned(c->g.batch)), bs(32, IMPS_GROUPS);
+        if (nseg <= 8 * IMPS_GROUPS) k_imp_yscan<T, 8><<<gs, bs, 0, c->stream>>>(as);
+        else k_imp_yscan<T, 16><<<gs, bs, 0, c->stream>>>(as);
+        CKL();
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (c->timing) {
+            tsw_status st2 = timing_events(c, &e0, &e1);
+            if (st2) return st2;
+            CK(cudaEventRecord(e0, c->stream));
+        }
+        if (start) k_imp_yfin<T, 1><<<g2, dim3(32, 8), 0, c->stream>>>(as);
+        else k_imp_yfin<T, 0><<<g2, dim3(32, 8), 0, c->stream>>>(as);
+        CKL();
+        if (c->timing) {
+            CK(cudaEventRecord(e1, c->stream));
+            c->timed_launches++;
+            c->timed_updates += int64_t(m) * my * c->g.batch;
+        }
+        c->launches += 4;
+        std::swap(c->ic, c->ip);
+        c->n++;
+        return TSW_OK;
+    }
     ImpYArgs ay;
     ay.z = c->imp_s1;
     ay.prev = c->buf[c->ip];
@@ -450,7 +517,7 @@ tsw_status implicit_level_t(tsw_ctx* c, bool start) {
         return TSW_OK;
     }
     const int64_t nx = c->g.nx, ny = c->g.ny;
-    if (c->imp_solver == 0) return implicit_level_scan_t<T>(c, start);
+    if (c->imp_solver != 1) return implicit_level_scan_t<T>(c, start);
     // (1) x lines: (I − ½L_x) z = scale·u  on the interior rows (view rows 2 .. ny−1)
     CrArgs ax;
     ax.src = c->buf[c->ic];
@@ -990,6 +1057,7 @@ tsw_status prescale_all(tsw_ctx* c) {
     }
     c->launches += (c->g.dim == 2) ? 2 : 1;
     c->imp_fact_valid = false;
+    c->imp_ycol_stale = true;
     return TSW_OK;
 }
 
@@ -1474,6 +1542,8 @@ void tsw_destroy(tsw_ctx* c) {
     dfree_guarded(c->imp_s1, c->fshift);
     if (c->imp_t) cudaFree(c->imp_t);
     if (c->imp_tab) cudaFree(c->imp_tab);
+    for (void* p : {c->imp_ycol, c->imp_cF, c->imp_cB, c->imp_ccon})
+        if (p) cudaFree(p);
     dfree_guarded(c->h1, c->cshift_h);
     dfree_guarded(c->h2, c->cshift_h);
     dfree_guarded(c->c1, c->cshift);
@@ -2324,7 +2394,8 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return guard_fill(c);
     }
     if (key == TSW_OPT_IMPLICIT_SOLVER) {
-        if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "implicit solver must be 0 (scans) or 1 (cyclic reduction)");
+        if (value < 0 || value > 3)
+            return fail(TSW_ERR_ARG, "implicit solver must be 0 (auto), 1 (cyclic reduction), 2 (streaming scans) or 3 (cluster scans)");
         if (value == 1 && c->g.dim == 2) {
             int64_t lim = 1;  // largest 2^q − 1 whose four line arrays fit in 227 KB
             while ((2 * lim + 1) * 4 * int64_t(c->esz) <= 227 * 1024) lim = 2 * lim + 1;

@@ -16,7 +16,7 @@ from tests.helpers import NP, host_cores, rel_maxnorm
 
 pytestmark = pytest.mark.gpu
 oracle.set_threads(host_cores())
-SOLVERS = {"scan": 0, "cr": 1}
+SOLVERS = {"scan": 3, "cr": 1, "stream": 2, "auto": 0}
 
 
 def _implicit_solver(cfg, dtype="f64", solver="scan"):
@@ -58,7 +58,7 @@ def _oracle_2d(s, cfg, u0, v1, n, dtype):
 SHAPES = [(130, 97), (300, 257), (64, 700), (40, 1500), (33, 3000), (9, 5000), (1029, 40), (3, 3), (4, 70), (70, 4)]
 
 
-@pytest.mark.parametrize("solver", ["scan", "cr"])
+@pytest.mark.parametrize("solver", ["scan", "cr", "stream"])
 @pytest.mark.parametrize("shape", SHAPES)
 def test_implicit_2d_vs_oracle(shape, solver):
     ny, nx = shape
@@ -85,7 +85,7 @@ def test_implicit_2d_vs_oracle(shape, solver):
     s.close()
 
 
-@pytest.mark.parametrize("solver", ["scan", "cr"])
+@pytest.mark.parametrize("solver", ["scan", "cr", "stream"])
 def test_implicit_2d_f32(solver):
     cfg = inputs.config(3, nx=515, ny=260, dx=0.02, dy=0.02, eps=[0.1], amp=[1.0], dt=0.02)
     s = _implicit_solver(cfg, "f32", solver)
@@ -105,13 +105,14 @@ def test_implicit_solvers_agree_and_constant_coeffs_symmetric():
     u0 = inputs.uniform_dense((257, 257), seed=8)
     u0 = 0.5 * (u0 + u0.T)
     res = []
-    for solver in ("scan", "cr"):
+    for solver in ("scan", "cr", "stream"):
         s = _implicit_solver(cfg, solver=solver)
         s.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
         s.step(30)
         res.append(s.read(0)[0])
         s.close()
     assert rel_maxnorm(res[0], res[1]) < 1e-10
+    assert rel_maxnorm(res[0], res[2]) < 1e-10
     assert rel_maxnorm(res[0], res[0].T) < 1e-11
 
 

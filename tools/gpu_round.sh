@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_tblock_gpu.py tests/test_family_gpu.py tests/test_guards_gpu.py -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_e.log 2>&1; echo pytest_exit=$?
-tail -2 gpurun_out/pytest_e.log
-timeout 300 python bench.py --steps 200 --warmup 3 --no-cpu-baseline --no-also --no-e2e > gpurun_out/b_short.json 2>&1 && \
-timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"k_energy2d" --csv --log-file gpurun_out/launches_energy.csv python bench.py --steps 200 --warmup 3 --no-cpu-baseline --no-also --no-e2e > gpurun_out/ncu_e.log 2>&1; echo ncu=$?
+timeout 600 python -m pytest tests/test_implicit_gpu.py tests/test_guards_gpu.py -q -x --timeout 120 -p no:cacheprovider > gpurun_out/pytest_imp.log 2>&1; echo pytest_exit=$?
+tail -2 gpurun_out/pytest_imp.log; grep -E "^E  " gpurun_out/pytest_imp.log | head -5
+timeout 300 python bench.py --workload table1 --steps 100 > gpurun_out/bench_table1_f64.json 2> gpurun_out/bench_table1.err; echo t1=$?
+timeout 300 python bench.py --workload table1 --steps 100 --dtype f32 --no-cpu-baseline > gpurun_out/bench_table1_f32.json 2>> gpurun_out/bench_table1.err; echo t1f32=$?
