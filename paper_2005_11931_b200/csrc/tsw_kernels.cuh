@@ -2108,6 +2108,204 @@ __global__ void __launch_bounds__(1024, 1) k_imp_x(const ImpXArgs a) {
     }
 }
 
+// Two rows per iteration (rows line and line + gridDim.x): the dependent scan chains of the two
+// rows interleave and the four barriers per iteration serve both.  The LU tables live in shared
+// memory as [k][thread] (conflict-free) so both rows' data and prefetch fit the 64 registers.
+template <typename T, int R>
+__global__ void __launch_bounds__(1024, 1) k_imp_x2(const ImpXArgs a) {
+    __shared__ T fwv[2][IMPX_MAXW], bwv[2][IMPX_MAXW], fwc[2][IMPX_MAXW], bwc[2][IMPX_MAXW];
+    __shared__ T fwa[IMPX_MAXW], bwa[IMPX_MAXW];
+    __shared__ T fxa[5][IMPX_MAXW], bxa[5][IMPX_MAXW];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int t = threadIdx.x, nt = blockDim.x;
+    T* lvf = reinterpret_cast<T*>(smem_raw);   // [5][nt]
+    T* lvb = lvf + 5 * nt;                      // [5][nt]
+    T* stl = lvb + 5 * nt;                      // [R][nt]  −l
+    T* siu = stl + R * nt;                      // [R][nt]  1/u
+    T* ste = siu + R * nt;                      // [R][nt]  −e
+    const int b = blockIdx.y;
+    const int nx = a.nx, m = nx - 2;
+    const int nwarps = nt >> 5;
+    const int c0 = t * R;
+    const int lane = t & 31, warp = t >> 5;
+    T aexf, aexb;
+    {
+        const T* tab = static_cast<const T*>(a.tab) + b * 3 * a.tpitch;
+        T Af = (T)1, Ab = (T)1;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int c = c0 + k;
+            const bool ok = c >= 1 && c <= m;
+            const T l = ok ? -tab[c - 1] : (T)0;
+            const T e = ok ? -tab[2 * a.tpitch + c - 1] : (T)0;
+            stl[k * nt + t] = l;
+            siu[k * nt + t] = ok ? tab[a.tpitch + c - 1] : (T)0;
+            ste[k * nt + t] = e;
+            Af = Af * l;
+            Ab = Ab * e;
+        }
+        int lv = 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1, ++lv) {
+            const T Au = __shfl_up_sync(0xffffffffu, Af, off);
+            const T Ad = __shfl_down_sync(0xffffffffu, Ab, off);
+            lvf[lv * nt + t] = (lane >= off) ? Af : (T)0;
+            lvb[lv * nt + t] = (lane + off < 32) ? Ab : (T)0;
+            if (lane >= off) Af = Af * Au;
+            if (lane + off < 32) Ab = Ab * Ad;
+        }
+        aexf = __shfl_up_sync(0xffffffffu, Af, 1);
+        aexb = __shfl_down_sync(0xffffffffu, Ab, 1);
+        if (lane == 0) aexf = (T)1;
+        if (lane == 31) aexb = (T)1;
+        if (lane == 31) fwa[warp] = Af;
+        if (lane == 0) bwa[warp] = Ab;
+        __syncthreads();
+        if (warp == 0) {
+            T A = (lane < nwarps) ? fwa[lane] : (T)1;
+            T B = (lane < nwarps) ? bwa[lane] : (T)1;
+            int l2 = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++l2) {
+                const T Au = __shfl_up_sync(0xffffffffu, A, off);
+                const T Bd = __shfl_down_sync(0xffffffffu, B, off);
+                fxa[l2][lane] = (lane >= off) ? A : (T)0;
+                bxa[l2][lane] = (lane + off < 32) ? B : (T)0;
+                if (lane >= off) A = A * Au;
+                if (lane + off < 32) B = B * Bd;
+            }
+        }
+        __syncthreads();
+    }
+    const T sc = (T)a.scale;
+    const T* srcb = static_cast<const T*>(a.src) + b * a.mstride;
+    T* dstb = static_cast<T*>(a.dst) + b * a.mstride;
+    const int G = gridDim.x;
+    int line = blockIdx.x;
+    T nA[R], nB[R];
+    auto fetch = [&](int l0, T (&x)[R], T (&y)[R]) {
+        if (l0 < a.nrows) load_span<T, R>(srcb + int64_t(a.row0 + l0) * a.pitch, c0, nx, x);
+        if (l0 + G < a.nrows) load_span<T, R>(srcb + int64_t(a.row0 + l0 + G) * a.pitch, c0, nx, y);
+        else {
+#pragma unroll
+            for (int k = 0; k < R; ++k) y[k] = (T)0;
+        }
+    };
+    fetch(line, nA, nB);
+    for (; line < a.nrows; line += 2 * G) {
+        const bool hasB = line + G < a.nrows;
+        T dA[R], dB[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            dA[k] = sc * nA[k];
+            dB[k] = sc * nB[k];
+        }
+        fetch(line + 2 * G, nA, nB);
+        // forward y_c = d_c − l_c y_{c−1}
+        T vA = (T)0, vB = (T)0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const T l = stl[k * nt + t];
+            vA = fmaT(l, vA, dA[k]);
+            vB = fmaT(l, vB, dB[k]);
+            dA[k] = vA;
+            dB[k] = vB;
+        }
+        {
+            int lv = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++lv) {
+                const T f = lvf[lv * nt + t];
+                const T uA = __shfl_up_sync(0xffffffffu, vA, off), uB = __shfl_up_sync(0xffffffffu, vB, off);
+                vA = fmaT(f, uA, vA);
+                vB = fmaT(f, uB, vB);
+            }
+        }
+        T xA = __shfl_up_sync(0xffffffffu, vA, 1), xB = __shfl_up_sync(0xffffffffu, vB, 1);
+        if (lane == 0) {
+            xA = (T)0;
+            xB = (T)0;
+        }
+        if (lane == 31) {
+            fwv[0][warp] = vA;
+            fwv[1][warp] = vB;
+        }
+        __syncthreads();
+        if (warp < 2) {   // warp 0: row A, warp 1: row B
+            T V = (lane < nwarps) ? fwv[warp][lane] : (T)0;
+            int l2 = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++l2) V = fmaT(fxa[l2][lane], __shfl_up_sync(0xffffffffu, V, off), V);
+            const T Vx = __shfl_up_sync(0xffffffffu, V, 1);
+            if (lane < nwarps) fwc[warp][lane] = (lane == 0) ? (T)0 : Vx;
+        }
+        __syncthreads();
+        {
+            const T cA = fmaT(aexf, fwc[0][warp], xA), cB = fmaT(aexf, fwc[1][warp], xB);
+            T pi = (T)1;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                pi = pi * stl[k * nt + t];
+                dA[k] = fmaT(pi, cA, dA[k]);
+                dB[k] = fmaT(pi, cB, dB[k]);
+            }
+        }
+        // backward x_c = y_c/u_c − e_c x_{c+1}
+        vA = (T)0;
+        vB = (T)0;
+#pragma unroll
+        for (int k = R - 1; k >= 0; --k) {
+            const T e = ste[k * nt + t], iu = siu[k * nt + t];
+            vA = fmaT(e, vA, dA[k] * iu);
+            vB = fmaT(e, vB, dB[k] * iu);
+            dA[k] = vA;
+            dB[k] = vB;
+        }
+        {
+            int lv = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++lv) {
+                const T f = lvb[lv * nt + t];
+                const T uA = __shfl_down_sync(0xffffffffu, vA, off), uB = __shfl_down_sync(0xffffffffu, vB, off);
+                vA = fmaT(f, uA, vA);
+                vB = fmaT(f, uB, vB);
+            }
+        }
+        xA = __shfl_down_sync(0xffffffffu, vA, 1);
+        xB = __shfl_down_sync(0xffffffffu, vB, 1);
+        if (lane == 31) {
+            xA = (T)0;
+            xB = (T)0;
+        }
+        if (lane == 0) {
+            bwv[0][warp] = vA;
+            bwv[1][warp] = vB;
+        }
+        __syncthreads();
+        if (warp < 2) {
+            T V = (lane < nwarps) ? bwv[warp][lane] : (T)0;
+            int l2 = 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1, ++l2) V = fmaT(bxa[l2][lane], __shfl_down_sync(0xffffffffu, V, off), V);
+            const T Vx = __shfl_down_sync(0xffffffffu, V, 1);
+            if (lane < nwarps) bwc[warp][lane] = (lane == nwarps - 1) ? (T)0 : Vx;
+        }
+        __syncthreads();
+        {
+            const T cA = fmaT(aexb, bwc[0][warp], xA), cB = fmaT(aexb, bwc[1][warp], xB);
+            T pi = (T)1;
+#pragma unroll
+            for (int k = R - 1; k >= 0; --k) {
+                pi = pi * ste[k * nt + t];
+                dA[k] = fmaT(pi, cA, dA[k]);
+                dB[k] = fmaT(pi, cB, dB[k]);
+            }
+        }
+        store_span<T, R>(dstb + int64_t(a.row0 + line) * a.pitch, c0, 1, nx - 1, dA);
+        if (hasB) store_span<T, R>(dstb + int64_t(a.row0 + line + G) * a.pitch, c0, 1, nx - 1, dB);
+    }
+}
+
 struct ImpYArgs {
     const void* z;     // x-solve output (field layout, view rows)
     void* prev;        // u^{n−1} (MODE 0) or u₁ (MODE 1); overwritten by u^{n+1}

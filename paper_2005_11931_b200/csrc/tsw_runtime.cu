@@ -216,6 +216,7 @@ struct tsw_ctx {
     void* imp_s1 = nullptr;   // implicit: x-solve output (field layout)
     void* imp_t = nullptr;    // implicit: transposed field [B][nx][pt]
     int64_t imp_pt = 0;       // its pitch (≥ ny, multiple of 32)
+    int imp_x2 = 0;           // x solve: one row per iteration (0, default) or two (1; measured slower)
     int imp_solver = 0;       // 0 auto, 1 cyclic reduction (the paper's), 2 streaming scans, 3 cluster scans (R28)
     void* imp_tab = nullptr;  // x-line LU tables [B][3][imp_tpitch] (scan solver)
     int64_t imp_tpitch = 0;
@@ -320,6 +321,17 @@ template <typename T, int R>
 tsw_status launch_imp_x(tsw_ctx* c, const ImpXArgs& ax) {
     const int threads = int(round_up((c->g.nx + R - 1) / R, 32));
     if (threads > 1024) return fail(TSW_ERR_ARG, "implicit x solver: row too long");
+    if (c->imp_x2) {   // two rows per iteration, tables in shared memory
+        const size_t smem2 = size_t(10 + 3 * R) * threads * sizeof(T);
+        if (smem2 <= size_t(227) * 1024) {
+            CK(cudaFuncSetAttribute(k_imp_x2<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+            const int64_t want = (int64_t(c->sm_count) + c->g.batch - 1) / c->g.batch;
+            const unsigned gx = unsigned(std::max<int64_t>(1, std::min<int64_t>((ax.nrows + 1) / 2, want)));
+            k_imp_x2<T, R><<<dim3(gx, unsigned(c->g.batch)), threads, smem2, c->stream>>>(ax);
+            CKL();
+            return TSW_OK;
+        }
+    }
     const size_t smem = size_t(10) * threads * sizeof(T);
     CK(cudaFuncSetAttribute(k_imp_x<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
@@ -2392,6 +2404,11 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         tsw_status st = set_dev(c);
         if (st) return st;
         return guard_fill(c);
+    }
+    if (key == TSW_OPT_IMPLICIT_XROWS) {
+        if (value != 1 && value != 2) return fail(TSW_ERR_ARG, "implicit x-solve rows per iteration must be 1 or 2");
+        c->imp_x2 = (value == 2) ? 1 : 0;
+        return TSW_OK;
     }
     if (key == TSW_OPT_IMPLICIT_SOLVER) {
         if (value < 0 || value > 3)

@@ -85,6 +85,22 @@ def test_implicit_2d_vs_oracle(shape, solver):
     s.close()
 
 
+@pytest.mark.parametrize("xrows", [1, 2])
+@pytest.mark.parametrize("shape", [(257, 300), (40, 1500), (9, 5000)])
+def test_implicit_x_rows_per_iteration(shape, xrows):
+    """The x-line solve with one and two rows per iteration (odd and even row counts per CTA)."""
+    ny, nx = shape
+    cfg = inputs.config(3, nx=nx, ny=ny, dx=0.02, dy=0.02, eps=[0.1], amp=[1.0], dt=0.02)
+    s = _implicit_solver(cfg)
+    s.set_option(tsw.TSW_OPT_IMPLICIT_XROWS, xrows)
+    u0 = inputs.uniform_dense((ny, nx), seed=9)
+    s.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    s.step(10)
+    on = _oracle_2d(s, cfg, u0, None, 10, "f64")[0]
+    assert rel_maxnorm(s.read(0)[0], on) < 1e-11
+    s.close()
+
+
 @pytest.mark.parametrize("solver", ["scan", "cr", "stream"])
 def test_implicit_2d_f32(solver):
     cfg = inputs.config(3, nx=515, ny=260, dx=0.02, dy=0.02, eps=[0.1], amp=[1.0], dt=0.02)

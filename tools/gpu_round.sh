@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_implicit_gpu.py tests/test_guards_gpu.py -q -x --timeout 120 -p no:cacheprovider > gpurun_out/pytest_imp.log 2>&1; echo pytest_exit=$?
+timeout 600 python -m pytest tests/test_implicit_gpu.py -q -x --timeout 120 -p no:cacheprovider > gpurun_out/pytest_imp.log 2>&1; echo pytest_exit=$?
 tail -2 gpurun_out/pytest_imp.log; grep -E "^E  " gpurun_out/pytest_imp.log | head -5
-timeout 300 python bench.py --workload table1 --steps 100 > gpurun_out/bench_table1_f64.json 2> gpurun_out/bench_table1.err; echo t1=$?
-timeout 300 python bench.py --workload table1 --steps 100 --dtype f32 --no-cpu-baseline > gpurun_out/bench_table1_f32.json 2>> gpurun_out/bench_table1.err; echo t1f32=$?
+for xr in 1 2 1 2; do timeout 120 python tools/table1.py --sizes 4096 --xrows $xr 2>&1 | cut -c1-140; done

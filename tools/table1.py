@@ -22,7 +22,7 @@ PAPER_GPU_S = {256: 0.88, 512: 2.07, 1024: 7.16, 2048: 20.30, 4096: 62.76}
 PAPER_CPU_S = {256: 0.91, 512: 3.73, 1024: 15.92, 2048: 64.8, 4096: 280.54}
 
 
-def run(n, dtype, steps, reps, solver=0):
+def run(n, dtype, steps, reps, solver=0, xrows=1):
     sc = inputs.paper_2d(dx=100.0 / (n - 1))
     assert sc.nx == n and sc.ny == n, (sc.nx, sc.ny)
     stream = torch.cuda.Stream()
@@ -30,6 +30,7 @@ def run(n, dtype, steps, reps, solver=0):
     s.set_coeff_profile(sc.seg_value, sc.seg_break, [0.8], isotropic=True)
     s.set_option(tsw.TSW_OPT_SCHEME, 1)
     s.set_option(tsw.TSW_OPT_IMPLICIT_SOLVER, solver)
+    s.set_option(tsw.TSW_OPT_IMPLICIT_XROWS, xrows)
     u0 = sc.initial().astype(np.float64 if dtype == "f64" else np.float32)[None]
     u0d = torch.from_numpy(u0).cuda()
     best = None
@@ -57,13 +58,14 @@ def main():
     ap.add_argument("--dtypes", default="f64,f32")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--xrows", type=int, default=1)
     ap.add_argument("--solver", type=int, default=0, help="TSW_OPT_IMPLICIT_SOLVER (0 cluster scans, 1 CR, 2 streaming scans)")
     args = ap.parse_args()
     for dtype in args.dtypes.split(","):
         for n in [int(x) for x in args.sizes.split(",")]:
-            ms, launches, umax = run(n, dtype, args.steps, args.reps, args.solver)
+            ms, launches, umax = run(n, dtype, args.steps, args.reps, args.solver, args.xrows)
             esz = 8 if dtype == "f64" else 4
-            line = {"workload": f"table1_implicit_{n}x{n}", "dtype": dtype, "solver": args.solver, "steps": args.steps, "ms": ms,
+            line = {"workload": f"table1_implicit_{n}x{n}", "dtype": dtype, "solver": args.solver, "xrows": args.xrows, "steps": args.steps, "ms": ms,
                     "mpts": n * n * args.steps / (ms * 1e-3) / 1e6, "launches": launches, "max_abs_u": umax,
                     "paper_gpu_s": PAPER_GPU_S.get(n), "paper_cpu_s": PAPER_CPU_S.get(n),
                     "speedup_vs_paper_gpu": (PAPER_GPU_S[n] * 1e3 / ms) if n in PAPER_GPU_S else None,
