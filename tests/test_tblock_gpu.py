@@ -133,3 +133,21 @@ def test_concurrent_contexts_do_not_interfere():
         assert np.array_equal(s.read(0), ref), f"iteration {it}"
         s.close()
         busy.close()
+
+
+@pytest.mark.parametrize("K", [2, 4, 8])
+@pytest.mark.parametrize("shape", [(3, 3), (4, 5), (5, 67), (6, 2000)])
+def test_tblock_degenerate_grids(K, shape):
+    """One interior node, a single interior row or column, a strip narrower than the halo: the
+    temporally blocked path ≡ the one-level path, bitwise; step(0) changes nothing."""
+    ny, nx = shape
+    cfg = inputs.config(3, nx=nx, ny=ny, dx=0.05, dy=0.05, eps=[0.2], amp=[1.0], dt=0.005)
+    u0 = inputs.uniform_dense((ny, nx), seed=13)
+    ref = _run(cfg, "f64", 1, 2 * K + 3, u0)
+    s = _run(cfg, "f64", K, 2 * K + 3, u0)
+    before = s.read(0)
+    s.step(0)
+    assert np.array_equal(s.read(0), before)
+    assert np.array_equal(before, ref.read(0)) and np.array_equal(s.read(1), ref.read(1))
+    s.close()
+    ref.close()
