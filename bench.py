@@ -582,6 +582,11 @@ def main():
                                               "peak = 64 (fp64) / 128 (fp32) ops/clk/SM x 148 SMs x median SM clock"}},
             "gpu_launches": main_res["launches"],
             "clocks": main_res["clocks"],
+            "context": {"paper_table1": "implicit cyclic-reduction scheme (a different algorithm), 4096^2, 100 steps: "
+                                        "62.76 s on an NVIDIA GeForce RTX 2080 Ti vs 280.54 s serial on an Intel Core "
+                                        "i7-9800X (speedup 4.47, P:1168-1183); this repo's implicit path: "
+                                        "bench.py --workload table1",
+                        "note": "context only, not a target (BASELINE.md section 2)"},
         }
         if "e2e" in main_res:
             line["e2e"] = main_res["e2e"]
