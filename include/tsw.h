@@ -235,6 +235,9 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               0 (default): auto — 2 for fp64 grids of ≥ 8 M nodes, else 3.
                               1: cyclic reduction per line in shared memory with tiled transposes
                               (the paper's solver), ≤ 4095 (fp64) / 8191 (fp32) unknowns per line. */
+#define TSW_OPT_TB_WARPS 13 /* CTA width of the temporally blocked stencil: 8 warps (512-column strips), 4
+                              (256-column strips: less redundant halo work on narrow grids), 0 (default):
+                              4 for rows of ≤ 4096 columns, else 8 */
 #define TSW_OPT_IMPLICIT_XROWS 12 /* rows per iteration of the implicit x-line solve: 1 (default; LU tables
                               in registers) or 2 (the two rows' scan chains interleave, tables in shared
                               memory — measured 4 % slower at 4096², kept for comparison) */

@@ -485,10 +485,10 @@ constexpr int TB_NC = 8;
 // ghost rows per side of a slab: the deepest temporal blocking (K = 8) exchanges 8 rows every 8 levels
 constexpr int TSW_MAX_GHOST = 8;
 
-template <typename T, int K>
+template <typename T, int K, int NC = TB_NC>
 struct TbGeom {
     static constexpr int V = 2;                                  // columns per thread
-    static constexpr int NT = TB_NC * 32;
+    static constexpr int NT = NC * 32;
     static constexpr int A = (16 / int(sizeof(T))) > V ? (16 / int(sizeof(T))) : V;  // 16-byte TMA alignment
     static constexpr int H = ((K + A - 1) / A) * A;              // halo columns per side (≥ K)
     static constexpr int WE = NT * V;                            // 512 columns
@@ -562,12 +562,12 @@ template <typename T> struct TbYCache {
     static constexpr bool smem = sizeof(T) == 8 && TSW_TB_YCACHE_SMEM;     // shared memory
 };
 
-template <typename T, int K>
+template <typename T, int K, int NC = TB_NC>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
-    return size_t(depth) * 2 * TbGeom<T, K>::WE * sizeof(T) +
-           size_t(K) * 2 * (TbGeom<T, K>::WE + 2 * TbPad<T>::P) * sizeof(T) +
+    return size_t(depth) * 2 * TbGeom<T, K, NC>::WE * sizeof(T) +
+           size_t(K) * 2 * (TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P) * sizeof(T) +
            (size_t(depth) * sizeof(uint64_t) + 15) / 16 * 16 +
-           (TbYCache<T>::smem ? size_t(K + 1) * TbGeom<T, K>::NT * TbGeom<T, K>::V * sizeof(T) : 0);
+           (TbYCache<T>::smem ? size_t(K + 1) * TbGeom<T, K, NC>::NT * TbGeom<T, K, NC>::V * sizeof(T) : 0);
 }
 
 // Per-thread state of one item's wavefront.  Window slots rotate with the row phase PH ∈ {0,1,2}:
@@ -589,12 +589,12 @@ struct TbState {
 // One input row of the wavefront.  `cr` / `cw`: this thread's element in the centre-row buffers
 // of the previous / current row parity (level m at offset m·2·WEP).  MASKED: force the Dirichlet
 // rows/columns to +0 (only items whose dependency cone touches them need it).
-template <typename T, int K, int PH, bool MASKED>
+template <typename T, int K, int PH, bool MASKED, int NC>
 __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
                                        int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
                                        T* __restrict__ yc) {
     constexpr int V = 2;
-    constexpr int WEP = TbGeom<T, K>::WE + 2 * TbPad<T>::P;
+    constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
     constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
     // level 0
 #pragma unroll
@@ -618,7 +618,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
         bool rowok = true;
         if (MASKED) rowok = unsigned(R - m - rowlo) <= unsigned(rowhi - rowlo);
         T gdv[V], guv[V];
-        if (TbYCache<T>::smem) lds_v2(yc + m * TbGeom<T, K>::NT * V, gdv);
+        if (TbYCache<T>::smem) lds_v2(yc + m * TbGeom<T, K, NC>::NT * V, gdv);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const T cu = S.w[m - 1][N][k];
@@ -644,7 +644,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
                 nv[k] = v;
             }
         }
-        if (TbYCache<T>::smem) sts_v2(yc + m * TbGeom<T, K>::NT * V, guv);
+        if (TbYCache<T>::smem) sts_v2(yc + m * TbGeom<T, K, NC>::NT * V, guv);
         if (m < K) {
 #pragma unroll
             for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
@@ -661,9 +661,9 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
 // The producer is thread 0: after every second input row it refills the two stages consumed by
 // the previous rows (every thread has passed the per-row barrier, so they are free) with the next
 // stages of its stream (needs a ring of ≥ 3 stages).
-template <typename T, int K, bool PEER = false>
-__global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, int depth) {
-    using G = TbGeom<T, K>;
+template <typename T, int K, bool PEER = false, int NC = TB_NC>
+__global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> a, int depth) {
+    using G = TbGeom<T, K, NC>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
     constexpr int PAD = TbPad<T>::P, WEP = WE + 2 * PAD;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(TB_NC * 32, 2) k_step2d_tb(const TbArgs<T> a, 
             const int par = R & 1;
             T* cw = cen + par * WEP + e0;
             const T* cr = cen + (par ^ 1) * WEP + e0;
-            tb_row<T, K, PH, MASKED>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache);
+            tb_row<T, K, PH, MASKED, NC>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
                 // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH

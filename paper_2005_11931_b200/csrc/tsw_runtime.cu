@@ -227,7 +227,8 @@ struct tsw_ctx {
     void* imp_ccon = nullptr;   //   βz₁, A₂' [B][2][ncolp]
     bool imp_ycol_stale = true;
     int tb_depth = 4;     // its input ring stages
-    int tb_occ[2][9] = {};  // [f64][K] resident CTAs per SM (cached)
+    int tb_occ[2][9][2] = {};  // [f64][K][8 warps] resident CTAs per SM (cached)
+    int tb_warps = 0;          // CTA width of the temporally blocked stencil: 0 auto, 4 or 8 warps
     int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
     int bulk_occ_key[2][2] = {{0, 0}, {0, 0}};
     int step_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};  // [mode][start]
@@ -688,20 +689,19 @@ bool has_nb(const tsw_ctx* c, int side) { return side == 0 ? c->g.rank > 0 : c->
 bool peer_mode(const tsw_ctx* c) { return c->g.nranks > 1 && c->g.dim == 2 && c->halo_mode == 1; }
 
 // ---- temporally blocked pass: K levels, (buf[ic], buf[ip]) → (buf[fk], buf[fkm1]) -----------
-template <typename T, int K>
-tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
-    if (s_hi <= s_lo) return TSW_OK;
-    using G = TbGeom<T, K>;
+template <typename T, int K, int NC>
+tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
+    using G = TbGeom<T, K, NC>;
     const int depth = c->tb_depth;
-    const size_t smem = tb_smem_bytes<T, K>(depth);
+    const size_t smem = tb_smem_bytes<T, K, NC>(depth);
     const bool peer = peer_mode(c);
-    int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K];
+    int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K][NC == 8 ? 1 : 0];
     if (occ == 0) {
-        for (auto fn : {k_step2d_tb<T, K, false>, k_step2d_tb<T, K, true>}) {
+        for (auto fn : {k_step2d_tb<T, K, false, NC>, k_step2d_tb<T, K, true, NC>}) {
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         }
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K, false>, TB_NC * 32, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K, false, NC>, NC * 32, smem));
         if (occ < 1) return fail(TSW_ERR_ARG, "temporally blocked stencil (K=%d) does not fit on an SM", K);
     }
     TbArgs<T> a;
@@ -754,9 +754,9 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi)
         CK(cudaEventRecord(e0, c->stream));
     }
     if (peer)
-        k_step2d_tb<T, K, true><<<unsigned(blocks), TB_NC * 32, smem, c->stream>>>(a, depth);
+        k_step2d_tb<T, K, true, NC><<<unsigned(blocks), NC * 32, smem, c->stream>>>(a, depth);
     else
-        k_step2d_tb<T, K, false><<<unsigned(blocks), TB_NC * 32, smem, c->stream>>>(a, depth);
+        k_step2d_tb<T, K, false, NC><<<unsigned(blocks), NC * 32, smem, c->stream>>>(a, depth);
     CKL();
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
@@ -765,6 +765,21 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi)
     }
     c->launches++;
     return TSW_OK;
+}
+
+// CTA width: 8 warps (512-column strips) or 4 (256-column strips).  Auto (TSW_OPT_TB_WARPS = 0):
+// 4 warps only where its strips compute ≥ 5 % fewer columns (narrow grids, e.g. config 5's 2048:
+// +12 % fp64, +17 % fp32 measured; at 4096 columns 8 warps are as fast or faster)
+template <typename T, int K>
+tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
+    if (s_hi <= s_lo) return TSW_OK;
+    int nc = c->tb_warps;
+    if (!nc) {
+        const int64_t cols8 = (c->pitch + TbGeom<T, K, 8>::WO - 1) / TbGeom<T, K, 8>::WO * TbGeom<T, K, 8>::WE;
+        const int64_t cols4 = (c->pitch + TbGeom<T, K, 4>::WO - 1) / TbGeom<T, K, 4>::WO * TbGeom<T, K, 4>::WE;
+        nc = (double(cols4) < 0.95 * double(cols8)) ? 4 : 8;
+    }
+    return nc == 4 ? launch_tb_nc<T, K, 4>(c, fk, fkm1, s_lo, s_hi) : launch_tb_nc<T, K, 8>(c, fk, fkm1, s_lo, s_hi);
 }
 
 template <typename T>
@@ -2427,7 +2442,13 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         if (value < 3 || value > 16) return fail(TSW_ERR_ARG, "TB ring depth must be in [3, 16]");
         c->tb_depth = int(value);
         for (auto& r : c->tb_occ)
-            for (int& o : r) o = 0;
+            for (auto& q : r)
+                for (int& o : q) o = 0;
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_TB_WARPS) {
+        if (value != 0 && value != 4 && value != 8) return fail(TSW_ERR_ARG, "TB CTA width must be 0 (auto), 4 or 8 warps");
+        c->tb_warps = int(value);
         return TSW_OK;
     }
     if (key == TSW_OPT_ROWS_PER_ITEM) {

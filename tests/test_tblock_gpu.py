@@ -151,3 +151,21 @@ def test_tblock_degenerate_grids(K, shape):
     assert np.array_equal(before, ref.read(0)) and np.array_equal(s.read(1), ref.read(1))
     s.close()
     ref.close()
+
+
+@pytest.mark.parametrize("warps", [4, 8])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_tblock_cta_width_bitwise(warps, dtype):
+    """Both CTA widths of the temporally blocked stencil (TSW_OPT_TB_WARPS) ≡ the one-level path."""
+    cfg = inputs.config(3, nx=2049, ny=97, dx=0.01, dy=0.01, eps=[0.1, 0.3], amp=[1.0, 2.0], dt=2e-3)
+    u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(NP[dtype])
+    K = 4 if dtype == "f64" else 8
+    ref = _run(cfg, dtype, 1, 3 * K + 2, u0)
+    s = tsw.Solver.from_config(cfg, dtype)
+    s.set_option(tsw.TSW_OPT_TBLOCK, K)
+    s.set_option(tsw.TSW_OPT_TB_WARPS, warps)
+    s.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    s.step(3 * K + 2)
+    assert np.array_equal(s.read(0), ref.read(0)) and np.array_equal(s.read(1), ref.read(1))
+    s.close()
+    ref.close()
