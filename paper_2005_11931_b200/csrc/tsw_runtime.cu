@@ -915,10 +915,21 @@ tsw_status tb_pass(tsw_ctx* c) {
     if (c->g.nranks == 1) {
         if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
     } else if (peer_mode(c)) {
-        // one launch; the kernel itself stores the boundary rows into the neighbours' ghost rows
+        // the kernel itself stores the boundary rows into the neighbours' ghost rows.  With a slab
+        // of ≥ 3K rows the first / last K rows go first and the epoch is published before the
+        // interior rows: those read no ghost rows, so the neighbours' next pass may start (and push
+        // into the other buffer pair's ghost rows) while the interior is still running
+        const TbSplit p = tb_split(c);
         if ((st = peer_begin(c, c->stream))) return st;
-        if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
-        if ((st = peer_end(c, c->stream))) return st;
+        if (p.split) {
+            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi))) return st;
+            if ((st = launch_tb_rows(c, fk, fkm1, p.bot_lo, p.bot_hi))) return st;
+            if ((st = peer_end(c, c->stream))) return st;
+            if ((st = launch_tb_rows(c, fk, fkm1, p.ilo, p.ihi))) return st;
+        } else {
+            if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
+            if ((st = peer_end(c, c->stream))) return st;
+        }
         c->gdepth[fk] = c->gdepth[fkm1] = K;
     } else {
         const TbSplit p = tb_split(c);
