@@ -29,24 +29,33 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libtsw.so if any source is newer than it.  Returns its path."""
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines: tuple = ()) -> str:
+    """Compile libtsw.so if any source is newer than it.  Returns its path.
+
+    `out` / `defines` build an alternative library (e.g. `-DTSW_TB_F32X2=0`) for A/B timing
+    through the TSW_LIB override; the default build is the product.
+    """
+    if not force and os.path.exists(out):
+        t = os.path.getmtime(out)
         if all(os.path.getmtime(d) <= t for d in DEPS):
-            return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SRC, "-ldl"]
+            return out
+    cmd = [nvcc(), *NVCC_FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp", *SRC, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libtsw.so")
-    with open(os.path.join(PKG, "build_ptxas.log"), "w") as f:
-        f.write(r.stderr)
+    if out == LIB:
+        with open(os.path.join(PKG, "build_ptxas.log"), "w") as f:
+            f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    # python -m paper_2005_11931_b200.build [--force] [--verbose] [--out PATH] [-DNAME=V ...]
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else LIB
+    print(build(force="--force" in argv, verbose="--verbose" in argv, out=out,
+                defines=tuple(a for a in argv if a.startswith("-D"))))

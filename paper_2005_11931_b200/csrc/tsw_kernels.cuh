@@ -287,6 +287,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// one lane of the (fully active) warp returns true
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 constexpr int TMA_NC = 8;  // consumer warps per CTA (+1 producer warp)
 
 template <typename T>
@@ -562,6 +573,14 @@ template <typename T> struct TbYCache {
     static constexpr bool smem = sizeof(T) == 8 && TSW_TB_YCACHE_SMEM;     // shared memory
 };
 
+// TSW_TB_WAIT1=1: only thread 0 waits on a stage's "full" mbarrier, before the per-row CTA barrier
+// (the others see the stage through that barrier).  Measured 5 % slower than every warp waiting
+// after the barrier (f64 K = 4: 655 vs 693 Gpt/s; f32 K = 8: 1234 vs 1293): the waits of the 8
+// warps overlap, a single waiter's ≈ 90-cycle try_wait is serialised in front of the barrier.
+#ifndef TSW_TB_WAIT1
+#define TSW_TB_WAIT1 0
+#endif
+
 template <typename T, int K, int NC = TB_NC>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
     return size_t(depth) * 2 * TbGeom<T, K, NC>::WE * sizeof(T) +
@@ -695,38 +714,44 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         in_hi = min(s1 + K, a.smax + 1);
     };
 
-    // ---- producer state (thread 0): the stream of (item, input row) stages ----
+    // ---- producer state: the stream of (item, input row) stages.  Every thread tracks it (the
+    // values are CTA-uniform, so they live in uniform registers); one elected lane of a rotating
+    // warp issues each refill, so no warp carries the producer's instructions on every row.
     int64_t p_item = blockIdx.x;
-    int p_R = 0, p_hi = 0, p_b = 0, p_slot = 0;
-    int64_t p_cs = 0;
-    if (tid == 0 && p_item < a.items) {
-        int s0, s1;
-        geom(p_item, p_cs, s0, s1, p_b, p_R, p_hi);
-    }
-    auto produce = [&]() {  // thread 0 only
+    int p_R = 0, p_hi = 0, p_slot = 0;
+    int64_t p_e = 0;            // element offset of the next stage's rows in u^n and u^{n−1}
+    auto p_start = [&]() {
+        int64_t cs;
+        int s0, s1, b;
+        geom(p_item, cs, s0, s1, b, p_R, p_hi);
+        p_e = b * a.mstride + int64_t(p_R) * a.pitch + cs - H;
+    };
+    if (p_item < a.items) p_start();
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform by construction
+    auto produce = [&](bool issue) {
         if (p_item >= a.items) return;
-        T* st = ring + size_t(p_slot) * 2 * WE;
-        mbar_arrive_expect_tx(&full[p_slot], 2 * WE * sizeof(T));
-        bulk_g2s(st, a.un + p_b * a.mstride + p_R * a.pitch + p_cs - H, WE * sizeof(T), &full[p_slot]);
-        bulk_g2s(st + WE, a.unm1 + p_b * a.mstride + p_R * a.pitch + p_cs - H, WE * sizeof(T), &full[p_slot]);
+        if (issue && elect_one()) {
+            T* st = ring + size_t(p_slot) * 2 * WE;
+            mbar_arrive_expect_tx(&full[p_slot], 2 * WE * sizeof(T));
+            bulk_g2s(st, a.un + p_e, WE * sizeof(T), &full[p_slot]);
+            bulk_g2s(st + WE, a.unm1 + p_e, WE * sizeof(T), &full[p_slot]);
+        }
         if (++p_slot == depth) p_slot = 0;
+        p_e += a.pitch;
         if (++p_R == p_hi) {
             p_item += gridDim.x;
-            if (p_item < a.items) {
-                int s0, s1;
-                geom(p_item, p_cs, s0, s1, p_b, p_R, p_hi);
-            }
+            if (p_item < a.items) p_start();
         }
     };
-    if (tid == 0)
-        for (int k = 0; k < depth; ++k) produce();
+    for (int k = 0; k < depth; ++k) produce(warp == 0);
+    int rot = 0;  // the warp that issues the next refill
 
     const int e0 = tid * V;  // my first column of the extended strip
     // interior storage rows of the global grid: g ∈ [1, ny−2] ⇔ storage s ∈ [rowlo, rowhi]
     const int rowlo = int(1 - a.r0 + 1), rowhi = int(a.ny - 2 - a.r0 + 1);
     int cslot = 0;
     uint32_t cphase = 0;
-    int pending = 0;  // stages consumed but not yet refilled (thread 0's count is the one used)
+    int pending = 0;  // the previous row consumed a stage that is not yet refilled
     TbState<T, K> S;
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
         int64_t cs;
@@ -778,19 +803,20 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             constexpr int PH = decltype(ph)::value;
             constexpr bool MASKED = decltype(msk)::value;
             const int R = in_lo + i;
+            if (TSW_TB_WAIT1 && tid == 0 && i < nload) mbar_wait(&full[cslot], cphase);
             __syncthreads();  // the previous rows' stages and centre rows are consumed / published
-            // refill the consumed stages two at a time (their shared-memory reads completed before
-            // this barrier: the values were used in the previous rows' arithmetic)
-            if (tid == 0 && pending >= 2) {
-                produce();
-                produce();
+            // refill the stage consumed by the previous row (its shared-memory reads completed
+            // before this barrier: the values were used in that row's arithmetic)
+            if (pending) {
+                produce(warp == rot);
+                if (++rot == NC) rot = 0;
                 pending = 0;
             }
             T nw[V], pv_new[V];
             const bool refill = (i < nload);
-            pending += refill ? 1 : 0;
+            pending = refill ? 1 : 0;
             if (refill) {
-                mbar_wait(&full[cslot], cphase);
+                if (!TSW_TB_WAIT1) mbar_wait(&full[cslot], cphase);
                 const T* st = ring + size_t(cslot) * 2 * WE;
                 lds_v2(st + e0, nw);
                 lds_v2(st + WE + e0, pv_new);
