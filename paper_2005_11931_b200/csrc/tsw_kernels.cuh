@@ -611,20 +611,27 @@ struct TbState {
 template <typename T, int K, int PH, bool MASKED, int NC>
 __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
                                        int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
-                                       T* __restrict__ yc) {
+                                       T* __restrict__ yc, const T (&lr1)[2]) {
     constexpr int V = 2;
     constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
     constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
     // level 0
 #pragma unroll
     for (int k = 0; k < V; ++k) S.w[0][O][k] = nw[k];
-    sts_v2(cw, nw);
+    // left/right neighbours of level m−1's centre row (written in the previous row, other parity
+    // buffer): level 1's were loaded by the caller before the stage wait; level m+1's are loaded
+    // before level m's arithmetic and store, so no level waits on a shared-memory load
+    T left = lr1[0], right = lr1[1];
 #pragma unroll
     for (int m = 1; m <= K; ++m) {
         // level m−1 after its update: rows (r−1, r, r+1) in slots (C, N, O); level m−2: row r in C
-        const T* ce = cr + (m - 1) * 2 * WEP;
-        const T left = ce[-1];
-        const T right = ce[V];
+        T nleft = (T)0, nright = (T)0;
+        if (m < K) {
+            const T* cn = cr + m * 2 * WEP;
+            nleft = cn[-1];
+            nright = cn[V];
+        }
+        if (m == 1) sts_v2(cw, nw);
         // canonical tree with shared face fluxes:
         //   F_{i+1/2} = c1_{i+1/2}·(u_{i+1} − u_i) is node i's right and node i+1's left x-flux,
         //   G_{j+1/2} = c2·(u_{j+1} − u_j) is row j's upper and row j+1's lower y-flux
@@ -672,6 +679,8 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
 #pragma unroll
             for (int k = 0; k < V; ++k) lastk[k] = nv[k];
         }
+        left = nleft;
+        right = nright;
     }
 #pragma unroll
     for (int k = 0; k < V; ++k) S.pm1[k] = pv_new[k];
@@ -812,6 +821,10 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
                 if (++rot == NC) rot = 0;
                 pending = 0;
             }
+            const int par = R & 1;
+            T* cw = cen + par * WEP + e0;
+            const T* cr = cen + (par ^ 1) * WEP + e0;
+            const T lr1[V] = {cr[-1], cr[V]};  // level 1's left/right neighbours, before the stage wait
             T nw[V], pv_new[V];
             const bool refill = (i < nload);
             pending = refill ? 1 : 0;
@@ -829,10 +842,7 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
                 for (int k = 0; k < V; ++k) nw[k] = pv_new[k] = (T)0;
             }
             T lastk[V];
-            const int par = R & 1;
-            T* cw = cen + par * WEP + e0;
-            const T* cr = cen + (par ^ 1) * WEP + e0;
-            tb_row<T, K, PH, MASKED, NC>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache);
+            tb_row<T, K, PH, MASKED, NC>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
                 // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH
