@@ -7,8 +7,9 @@ GPU (global grid 32768 × 4096·N, dx = dy = 0.0025, ε = 0.05, dt = 4e−4), de
 data (SURVEY §8(d) data-independence guard), fp64 by default.  One "step" = one pass of the
 hot path over the slab: the leapfrog stencil (S3), the NCCL ghost-row exchange at N > 1 (S4),
 and the discrete-energy reduction every `--energy-every` steps (S5).  By default the stencil is
-temporally blocked (K levels per HBM pass — 4 in fp64, 8 in fp32 by default — with K-deep ghost
-rows exchanged every K levels on slabs); `--tblock 1` times the one-level-per-pass kernel.  Inputs (2 × 1.07 GB per
+temporally blocked (K = 8 levels per HBM pass in both precisions by default; a stepping call's
+remainder of r < K levels is one pass of depth r; K-deep ghost rows on slabs); `--tblock 1` times
+the one-level-per-pass kernel.  Inputs (2 × 1.07 GB per
 GPU in fp64) exceed the 126 MB L2, so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f64|f32] [--impl tsw|reference]
@@ -34,7 +35,26 @@ sys.path.insert(0, ROOT)
 METRIC = "2D stencil Gpoint-updates/s & HBM GB/s vs 8 TB/s peak, at 1/2/4/8 B200"
 UNIT = "Gpt/s"
 ESZ = {"f64": 8, "f32": 4}
-TB_DEFAULT = {"f64": 4, "f32": 8}   # levels per HBM pass (sweep optimum on B200, profiles/r01)
+TB_DEFAULT = {"f64": 8, "f32": 8}   # levels per HBM pass (sweep optimum on B200, profiles/r01)
+
+
+def words_per_update(steps: int, cadence: int, K: int) -> float:
+    """Algorithmic HBM words per point-update of the timed loop: a one-level step
+    moves 3 words per node (read u^n, u^{n-1}; write u^{n+1}), a temporally blocked pass of any
+    depth 4 (read u^n, u^{n-1}; write u^{n+K}, u^{n+K-1}).  A stepping call of q·K + r levels runs
+    q passes of depth K and, for r >= 2, one pass of depth r (r = 1: one level)."""
+    words = levels = 0
+    done = 0
+    while done < steps:
+        k = min(cadence, steps - done) if cadence > 0 else steps - done
+        if K <= 1:
+            words += 3 * k
+        else:
+            q, r = divmod(k, K)
+            words += 4 * (q + (1 if r >= 2 else 0)) + (3 if r == 1 else 0)
+        levels += k
+        done += k
+    return words / levels
 
 
 def host_cores() -> int:
@@ -50,6 +70,23 @@ def measured_peak():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _sm_max_mhz() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        return 1965.0   # B200 maximum SM clock
+
+
+SM_MAX_MHZ = _sm_max_mhz()
+
+
+def alu_peak(dtype: str) -> float:
+    """Non-FMA arithmetic roof in TFLOP/s: 64 fp64 / 128 fp32 lanes per clock per SM,
+    148 SMs, maximum SM clock."""
+    return (64.0 if dtype == "f64" else 128.0) * 148 * SM_MAX_MHZ * 1e6 / 1e12
 
 
 def ncu_traffic(dtype: str, workload: str, tblock: int = 1, kernel: str = ""):
@@ -544,14 +581,26 @@ def main():
         peak, peak_src = measured_peak()
         esz = ESZ[args.dtype]
         # algorithmic bytes per point-update: 3 words per step; with temporal
-        # blocking of depth K, (2 reads + 2 writes)/K words
-        words = 3.0 if tblock == 1 else 4.0 / tblock
+        # blocking, (2 reads + 2 writes) per pass (words_per_update)
+        words = words_per_update(args.steps, args.energy_every, tblock)
         upd_s = main_res["kernel_updates_per_launch"] / (main_res["kernel_avg_ms"] * 1e-3)
         achieved = upd_s * words * esz / 1e9
         wl = workload_name(cfg, world)
         traffic = ncu_traffic(args.dtype, wl, tblock)
-        clk = (main_res["clocks"] or {}).get("sm_mhz") or 1965.0
-        fp_peak = (64.0 if args.dtype == "f64" else 128.0) * 148 * clk * 1e6 / 1e12  # non-FMA ops/clk/SM
+        hbm_frac = achieved / peak
+        # ALU roof: 64 fp64 / 128 fp32 non-FMA lanes per clock per SM x 148 SMs at the
+        # maximum SM clock; 14 non-contracted operations per update (canonical tree)
+        fp_peak = alu_peak(args.dtype)
+        alu_ach = upd_s * 14 / 1e12
+        alu_frac = alu_ach / fp_peak
+        hbm_obj = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": hbm_frac,
+                   "traffic": traffic, "algorithmic_bytes_per_update": words * esz, "peak_source": peak_src}
+        alu_obj = {"bound": "alu", "achieved": alu_ach, "peak": fp_peak, "unit": "TFLOP/s", "frac": alu_frac,
+                   "traffic": traffic, "ops_per_update": 14,
+                   "peak_source": "derived (DESIGN.md section 6): %d %s lanes/clk/SM x 148 SMs x %.0f MHz" %
+                                  (64 if args.dtype == "f64" else 128, args.dtype, SM_MAX_MHZ)}
+        # the binding roof is the one the kernel is closer to; the other is reported beside it
+        roof, other_view = (alu_obj, hbm_obj) if alu_frac > hbm_frac else (hbm_obj, alu_obj)
         line = {
             "metric": METRIC, "value": main_res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": main_res["ms"] / args.steps, "higher_is_better": True,
@@ -569,17 +618,12 @@ def main():
                        "l2": "inputs exceed L2 (2 levels x %.2f GB per GPU), no flush" %
                              ((cfg.nx * (cfg.ny // world) * esz * cfg.batch) / 1e9)},
             "hbm_gbs_effective": main_res["value"] * words * esz,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic,
+            "roofline": {**roof,
                          "kernel": ("k_step2d_tma (S3 leapfrog, one level per pass)" if tblock == 1 else
                                     f"k_step2d_tb (S3 leapfrog, K={tblock} levels per HBM pass)"),
-                         "algorithmic_bytes_per_update": words * esz, "peak_source": peak_src,
                          "kernel_avg_ms": main_res["kernel_avg_ms"],
                          "per_step_roofline_gpts": peak / (3 * esz),
-                         "alu_view": {"unit": "TFLOP/s", "achieved": upd_s * 14 / 1e12, "peak": fp_peak,
-                                      "frac": upd_s * 14 / 1e12 / fp_peak,
-                                      "note": "14 non-contracted ops per update (canonical tree, no FMA); "
-                                              "peak = 64 (fp64) / 128 (fp32) ops/clk/SM x 148 SMs x median SM clock"}},
+                         ("alu_view" if roof is hbm_obj else "hbm_view"): other_view},
             "gpu_launches": main_res["launches"],
             "clocks": main_res["clocks"],
             "context": {"paper_table1": "implicit cyclic-reduction scheme (a different algorithm), 4096^2, 100 steps: "
@@ -592,10 +636,12 @@ def main():
             line["e2e"] = main_res["e2e"]
         if also:
             e2 = ESZ[other]
-            words2 = 3.0 if tblock_other == 1 else 4.0 / tblock_other
-            ach2 = also["kernel_updates_per_launch"] / (also["kernel_avg_ms"] * 1e-3) * words2 * e2 / 1e9
+            words2 = words_per_update(args.steps, args.energy_every, tblock_other)
+            upd2 = also["kernel_updates_per_launch"] / (also["kernel_avg_ms"] * 1e-3)
+            ach2 = upd2 * words2 * e2 / 1e9
             line["also"] = {"dtype": other, "value": also["value"], "unit": UNIT, "temporal_blocking": tblock_other,
-                            "ms_per_step": also["ms"] / args.steps, "roofline_frac": ach2 / peak, "achieved_gbs": ach2}
+                            "ms_per_step": also["ms"] / args.steps, "roofline_frac": ach2 / peak, "achieved_gbs": ach2,
+                            "alu_frac": upd2 * 14 / 1e12 / alu_peak(other)}
         if per_step:
             ach1 = per_step["kernel_updates_per_launch"] * 3 * esz / (per_step["kernel_avg_ms"] * 1e-3) / 1e9
             line["per_step_kernel"] = {"kernel": "k_step2d_tma", "value": per_step["value"], "unit": UNIT,

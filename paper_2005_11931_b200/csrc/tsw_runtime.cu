@@ -14,6 +14,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <vector>
+#include <memory>
 #include <map>
 #include <mutex>
 
@@ -1339,15 +1341,42 @@ tsw_status ensure_ghosts_nccl(tsw_ctx* c, int K) {
 
 bool tb_usable(const tsw_ctx* c);
 
+// The remainder of a stepping call (2 ≤ r < K levels) runs as one pass of depth r instead of r
+// single levels: every node is the same canonical expression, so the result is bitwise that of r
+// one-level steps, and the fields make one HBM round trip instead of r.
+struct DepthScope {
+    tsw_ctx* c;
+    int k0;
+    DepthScope(tsw_ctx* c_, int r) : c(c_), k0(c_->tblock) { c->tblock = r; }
+    ~DepthScope() { c->tblock = k0; }
+};
+struct GroupDepth {
+    tsw_ctx** cs;
+    int n;
+    std::vector<int> k0;
+    GroupDepth(tsw_ctx** cs_, int n_, int r) : cs(cs_), n(n_), k0(n_) {
+        for (int i = 0; i < n; ++i) {
+            k0[i] = cs[i]->tblock;
+            cs[i]->tblock = r;
+        }
+    }
+    ~GroupDepth() {
+        for (int i = 0; i < n; ++i) cs[i]->tblock = k0[i];
+    }
+};
+int pass_depth(const tsw_ctx* c, int64_t remaining) {
+    return int(std::min<int64_t>(c->tblock, remaining));
+}
+
 // Peer halos: the halo operations of a stepping call, one epoch each.  The next operation follows
 // from the ctx state alone, so every rank of a group issues the same sequence.
 enum PeerOp { PEER_NONE = 0, PEER_ENSURE_1, PEER_ENSURE_K, PEER_LEVEL, PEER_PASS };
 PeerOp next_peer_op(const tsw_ctx* c, int64_t remaining) {
     if (remaining <= 0) return PEER_NONE;
-    const int K = c->tblock;
-    const bool pass = tb_usable(c) && c->n > 0 && remaining >= K;
+    const int d = pass_depth(c, remaining);  // a full pass, or the remainder as a shallower one
+    const bool pass = tb_usable(c) && c->n > 0 && d >= 2;
     if (pass) {
-        if (c->gdepth[c->ic] < K || c->gdepth[c->ip] < K) return PEER_ENSURE_K;
+        if (c->gdepth[c->ic] < d || c->gdepth[c->ip] < d) return PEER_ENSURE_K;
         return PEER_PASS;
     }
     if (c->gdepth[c->ic] < 1) return PEER_ENSURE_1;
@@ -1356,13 +1385,17 @@ PeerOp next_peer_op(const tsw_ctx* c, int64_t remaining) {
 tsw_status ensure_ghosts_nccl(tsw_ctx* c, int K);
 tsw_status step_slab_peer(tsw_ctx* c);
 tsw_status tb_pass(tsw_ctx* c);
-tsw_status run_peer_op(tsw_ctx* c, PeerOp op, int64_t* consumed) {
+tsw_status run_peer_op(tsw_ctx* c, PeerOp op, int64_t remaining, int64_t* consumed) {
     *consumed = 0;
     switch (op) {
         case PEER_ENSURE_1: return ensure_ghosts_nccl(c, 1);
         case PEER_ENSURE_K: return ensure_ghosts_nccl(c, c->tblock);
         case PEER_LEVEL: *consumed = 1; return step_slab_peer(c);
-        case PEER_PASS: *consumed = c->tblock; return tb_pass(c);
+        case PEER_PASS: {
+            DepthScope ds(c, pass_depth(c, remaining));
+            *consumed = c->tblock;
+            return tb_pass(c);
+        }
         default: return TSW_OK;
     }
 }
@@ -1426,7 +1459,7 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
             const PeerOp op = next_peer_op(c, k - s);
             if (op == PEER_NONE) return TSW_OK;
             int64_t used = 0;
-            if ((st = run_peer_op(c, op, &used))) return st;
+            if ((st = run_peer_op(c, op, k - s, &used))) return st;
             s += used;
         }
     }
@@ -1436,10 +1469,15 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
             if ((st = step_slab_overlapped(c))) return st;
             s = 1;
         }
-        if (tb_usable(c) && s + c->tblock <= k) {
+        if (tb_usable(c) && pass_depth(c, k - s) >= 2) {
             if ((st = ensure_ghosts_nccl(c, c->tblock))) return st;
             for (; s + c->tblock <= k; s += c->tblock)
                 if ((st = tb_pass(c))) return st;
+            if (k - s >= 2) {
+                DepthScope ds(c, int(k - s));
+                if ((st = tb_pass(c))) return st;
+                s = k;
+            }
         }
         for (; s < k; ++s)
             if ((st = step_slab_overlapped(c))) return st;
@@ -1452,9 +1490,15 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
         c->n++;
         s = 1;
     }
-    if (tb_usable(c))
+    if (tb_usable(c)) {
         for (; s + c->tblock <= k; s += c->tblock)
             if ((st = tb_pass(c))) return st;
+        if (k - s >= 2) {
+            DepthScope ds(c, int(k - s));
+            if ((st = tb_pass(c))) return st;
+            s = k;
+        }
+    }
     const bool graphs = c->use_graphs && !c->timing;
     for (; s + 1 < k && graphs; s += 2)
         if ((st = step_pair_graph(c))) return st;
@@ -1864,7 +1908,7 @@ tsw_status tsw_step_op(tsw_ctx* c, int64_t nsteps, int64_t* consumed) {
     tsw_status st = set_dev(c);
     if (st) return st;
     const PeerOp op = next_peer_op(c, nsteps);
-    return run_peer_op(c, op, consumed);
+    return run_peer_op(c, op, nsteps, consumed);
 }
 
 tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
@@ -1891,7 +1935,7 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
             if (op == PEER_NONE) return TSW_OK;
             int64_t used = 0;
             for (int r = 0; r < n; ++r)
-                if ((st = run_peer_op(cs[r], op, &used))) return st;
+                if ((st = run_peer_op(cs[r], op, nsteps - s, &used))) return st;
             s += used;
         }
     }
@@ -1936,43 +1980,54 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
         if ((st = single())) return st;
         s = 1;
     }
-    const int K = c0->tblock;
-    if (tb_usable(c0) && s + K <= nsteps) {
+    // one pass of K levels (every member's depth set to K for its duration)
+    auto pass = [&](int K) -> tsw_status {
+        GroupDepth gd(cs, n, K);
         for (int lv = 0; lv < 2; ++lv) {
             const int bi = lv ? c0->ip : c0->ic;
             if (c0->gdepth[bi] < K) {
-                if ((st = exchange_loopback_buf(cs, n, bi, c0->stream, K))) return st;
+                tsw_status e = exchange_loopback_buf(cs, n, bi, c0->stream, K);
+                if (e) return e;
                 for (int r = 0; r < n; ++r) cs[r]->gdepth[bi] = K;
             }
         }
         bool split = true;
         for (int r = 0; r < n; ++r) split = split && tb_split(cs[r]).split;
-        for (; s + K <= nsteps; s += K) {
-            int fk, fkm1;
-            free_pair(c0, &fk, &fkm1);
-            if (split) {
-                for (int r = 0; r < n; ++r) {
-                    const TbSplit p = tb_split(cs[r]);
-                    if ((st = launch_tb_rows(cs[r], fk, fkm1, p.top_lo, p.top_hi))) return st;
-                    if ((st = launch_tb_rows(cs[r], fk, fkm1, p.bot_lo, p.bot_hi))) return st;
-                }
-                CK(cudaEventRecord(c0->ev_bnd, c0->stream));
-                CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
-                if ((st = exchange_loopback_buf(cs, n, fk, c0->aux, K))) return st;
-                if ((st = exchange_loopback_buf(cs, n, fkm1, c0->aux, K))) return st;
-                CK(cudaEventRecord(c0->ev_comm, c0->aux));
-                for (int r = 0; r < n; ++r) {
-                    const TbSplit p = tb_split(cs[r]);
-                    if ((st = launch_tb_rows(cs[r], fk, fkm1, p.ilo, p.ihi))) return st;
-                }
-                CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
-            } else {
-                for (int r = 0; r < n; ++r)
-                    if ((st = launch_tb_rows(cs[r], fk, fkm1, cs[r]->s_lo, cs[r]->s_hi))) return st;
-                if ((st = exchange_loopback_buf(cs, n, fk, c0->stream, K))) return st;
-                if ((st = exchange_loopback_buf(cs, n, fkm1, c0->stream, K))) return st;
+        int fk, fkm1;
+        free_pair(c0, &fk, &fkm1);
+        tsw_status e;
+        if (split) {
+            for (int r = 0; r < n; ++r) {
+                const TbSplit p = tb_split(cs[r]);
+                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.top_lo, p.top_hi))) return e;
+                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.bot_lo, p.bot_hi))) return e;
             }
-            advance(fk, fkm1, K, K);
+            CK(cudaEventRecord(c0->ev_bnd, c0->stream));
+            CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
+            if ((e = exchange_loopback_buf(cs, n, fk, c0->aux, K))) return e;
+            if ((e = exchange_loopback_buf(cs, n, fkm1, c0->aux, K))) return e;
+            CK(cudaEventRecord(c0->ev_comm, c0->aux));
+            for (int r = 0; r < n; ++r) {
+                const TbSplit p = tb_split(cs[r]);
+                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.ilo, p.ihi))) return e;
+            }
+            CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
+        } else {
+            for (int r = 0; r < n; ++r)
+                if ((e = launch_tb_rows(cs[r], fk, fkm1, cs[r]->s_lo, cs[r]->s_hi))) return e;
+            if ((e = exchange_loopback_buf(cs, n, fk, c0->stream, K))) return e;
+            if ((e = exchange_loopback_buf(cs, n, fkm1, c0->stream, K))) return e;
+        }
+        advance(fk, fkm1, K, K);
+        return TSW_OK;
+    };
+    if (tb_usable(c0)) {
+        const int K = c0->tblock;
+        for (; s + K <= nsteps; s += K)
+            if ((st = pass(K))) return st;
+        if (nsteps - s >= 2) {  // the remainder as one shallower pass (see DepthScope)
+            if ((st = pass(int(nsteps - s)))) return st;
+            s = nsteps;
         }
     }
     for (; s < nsteps; ++s)

@@ -30,7 +30,7 @@ def _group(cfg, P, K, dtype="f64"):
 
 
 @pytest.mark.parametrize("P", [2, 3])
-@pytest.mark.parametrize("K", [1, 4, 8])
+@pytest.mark.parametrize("K", [1, 4, 5, 8])
 @pytest.mark.parametrize("ny", [151, 29])
 def test_peer_halo_slabs_bitwise(P, K, ny):
     cfg = inputs.config(3, nx=700, ny=ny, dx=0.01, dy=0.01, eps=[0.1, 0.3], amp=[1.0, 2.0], dt=2e-3)
@@ -60,19 +60,20 @@ def test_peer_halo_slabs_bitwise(P, K, ny):
     ref.close()
 
 
-def test_peer_halo_bench_shape_sampled():
-    """The bench workload split into 2 slabs with K = 4 peer halos: sampled rows ≡ single domain."""
+@pytest.mark.parametrize("K,n", [(4, 41), (8, 45)])
+def test_peer_halo_bench_shape_sampled(K, n):
+    """The bench workload split into 2 slabs with K-deep peer halos (K = 8: a 4-level remainder
+    pass): the slabs ≡ the single domain stepped one level at a time."""
     cfg = inputs.weak_unit(2, rows_per_rank=512)
     u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny)
     ref = tsw.Solver.from_config(cfg, "f64")
-    ref.set_option(tsw.TSW_OPT_TBLOCK, 4)
     ref.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
-    ref.step(41)
+    ref.step(n)
     g = ref.read(0)
-    parts, _ = _group(cfg, 2, 4)
+    parts, _ = _group(cfg, 2, K)
     for p in parts:
         p.set_initial(np.ascontiguousarray(u0[p.r0:p.r0 + p.ny_local]), None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
-    tsw.tsw_group_step([p.ctx for p in parts], 41)
+    tsw.tsw_group_step([p.ctx for p in parts], n)
     for p in parts:
         assert np.array_equal(p.read(0), g[:, p.r0:p.r0 + p.ny_local])
         p.close()

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("K,nsteps", [(1, 9), (4, 23)])
+@pytest.mark.parametrize("K,nsteps", [(1, 9), (4, 23), (8, 23)])
 def test_peer_halo_ipc_two_processes(K, nsteps):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29611", os.path.join(ROOT, "tests", "peer_ipc_worker.py"),

@@ -47,6 +47,25 @@ def test_tblock_bitwise_vs_oracle(dtype, K):
     s1.close()
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("K,levels", [(8, 13), (8, 10), (5, 7), (4, 3)])
+def test_tblock_remainder_is_one_shallower_pass(dtype, K, levels):
+    """A stepping call of q·K + r levels (2 ≤ r < K) runs q passes of depth K and ONE pass of depth r
+    (not r one-level steps) — one launch per pass — with the bits of one-level stepping."""
+    cfg = inputs.config(3, nx=900, ny=97, dx=0.01, dy=0.01, eps=[0.1], amp=[1.0], dt=2e-3)
+    u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(NP[dtype])
+    s = _run(cfg, dtype, K, 1, u0)  # start-up level
+    n0 = s.launches()
+    s.step(levels)
+    q, r = divmod(levels, K)
+    assert s.launches() - n0 == q + (1 if r >= 2 else r)
+    ref = _run(cfg, dtype, 1, 1 + levels, u0)
+    assert np.array_equal(s.read(0), ref.read(0))
+    assert np.array_equal(s.read(1), ref.read(1))
+    s.close()
+    ref.close()
+
+
 @pytest.mark.parametrize("K", [4, 8])
 def test_tblock_profile_isotropic_and_auto_chunks(K):
     sc = inputs.paper_2d(dx=0.1)

@@ -19,7 +19,7 @@ unit = dict(zip(h, r[1]))
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 rd = f("dram__bytes_read.sum") * scale.get(unit["dram__bytes_read.sum"], 1)
 wr = f("dram__bytes_write.sum") * scale.get(unit["dram__bytes_write.sum"], 1)
-tscale = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+tscale = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3}
 dur = f("gpu__time_duration.sum") * tscale.get(unit["gpu__time_duration.sum"], 1)
 esz = 8 if "double" in d["Kernel Name"] else 4
 algo = 32766 * 4094 * esz * (4 if levels > 1 else 3)
