@@ -785,7 +785,8 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         T* okm1p = a.out_km1 + b * a.mstride + gc0 + int64_t(in_lo - K) * a.pitch;
         // Dirichlet masking is only needed where the item's dependency cone (rows in_lo − K ..
         // s1 + K − 1, the extended strip's columns) touches a boundary row/column or the grid edge
-        const bool masked = !((in_lo - K >= rowlo) && (s1 + K - 1 <= rowhi) && (cs - H >= 1) && (cs - H + WE <= a.nx - 1));
+        const bool col_clear = (cs - H >= 1) && (cs - H + WE <= a.nx - 1);
+        const bool masked = !((in_lo - K >= rowlo) && (s1 + K - 1 <= rowhi) && col_clear);
 #pragma unroll
         for (int m = 0; m < K; ++m)
 #pragma unroll
@@ -868,20 +869,43 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             okp += a.pitch;
             okm1p += a.pitch;
         };
-        auto run_rows = [&](auto msk) {
-            int i = 0;
-            for (; i + 3 <= L; i += 3) {
+        // rows [i0, i1) of the item; i0 is a multiple of 3 (the window phase is i mod 3)
+        auto run_rows = [&](auto msk, int i0, int i1) {
+            int i = i0;
+            for (; i + 3 <= i1; i += 3) {
                 row(std::integral_constant<int, 0>{}, msk, i);
                 row(std::integral_constant<int, 1>{}, msk, i + 1);
                 row(std::integral_constant<int, 2>{}, msk, i + 2);
             }
-            if (i < L) row(std::integral_constant<int, 0>{}, msk, i++);
-            if (i < L) row(std::integral_constant<int, 1>{}, msk, i++);
+            if (i < i1) row(std::integral_constant<int, 0>{}, msk, i++);
+            if (i < i1) row(std::integral_constant<int, 1>{}, msk, i++);
         };
-        if (masked)
-            run_rows(std::integral_constant<bool, true>{});
-        else
-            run_rows(std::integral_constant<bool, false>{});
+        // Input row i computes levels m = 1..K at rows R − m (R = in_lo + i); it needs the
+        // boundary selects only while one of those rows lies outside [rowlo, rowhi].  In a strip
+        // clear of the boundary columns the item runs masked only at its ends (segment limits
+        // rounded to the window phase).
+        int ua = 0, ub = 0;
+        if (masked && col_clear) {
+            ua = rowlo + K - in_lo;
+            ub = rowhi + 2 - in_lo;
+            ua = (ua <= 0) ? 0 : (ua + 2) / 3 * 3;
+            ub = (ub >= L) ? L : (ub <= 0 ? 0 : ub / 3 * 3);
+            if (ub <= ua) ua = ub = 0;
+        } else if (!masked) {
+            ub = L;
+        }
+        if (ub <= ua) ua = ub = L;  // all masked: segment 0 covers the item
+        // segments [0, ua) masked, [ua, ub) unmasked, [ub, L) masked (one call site per variant)
+#pragma unroll 1
+        for (int sg = 0; sg < 3; ++sg) {
+            const int lo = (sg == 0) ? 0 : (sg == 1 ? ua : ub);
+            const int hi = (sg == 0) ? ua : (sg == 1 ? ub : L);
+            if (lo >= hi) continue;
+            if (sg == 1)
+                run_rows(std::integral_constant<bool, false>{}, lo, hi);
+            else
+                run_rows(std::integral_constant<bool, true>{}, lo, hi);
+        }
     }
 }
 
