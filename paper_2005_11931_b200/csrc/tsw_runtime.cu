@@ -755,7 +755,11 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
         if (st) return st;
         CK(cudaEventRecord(e0, c->stream));
     }
-    if (peer)
+    // the peer-store variant only where this launch's output rows include pushed rows (the
+    // interior launch of a split pass has none and runs the plain kernel, which needs fewer
+    // registers: the K = 8 fp64 peer variant spills)
+    const bool push = peer && ((has_nb(c, 0) && s_lo <= a.push_top) || (has_nb(c, 1) && s_hi - 1 >= a.push_bot));
+    if (push)
         k_step2d_tb<T, K, true, NC><<<unsigned(blocks), NC * 32, smem, c->stream>>>(a, depth);
     else
         k_step2d_tb<T, K, false, NC><<<unsigned(blocks), NC * 32, smem, c->stream>>>(a, depth);
