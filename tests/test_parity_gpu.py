@@ -261,7 +261,7 @@ def _dense_rows(cfg):
     return lambda j0, rows, i0, cols: inputs.uniform_dense_rows(cfg.nx, cfg.ny, j0, rows)[:, i0:i0 + cols]
 
 
-BENCH_K = {"f64": 4, "f32": 8}   # bench.py's default temporal-blocking depth per dtype
+from bench import TB_DEFAULT as BENCH_K   # bench.py's default temporal-blocking depth per dtype
 
 
 @pytest.mark.parametrize("dtype,K,full", [("f64", 1, False), ("f32", 1, False), ("f64", BENCH_K["f64"], False),

@@ -82,12 +82,14 @@ def test_tblock_profile_isotropic_and_auto_chunks(K):
     ref.close()
 
 
-def test_tblock_bench_shape_sampled():
-    """The bench workload (32768 × 4096 δ-line slab) with K = 4: sampled nodes ≡ the K = 1 run."""
+@pytest.mark.parametrize("K", [4, 8])
+def test_tblock_bench_shape_sampled(K):
+    """The bench workload (32768 × 4096 δ-line slab) with K = 4 and the bench's K = 8 (the start-up
+    level, passes and a remainder pass): the whole field ≡ the K = 1 run."""
     cfg = inputs.weak_unit(1)
     u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny)
-    a = _run(cfg, "f64", 4, 41, u0)
-    b = _run(cfg, "f64", 1, 41, u0)
+    a = _run(cfg, "f64", K, 41 + K // 2, u0)
+    b = _run(cfg, "f64", 1, 41 + K // 2, u0)
     ga, gb = a.read(0)[0], b.read(0)[0]
     bad = np.argwhere(ga != gb)
     if len(bad):
@@ -97,12 +99,12 @@ def test_tblock_bench_shape_sampled():
         thin.close()
         info = []
         for (j, i) in [tuple(bad[0]), (2048, 16000)]:
-            R = 42
+            R = 42 + K // 2
             i0, i1 = max(0, i - R), min(cfg.nx, i + R + 1)
             j0, j1 = max(0, j - R), min(cfg.ny, j + R + 1)
             c1 = oracle.prescale(np.tile(line[i0:i1 - 1], (j1 - j0, 1)), cfg.dt, cfg.dx, np.float64)
             c2 = oracle.prescale(np.full((j1 - j0 - 1, i1 - i0), 1.0), cfg.dt, cfg.dy, np.float64)
-            un, _ = oracle.run(2, c1, c2, np.ascontiguousarray(u0[j0:j1, i0:i1]), None, cfg.dt, 41)
+            un, _ = oracle.run(2, c1, c2, np.ascontiguousarray(u0[j0:j1, i0:i1]), None, cfg.dt, 41 + K // 2)
             info.append(((int(j), int(i)), un[j - j0, i - i0], ga[j, i], gb[j, i]))
         raise AssertionError((len(bad), bad[:4].tolist(), info))
     np.testing.assert_allclose(a.energy(), b.energy(), rtol=1e-13)
