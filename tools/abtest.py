@@ -17,6 +17,8 @@ def main():
     cfg = inputs.weak_unit(1)
     npdt = np.float64 if dtype == "f64" else np.float32
     s = tsw.Solver.from_config(cfg, dtype)
+    if os.environ.get("TSW_AB_WARPS"):   # CTA width of the TB stencil (TSW_OPT_TB_WARPS)
+        s.set_option(tsw.TSW_OPT_TB_WARPS, int(os.environ["TSW_AB_WARPS"]))
     s.set_initial(inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(npdt), None, cfg.dt,
                   flags=tsw.TSW_INIT_SHARED)
     s.step(1)
