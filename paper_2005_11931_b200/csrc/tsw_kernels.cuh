@@ -537,6 +537,9 @@ struct TbArgs {
     const T* c2;
     int64_t pitch, mstride, cstride, nx, ny, r0;
     int32_t s_lo, s_hi;  // output storage rows
+    // an optional second range of output rows (a slab's first and last K rows in one launch):
+    // chunks [0, chunks1) cover [s_lo, s_hi), the rest [s_lo2, s_hi2)
+    int32_t s_lo2 = 0, s_hi2 = 0, chunks1 = INT32_MAX;
     int32_t smin, smax;  // storage rows inside the grid (global rows 0 .. ny−1 of this slab)
     int32_t rows_per_item, chunks;
     int64_t strips, items;
@@ -717,8 +720,13 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         const int chunk = int(rest % a.chunks);
         b = int(rest / a.chunks);
         cs = strip * WO;
-        s0 = a.s_lo + chunk * a.rows_per_item;
-        s1 = min(s0 + a.rows_per_item, a.s_hi);
+        if (chunk < a.chunks1) {
+            s0 = a.s_lo + chunk * a.rows_per_item;
+            s1 = min(s0 + a.rows_per_item, a.s_hi);
+        } else {
+            s0 = a.s_lo2 + (chunk - a.chunks1) * a.rows_per_item;
+            s1 = min(s0 + a.rows_per_item, a.s_hi2);
+        }
         in_lo = max(s0 - K, a.smin);
         in_hi = min(s1 + K, a.smax + 1);
     };

@@ -692,7 +692,7 @@ bool peer_mode(const tsw_ctx* c) { return c->g.nranks > 1 && c->g.dim == 2 && c-
 
 // ---- temporally blocked pass: K levels, (buf[ic], buf[ip]) → (buf[fk], buf[fkm1]) -----------
 template <typename T, int K, int NC>
-tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
+tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi, int32_t s_lo2, int32_t s_hi2) {
     using G = TbGeom<T, K, NC>;
     const int depth = c->tb_depth;
     const size_t smem = tb_smem_bytes<T, K, NC>(depth);
@@ -740,13 +740,17 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
             a.push_bot = int32_t(c->ny_local) - K + 1;
         }
     }
-    const int64_t rows = s_hi - s_lo;
+    const int64_t rows1 = s_hi - s_lo, rows2 = s_hi2 - s_lo2;
+    const int64_t rows = rows1 + rows2;
     const int64_t Gw = int64_t(occ) * c->sm_count;
     int R = c->rows_per_item_opt;
     if (R <= 0) R = choose_rows_per_item(rows, a.strips, c->g.batch, Gw, 2.0 * K, 0.5, 4 * K);
-    if (R > rows) R = int(rows);
+    R = int(std::min<int64_t>(R, std::max(rows1, rows2)));
     a.rows_per_item = R;
-    a.chunks = int((rows + R - 1) / R);
+    a.chunks1 = int((rows1 + R - 1) / R);
+    a.s_lo2 = s_lo2;
+    a.s_hi2 = s_hi2;
+    a.chunks = a.chunks1 + int((rows2 + R - 1) / R);
     a.items = a.strips * a.chunks * c->g.batch;
     const int64_t blocks = std::min<int64_t>(a.items, Gw);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -758,7 +762,9 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
     // the peer-store variant only where this launch's output rows include pushed rows (the
     // interior launch of a split pass has none and runs the plain kernel, which needs fewer
     // registers: the K = 8 fp64 peer variant spills)
-    const bool push = peer && ((has_nb(c, 0) && s_lo <= a.push_top) || (has_nb(c, 1) && s_hi - 1 >= a.push_bot));
+    const bool top = s_lo <= a.push_top || (rows2 > 0 && s_lo2 <= a.push_top);
+    const bool bot = s_hi - 1 >= a.push_bot || (rows2 > 0 && s_hi2 - 1 >= a.push_bot);
+    const bool push = peer && ((has_nb(c, 0) && top) || (has_nb(c, 1) && bot));
     if (push)
         k_step2d_tb<T, K, true, NC><<<unsigned(blocks), NC * 32, smem, c->stream>>>(a, depth);
     else
@@ -777,27 +783,36 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
 // 4 warps only where its strips compute ≥ 5 % fewer columns (narrow grids, e.g. config 5's 2048:
 // +12 % fp64, +17 % fp32 measured; at 4096 columns 8 warps are as fast or faster)
 template <typename T, int K>
-tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
+tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi, int32_t s_lo2, int32_t s_hi2) {
+    if (s_hi2 <= s_lo2) s_lo2 = s_hi2 = 0;
+    if (s_hi <= s_lo) {  // the second range alone
+        s_lo = s_lo2;
+        s_hi = s_hi2;
+        s_lo2 = s_hi2 = 0;
+    }
     if (s_hi <= s_lo) return TSW_OK;
     int nc = c->tb_warps;
-    if (!nc) {
+    if (!nc && (s_hi - s_lo) + (s_hi2 - s_lo2) <= 2 * K) {
+        nc = 4;  // a slab's boundary rows: few rows, so twice the CTAs (256-column strips)
+    } else if (!nc) {
         const int64_t cols8 = (c->pitch + TbGeom<T, K, 8>::WO - 1) / TbGeom<T, K, 8>::WO * TbGeom<T, K, 8>::WE;
         const int64_t cols4 = (c->pitch + TbGeom<T, K, 4>::WO - 1) / TbGeom<T, K, 4>::WO * TbGeom<T, K, 4>::WE;
         nc = (double(cols4) < 0.95 * double(cols8)) ? 4 : 8;
     }
-    return nc == 4 ? launch_tb_nc<T, K, 4>(c, fk, fkm1, s_lo, s_hi) : launch_tb_nc<T, K, 8>(c, fk, fkm1, s_lo, s_hi);
+    return nc == 4 ? launch_tb_nc<T, K, 4>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2)
+                   : launch_tb_nc<T, K, 8>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
 }
 
 template <typename T>
-tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
+tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1, int32_t s_lo, int32_t s_hi, int32_t s_lo2, int32_t s_hi2) {
     switch (K) {
-        case 2: return launch_tb_t<T, 2>(c, fk, fkm1, s_lo, s_hi);
-        case 3: return launch_tb_t<T, 3>(c, fk, fkm1, s_lo, s_hi);
-        case 4: return launch_tb_t<T, 4>(c, fk, fkm1, s_lo, s_hi);
-        case 5: return launch_tb_t<T, 5>(c, fk, fkm1, s_lo, s_hi);
-        case 6: return launch_tb_t<T, 6>(c, fk, fkm1, s_lo, s_hi);
-        case 7: return launch_tb_t<T, 7>(c, fk, fkm1, s_lo, s_hi);
-        case 8: return launch_tb_t<T, 8>(c, fk, fkm1, s_lo, s_hi);
+        case 2: return launch_tb_t<T, 2>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 3: return launch_tb_t<T, 3>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 4: return launch_tb_t<T, 4>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 5: return launch_tb_t<T, 5>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 6: return launch_tb_t<T, 6>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 7: return launch_tb_t<T, 7>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 8: return launch_tb_t<T, 8>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
         default: return fail(TSW_ERR_ARG, "unsupported temporal blocking depth %d", K);
     }
 }
@@ -880,9 +895,11 @@ void free_pair(const tsw_ctx* c, int* fk, int* fkm1) {
     *fkm1 = ids[1];
 }
 
-tsw_status launch_tb_rows(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi) {
-    return is_f64(c) ? launch_tb_k<double>(c, c->tblock, fk, fkm1, s_lo, s_hi)
-                     : launch_tb_k<float>(c, c->tblock, fk, fkm1, s_lo, s_hi);
+// output rows [s_lo, s_hi) and, optionally, [s_lo2, s_hi2) in one launch
+tsw_status launch_tb_rows(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi, int32_t s_lo2 = 0,
+                          int32_t s_hi2 = 0) {
+    return is_f64(c) ? launch_tb_k<double>(c, c->tblock, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2)
+                     : launch_tb_k<float>(c, c->tblock, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
 }
 
 // Output rows of a slab pass that neighbours need: the first / last K owned rows.
@@ -928,8 +945,7 @@ tsw_status tb_pass(tsw_ctx* c) {
         const TbSplit p = tb_split(c);
         if ((st = peer_begin(c, c->stream))) return st;
         if (p.split) {
-            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi))) return st;
-            if ((st = launch_tb_rows(c, fk, fkm1, p.bot_lo, p.bot_hi))) return st;
+            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi, p.bot_lo, p.bot_hi))) return st;
             if ((st = peer_end(c, c->stream))) return st;
             if ((st = launch_tb_rows(c, fk, fkm1, p.ilo, p.ihi))) return st;
         } else {
@@ -940,8 +956,7 @@ tsw_status tb_pass(tsw_ctx* c) {
     } else {
         const TbSplit p = tb_split(c);
         if (p.split) {
-            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi))) return st;
-            if ((st = launch_tb_rows(c, fk, fkm1, p.bot_lo, p.bot_hi))) return st;
+            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi, p.bot_lo, p.bot_hi))) return st;
             CK(cudaEventRecord(c->ev_bnd, c->stream));
             CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
             if ((st = exchange_nccl(c, c->buf[fk], c->aux, K))) return st;
@@ -2003,8 +2018,7 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
         if (split) {
             for (int r = 0; r < n; ++r) {
                 const TbSplit p = tb_split(cs[r]);
-                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.top_lo, p.top_hi))) return e;
-                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.bot_lo, p.bot_hi))) return e;
+                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.top_lo, p.top_hi, p.bot_lo, p.bot_hi))) return e;
             }
             CK(cudaEventRecord(c0->ev_bnd, c0->stream));
             CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
