@@ -37,6 +37,15 @@ def main():
     one.step(1 + K)
     t_one = min(timed(lambda: one.step(n)) for _ in range(3))
     one.close()
+    # the weak-scaling reference: one slab's rows as a single domain (the N = 1 bench run), × P
+    c1 = inputs.weak_unit(1)
+    u1 = np.ascontiguousarray(u0[:c1.ny])
+    unit = tsw.Solver.from_config(c1, dtype, stream=stream.cuda_stream)
+    unit.set_option(tsw.TSW_OPT_TBLOCK, K)
+    unit.set_initial(u1, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    unit.step(1 + K)
+    t_unit = P * min(timed(lambda: unit.step(n)) for _ in range(3))
+    unit.close()
     parts = [tsw.Solver.from_config(cfg, dtype, rank=r, nranks=P, stream=stream.cuda_stream) for r in range(P)]
     for p in parts:
         p.set_option(tsw.TSW_OPT_TBLOCK, K)
@@ -56,7 +65,8 @@ def main():
     for p in parts:
         p.close()
     print(json.dumps({"dtype": dtype, "K": K, "P": P, "peer": peer, "levels": n, "ms_one_domain": round(t_one, 3),
-                      "ms_slabs": round(t_grp, 3), "overhead": round(t_grp / t_one - 1, 4)}))
+                      "ms_slabs": round(t_grp, 3), "overhead": round(t_grp / t_one - 1, 4),
+                      "ms_P_x_unit": round(t_unit, 3), "overhead_vs_unit": round(t_grp / t_unit - 1, 4)}))
 
 
 if __name__ == "__main__":
