@@ -216,8 +216,10 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
 #define TSW_OPT_DEPTH 4  /* TMA ring stages per CTA, 2..32 (default 4) */
 #define TSW_OPT_GRAPHS 5 /* 1 (default): single-rank steps replay a CUDA graph of two levels; 0: plain launches */
 #define TSW_OPT_TBLOCK 6 /* K ∈ {1,…,8}: levels per HBM pass of the temporally blocked stencil
-                            (single-rank 2D, δ-line / constant / profile kinds; allocates two more
-                            levels; results are bitwise those of K = 1).  Default 1. */
+                            (2D, δ-line / constant / profile kinds; slabs use K-deep ghost rows;
+                            allocates two more levels; results are bitwise those of K = 1).  A
+                            tsw_step call's remainder of r levels (2 ≤ r < K) runs as one pass of
+                            depth r.  Default 1. */
 #define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil, 3..16 (default 4) */
 #define TSW_OPT_SCHEME 8   /* 0 (default): explicit leapfrog (north_star).  1: the paper's implicit method
                               (§3.3, reading R26): factorised three-level Crank–Nicolson
@@ -237,7 +239,8 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               (the paper's solver), ≤ 4095 (fp64) / 8191 (fp32) unknowns per line. */
 #define TSW_OPT_TB_WARPS 13 /* CTA width of the temporally blocked stencil: 8 warps (512-column strips), 4
                               (256-column strips: less redundant halo work on narrow grids), 0 (default):
-                              4 for rows of ≤ 4096 columns, else 8 */
+                              4 where its strips compute ≥ 5 % fewer columns, and for a slab's launch of
+                              its first / last K rows; else 8 */
 #define TSW_OPT_IMPLICIT_XROWS 12 /* rows per iteration of the implicit x-line solve: 1 (default; LU tables
                               in registers) or 2 (the two rows' scan chains interleave, tables in shared
                               memory — measured 4 % slower at 4096², kept for comparison) */

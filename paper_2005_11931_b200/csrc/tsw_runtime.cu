@@ -14,8 +14,6 @@
 #include <cstring>
 #include <string>
 #include <vector>
-#include <vector>
-#include <memory>
 #include <map>
 #include <mutex>
 
