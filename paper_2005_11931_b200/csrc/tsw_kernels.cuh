@@ -1361,7 +1361,9 @@ struct Wave2Args {
     int bg;
     double dx, xs;
     const double* eps;  // [B] device
-    int nblk;
+    int nblk;           // CTAs per member = tiles × chunks
+    int64_t tiles;      // column tiles of 256·V columns
+    int32_t rows_per_chunk;
 };
 
 struct ArgVal {
@@ -1375,25 +1377,49 @@ __device__ __forceinline__ void arg_better_min(double& v, long long& i, double v
     if (i2 >= 0 && (i < 0 || v2 < v || (v2 == v && i2 < i))) { v = v2; i = i2; }
 }
 
+// A CTA owns a tile of 256·V columns (V = 16 bytes per thread) and a chunk of rows of one member:
+// 128-bit loads along rows, the region test once per column, tiles wholly outside the region
+// skipped (only the region's nodes are read).  Within a thread rows and columns are visited in
+// increasing row-major order and only a strictly better value replaces the running one, so the
+// first extremum is kept; CTAs and the final pass break ties by the smaller index.
 template <typename T>
 __global__ void __launch_bounds__(256) k_wave2(Wave2Args a, ArgVal* __restrict__ partial) {
+    constexpr int V = Vec16<T>::N;
     const int b = blockIdx.y;
     const T* U = static_cast<const T*>(a.u) + b * a.mstride;
     const T* G = static_cast<const T*>(a.u) + a.bg * a.mstride;
     const double xlim = a.xs - a.eps[b];
+    const int64_t tile = blockIdx.x % a.tiles;
+    const int chunk = int(blockIdx.x / a.tiles);
+    const int64_t col = (tile * 256 + threadIdx.x) * V;
     const int64_t rows = (a.dim == 1) ? 1 : a.ny_local;
-    const int64_t total = rows * a.nx;
+    const int64_t r_lo = int64_t(chunk) * a.rows_per_chunk;
+    const int64_t r_hi = min(r_lo + int64_t(a.rows_per_chunk), rows);
     double vmax = 0.0, vmin = 0.0;
     long long imax = -1, imin = -1;
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i = k % a.nx;
-        if (!(grid_node(i, a.nx, a.dx) <= xlim)) continue;
-        const int64_t s = (a.dim == 1) ? 0 : 1 + k / a.nx;
-        const int64_t g = (a.dim == 1) ? 0 : a.r0 + s - 1;
-        const T d = r_sub(U[s * a.pitch + i], G[s * a.pitch + i]);
-        const long long gi = (long long)(g * a.nx + i);
-        arg_better_max(vmax, imax, (double)d, gi);
-        arg_better_min(vmin, imin, (double)d, gi);
+    bool inreg[V];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        inreg[k] = (col + k < a.nx) && (grid_node(col + k, a.nx, a.dx) <= xlim);
+        any = any || inreg[k];
+    }
+    if (any) {
+        for (int64_t r = r_lo; r < r_hi; ++r) {
+            const int64_t s = (a.dim == 1) ? 0 : 1 + r;
+            const int64_t g = (a.dim == 1) ? 0 : a.r0 + r;
+            T uv[V], gv[V];
+            vload(U + s * a.pitch + col, uv);
+            vload(G + s * a.pitch + col, gv);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                if (!inreg[k]) continue;
+                const double d = (double)r_sub(uv[k], gv[k]);
+                const long long gi = (long long)(g * a.nx + col + k);
+                if (imax < 0 || d > vmax) { vmax = d; imax = gi; }
+                if (imin < 0 || d < vmin) { vmin = d; imin = gi; }
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -2153,8 +2153,15 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
     a.dx = c->g.dx;
     a.xs = c->xs;
     a.eps = c->d_eps;
-    const int64_t total = ((c->g.dim == 1) ? 1 : c->ny_local) * c->g.nx;
-    a.nblk = grid_for(total, 256, c->nblk_red);
+    // column tiles × row chunks: ≈ 8 CTAs per SM over the batch, ≤ nblk_red partials per member
+    const int64_t rows = (c->g.dim == 1) ? 1 : c->ny_local;
+    a.tiles = (c->g.nx + 256 * int64_t(16 / c->esz) - 1) / (256 * int64_t(16 / c->esz));
+    int64_t chunks = (int64_t(8) * c->sm_count + a.tiles * c->g.batch - 1) / (a.tiles * c->g.batch);
+    chunks = std::max<int64_t>(1, std::min<int64_t>({chunks, rows, std::max<int64_t>(1, c->nblk_red / a.tiles)}));
+    a.rows_per_chunk = int32_t((rows + chunks - 1) / chunks);
+    chunks = (rows + a.rows_per_chunk - 1) / a.rows_per_chunk;
+    a.nblk = int(a.tiles * chunks);
+    if (a.nblk > c->nblk_red) return fail(TSW_ERR_ARG, "wave2: too many partials (row too wide)");
     dim3 grid(unsigned(a.nblk), unsigned(c->g.batch));
     if (is_f64(c))
         k_wave2<double><<<grid, 256, 0, c->stream>>>(a, c->d_argpart);
