@@ -1249,7 +1249,7 @@ struct Energy2Args {
 };
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* __restrict__ partial) {
+__global__ void __launch_bounds__(256, 3) k_energy2d(const Energy2Args a, double* __restrict__ partial) {
     constexpr int V = Vec16<T>::N;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t item = blockIdx.x;
@@ -1281,15 +1281,29 @@ __global__ void __launch_bounds__(256) k_energy2d(const Energy2Args a, double* _
         // row ahead together with the row itself, so no load sits on an iteration's critical path
         const bool rok = (lane == 31) && (cs + 32 * V < a.pitch);
         const int64_t rcol = cs + 32 * V;
-        T ac[V], bc[V], an[V], bn[V];
+        // two rows in flight ahead of the one being reduced (the loads are long-latency; storage
+        // rows up to rows + 1 exist)
+        T ac[V], bc[V], an[V], bn[V], a2[V], b2[V];
         vload(A + s0 * a.pitch + col, ac);
         vload(Bv + s0 * a.pitch + col, bc);
+        vload(A + (s0 + 1) * a.pitch + col, a2);
+        vload(Bv + (s0 + 1) * a.pitch + col, b2);
         T xr = rok ? A[s0 * a.pitch + rcol] : (T)0, yr = rok ? Bv[s0 * a.pitch + rcol] : (T)0;
+        T x2 = rok ? A[(s0 + 1) * a.pitch + rcol] : (T)0, y2 = rok ? Bv[(s0 + 1) * a.pitch + rcol] : (T)0;
         for (int s = s0; s < s1; ++s) {
             const int64_t g = a.r0 + s - 1;
-            vload(A + (s + 1) * a.pitch + col, an);
-            vload(Bv + (s + 1) * a.pitch + col, bn);
-            const T xn = rok ? A[(s + 1) * a.pitch + rcol] : (T)0, yn = rok ? Bv[(s + 1) * a.pitch + rcol] : (T)0;
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                an[k] = a2[k];
+                bn[k] = b2[k];
+            }
+            const T xn = x2, yn = y2;
+            if (s + 2 <= a.rows + 1) {
+                vload(A + (s + 2) * a.pitch + col, a2);
+                vload(Bv + (s + 2) * a.pitch + col, b2);
+                x2 = rok ? A[(s + 2) * a.pitch + rcol] : (T)0;
+                y2 = rok ? Bv[(s + 2) * a.pitch + rcol] : (T)0;
+            }
             T ar = __shfl_down_sync(0xffffffffu, ac[0], 1);
             T br = __shfl_down_sync(0xffffffffu, bc[0], 1);
             if (lane == 31) {
