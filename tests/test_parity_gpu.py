@@ -494,3 +494,31 @@ def test_config5_and_config3_bench_launch_configuration(dtype):
     un, _, _, _ = oracle.run_member(cfg, 0, NP[dtype], nsteps=100, u0=u0)
     assert rel_maxnorm(s.read(0)[0], un) <= TOL[dtype]
     s.close()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("shape", [(37, 1300), (9, 4100), (300, 515)])
+def test_wave2_first_extremum_ties(dtype, shape):
+    """S6 on fields with many equal extrema: the values are fl_T(u_b − u_bg) exactly and the index is
+    the FIRST extremum in row-major order of the region x ≤ x_s − ε (R18) — across threads, CTA
+    tiles, row chunks and members (ragged widths, several column tiles)."""
+    ny, nx = shape
+    eps = [0.05, 0.2, 0.11]
+    cfg = inputs.config(3, nx=nx, ny=ny, dx=0.01, dy=0.01, eps=eps + [0.1], amp=[1.0, 1.0, 1.0, 0.0], dt=2e-3)
+    rng = np.random.default_rng(11)
+    u = rng.integers(-3, 4, size=(cfg.batch, ny, nx)).astype(NP[dtype])    # few distinct values → ties
+    u[:, 0, :] = u[:, -1, :] = 0
+    u[:, :, 0] = u[:, :, -1] = 0
+    s = tsw.Solver.from_config(cfg, dtype)
+    s.set_state(u, u, 5, cfg.dt)
+    w2, idx = s.wave2(3)
+    x = inputs.node_coords(nx, cfg.dx)
+    for b in range(cfg.batch):
+        reg = x <= 0.0 - cfg.eps[b]
+        d = (u[b] - u[3]).astype(NP[dtype])
+        masked = np.where(reg[None, :], d.astype(np.float64), np.nan)
+        flat = masked.reshape(-1)
+        imax, imin = int(np.nanargmax(flat)), int(np.nanargmin(flat))   # first occurrence
+        assert w2[b, 0] == flat[imax] and w2[b, 1] == flat[imin]
+        assert idx[b, 0] == imax and idx[b, 1] == imin, (b, idx[b], imax, imin)
+    s.close()
