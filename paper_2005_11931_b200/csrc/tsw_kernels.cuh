@@ -1136,7 +1136,8 @@ struct CflArgs {
 __global__ void k_cfl(CflArgs a, unsigned long long* __restrict__ out) {
     const int b = blockIdx.z;
     double m = 0.0;
-    const int64_t rows = (a.dim == 1) ? 1 : (a.s_hi - a.s_lo);
+    // x-only coefficients (1D, LINE): every row has the same row sums, so one row decides the max
+    const int64_t rows = (a.dim == 1 || a.mode == MODE_LINE) ? 1 : (a.s_hi - a.s_lo);
     const int64_t total = rows * (a.nx - 2);
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i = 1 + k % (a.nx - 2);
