@@ -405,6 +405,20 @@ def workload_name(cfg, world: int) -> str:
     return f"config4_weak_unit_delta_line_{cfg.nx}x{cfg.ny // world}_per_gpu"
 
 
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` started as one process: re-run the same command line under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous, a free port), as the driver's
+    multi-GPU launch does; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", str(max(1, host_cores() // n))))
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,8 +447,18 @@ def main():
                          "0 = per dtype: 4 for f64, 8 for f32 — the sweep optimum, tools/sweep.py)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     from paper_2005_11931_b200 import inputs, parallel
     rank, world, local = parallel.env_rank()
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
+    if args.impl != "reference":
+        import torch
+        if torch.cuda.device_count() < min(world, local + 1) or not torch.cuda.is_available():
+            sys.stderr.write(f"bench.py: rank {rank} needs GPU {local}, {torch.cuda.device_count()} visible\n")
+            return 2
     if args.workload == "table1":
         return run_table1(args, rank, world, local)
     if args.workload == "config5":

@@ -338,6 +338,40 @@ def test_cfl_threshold_exact():
         assert big != stable
 
 
+def test_cfl_gershgorin_2d_pinned():
+    """R16 in 2D (R16: leapfrog is stable iff dt²ρ(K)/4 < 1; the API's sufficient bound
+    dt ≤ 2/√ρ_G, ρ_G = max over interior nodes of Σ_faces 2h/d²), pinned three ways:
+    (a) brute force: ρ_G = twice the largest diagonal entry of K = −L/dt² assembled independently
+        (`_assemble_K`) from c = h/d² on a random grid with dx ≠ dy;
+    (b) closed form: constant vector depth (h1, h2), h1 ≠ h2, dx ≠ dy ⇒ ρ_G = 4(h1/dx² + h2/dy²)
+        (a dx↔dy or h1↔h2 swap, or a dropped factor 2, changes it);
+    (c) it is a bound: ρ_G ≥ every Gershgorin row sum Σ_j |K_kj| ≥ λ_max(K) (eigvalsh), so
+        2/√ρ_G ≤ the exact threshold 2/√λ_max."""
+    rng = np.random.default_rng(12)
+    ny, nx, dx, dy = 9, 12, 0.07, 0.03
+    h1 = rng.uniform(0.2, 3.0, (ny, nx - 1))
+    h2 = rng.uniform(0.2, 3.0, (ny - 1, nx))
+    K, _ = _assemble_K(h1 / dx ** 2, h2 / dy ** 2)
+    rho_g = 2.0 * np.max(np.diag(K))
+    dt_g = oracle.gershgorin_dt_max(2, h1, h2, dx, dy)
+    assert abs(dt_g - 2.0 / math.sqrt(rho_g)) <= 4e-16 * dt_g
+    assert np.max(np.sum(np.abs(K), axis=1)) <= rho_g * (1 + 1e-15)
+    lam = np.linalg.eigvalsh(K).max()
+    assert dt_g <= 2.0 / math.sqrt(lam)
+    # the boundary-adjacent rows count all four faces: a face on the Dirichlet ring can hold the max
+    h1b = h1.copy()
+    h1b[4, 0] = 50.0                                  # face (½, 4): between ring node 0 and node 1
+    Kb, _ = _assemble_K(h1b / dx ** 2, h2 / dy ** 2)
+    assert abs(oracle.gershgorin_dt_max(2, h1b, h2, dx, dy) - 2.0 / math.sqrt(2.0 * np.max(np.diag(Kb)))) <= 4e-16 * dt_g
+    # (b) closed form
+    a, b = 1.7, 0.4
+    dt_c = oracle.gershgorin_dt_max(2, np.full((ny, nx - 1), a), np.full((ny - 1, nx), b), dx, dy)
+    assert abs(dt_c - 2.0 / math.sqrt(4.0 * (a / dx ** 2 + b / dy ** 2))) <= 4e-16 * dt_c
+    assert abs(dt_c - 2.0 / math.sqrt(4.0 * (a / dy ** 2 + b / dx ** 2))) > 1e-3 * dt_c     # not symmetric
+    # 1D: ρ_G = 2(h_{i−½} + h_{i+½})/dx², closed form 4h/dx²
+    assert abs(oracle.gershgorin_dt_max(1, np.full(nx - 1, a), None, dx, dx) - dx / math.sqrt(a)) <= 4e-16
+
+
 def test_exact_lattice_speed():
     cfg = inputs.config(1)
     _, _, c1, _ = oracle.member_coefficients(cfg, 0, np.float64)
