@@ -10,6 +10,7 @@ import torch
 import torch.distributed as dist
 
 from paper_2005_11931_b200 import inputs, parallel, tsw
+from tests.helpers import check_slabs_against_oracle, slab_record
 
 
 def lockstep(rank, world, fn):
@@ -44,7 +45,7 @@ def main():
         done += used[0]
         ops += 1
     E = lockstep(rank, world, lambda: s.energy())
-    mine = (s.r0, s.read(0), s.read(1), E, tsw.tsw_peer_state(s.ctx))
+    mine = (s.r0, s.read(0), s.read(1), E, tsw.tsw_peer_state(s.ctx), slab_record(s))
     allp = [None] * world
     dist.all_gather_object(allp, mine)
     if rank == 0:
@@ -54,10 +55,11 @@ def main():
         ref.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
         ref.step(nsteps)
         g, gp = ref.read(0), ref.read(1)
-        for r0, a, b, _, state in allp:
+        for r0, a, b, _, state, _ in allp:
             assert np.array_equal(a, g[:, r0:r0 + a.shape[1]]), f"u^n slab at row {r0}"
             assert np.array_equal(b, gp[:, r0:r0 + b.shape[1]]), f"u^(n-1) slab at row {r0}"
             assert state[3] == 0, "a waiter timed out"
+        check_slabs_against_oracle([p[5] for p in allp], cfg, "f64", nsteps, u0)
         Es = sum(p[3] for p in allp)
         np.testing.assert_allclose(Es, ref.energy(), rtol=1e-12)
         print(f"peer-ipc ok K={K} steps={nsteps} ops={ops}", flush=True)

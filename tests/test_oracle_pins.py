@@ -465,3 +465,26 @@ def test_window_value_matches_full_run():
                               lambda j0, rows, i0, cols: inputs.uniform_dense_rows(96, 80, j0, rows)[:, i0:i0 + cols])
     for k, (j, i) in enumerate(samples):
         assert got[k] == full[j, i]
+
+
+def test_row_band_windows_match_full_run():
+    """Row bands stepped on their light-cone windows (band ± (nsteps + 1) rows, full width) — the
+    decomposition the full-grid config-4 parity test uses — reproduce the full-grid run bitwise
+    (both precisions); a halo of half that does not (the fixed window edge reaches the band: the
+    error front moves one node per level, shrinking by the factor c = dt²h/d² per node, so a
+    halo just short of nsteps + 1 may still round to bitwise equality)."""
+    cfg = inputs.config(3, nx=70, ny=150, dx=0.05, dy=0.05, eps=[0.2], dt=0.01)
+    n = 20
+    for npdt in (np.float64, np.float32):
+        u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(npdt)
+        _, _, c1, c2 = oracle.member_coefficients(cfg, 0, npdt)
+        full, _ = oracle.run(2, c1, c2, u0, None, cfg.dt, n)
+        for halo, exact in ((n + 1, True), (n // 2, False)):
+            same = True
+            for j0 in range(0, cfg.ny, 37):
+                j1 = min(cfg.ny, j0 + 37)
+                w0, w1 = max(0, j0 - halo), min(cfg.ny, j1 + halo)
+                un, _ = oracle.run(2, np.ascontiguousarray(c1[w0:w1]), np.ascontiguousarray(c2[w0:w1 - 1]),
+                                   np.ascontiguousarray(u0[w0:w1]), None, cfg.dt, n)
+                same &= bool(np.array_equal(un[j0 - w0:j1 - w0], full[j0:j1]))
+            assert same == exact, (npdt, halo)

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from paper_2005_11931_b200 import inputs, tsw
+from tests.helpers import check_slabs_against_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -52,6 +53,7 @@ def test_peer_halo_slabs_bitwise(P, K, ny):
         assert np.array_equal(p.read(0), g[:, p.r0:p.r0 + p.ny_local]), (P, K, ny, p.rank)
         assert np.array_equal(p.read(1), gp[:, p.r0:p.r0 + p.ny_local])
         assert tsw.tsw_peer_state(p.ctx)[3] == 0
+    check_slabs_against_oracle(parts, cfg, "f64", n, u0)
     # energy is a ghost-reading collective (one epoch per rank) returning the slab's share
     E = sum(p.energy() for p in parts)
     np.testing.assert_allclose(E, ref.energy(), rtol=1e-12)
@@ -76,5 +78,7 @@ def test_peer_halo_bench_shape_sampled(K, n):
     tsw.tsw_group_step([p.ctx for p in parts], n)
     for p in parts:
         assert np.array_equal(p.read(0), g[:, p.r0:p.r0 + p.ny_local])
+    check_slabs_against_oracle(parts, cfg, "f64", n, u0)
+    for p in parts:
         p.close()
     ref.close()

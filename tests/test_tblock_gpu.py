@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 from paper_2005_11931_b200 import inputs, tsw
-from tests.helpers import NP, host_cores
+from tests.helpers import NP, check_slabs_against_oracle, host_cores
 
 pytestmark = pytest.mark.gpu
 oracle.set_threads(host_cores())
@@ -134,6 +134,7 @@ def test_tblock_loopback_slabs_bitwise(P, K, ny):
     for p in parts:
         assert np.array_equal(p.read(0), g[:, p.r0:p.r0 + p.ny_local])
         assert np.array_equal(p.read(1), gp[:, p.r0:p.r0 + p.ny_local])
+    check_slabs_against_oracle(parts, cfg, "f64", n, u0)
     E = sum(p.energy() for p in parts)
     np.testing.assert_allclose(E, ref.energy(), rtol=1e-12)
     for p in parts:
