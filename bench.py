@@ -84,9 +84,22 @@ SM_MAX_MHZ = _sm_max_mhz()
 
 
 def alu_peak(dtype: str) -> float:
-    """Non-FMA arithmetic roof in TFLOP/s: 64 fp64 / 128 fp32 lanes per clock per SM,
-    148 SMs, maximum SM clock."""
+    """Derived non-FMA arithmetic roof in TFLOP/s: 64 fp64 / 128 fp32 lanes per clock per
+    SM, 148 SMs, maximum SM clock — the fallback when the probe is unavailable."""
     return (64.0 if dtype == "f64" else 128.0) * 148 * SM_MAX_MHZ * 1e6 / 1e12
+
+
+def alu_roof(dtype: str, device: int):
+    """(TOP/s, source) of the ALU roof: measured on this GPU by tsw_alu_probe (independent
+    non-contracted add/multiply chains on every SM, best of 3), else the derived figure."""
+    try:
+        from paper_2005_11931_b200 import tsw
+        v = tsw.tsw_alu_probe(device, tsw.TSW_F64 if dtype == "f64" else tsw.TSW_F32) / 1e12
+        return v, ("measured (tsw_alu_probe: %s add/mul chains on all SMs, best of 3; derived nominal %.2f)"
+                   % (dtype, alu_peak(dtype)))
+    except Exception as e:  # noqa: BLE001 — reported in the line
+        return alu_peak(dtype), "derived (probe failed: %s): %d lanes/clk/SM x 148 SMs x %.0f MHz" % (
+            e, 64 if dtype == "f64" else 128, SM_MAX_MHZ)
 
 
 def ncu_traffic(dtype: str, workload: str, tblock: int = 1, kernel: str = ""):
@@ -473,6 +486,9 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
+    # S5 in every timed region: the energy cadence is capped at the step count (an energy call
+    # at the end of the timed steps even for --steps < --energy-every)
+    cadence = min(args.energy_every, args.steps) if args.energy_every > 0 else 0
 
     import torch
     import torch.distributed as dist
@@ -534,10 +550,10 @@ def main():
         ev0.record(stream)
         done = 0
         while done < args.steps:
-            k = min(args.energy_every, args.steps - done) if args.energy_every > 0 else args.steps - done
+            k = min(cadence, args.steps - done) if cadence > 0 else args.steps - done
             s.step(k)
             done += k
-            if args.energy_every > 0 and done % args.energy_every == 0:
+            if cadence > 0 and done % cadence == 0:
                 s.energy()
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -548,7 +564,18 @@ def main():
         ms = ev0.elapsed_time(ev1)
         launches = s.launches() - l0
         kms, klaunch, kupd = s.kernel_stats()
+        lms, llev, lupd = s.kernel_launches()
         s.set_option(tsw.TSW_OPT_TIME_KERNELS, 0)
+        # the dominant kernel: the launches of the full depth (K-level passes; a call's shallower
+        # remainder pass is reported separately, not averaged in)
+        full_k = int(llev.max()) if len(llev) else 1
+        sel = llev == full_k
+        pass_ms = float(lms[sel].mean()) if sel.any() else kms / max(klaunch, 1)
+        pass_upd = float(lupd[sel].mean()) if sel.any() else kupd / max(klaunch, 1)
+        if world > 1:
+            t = torch.tensor([pass_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pass_ms = float(t[0])
         if world > 1:
             t = torch.tensor([ms, kms / max(klaunch, 1)], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -557,7 +584,9 @@ def main():
             kavg = kms / max(klaunch, 1)
         updates = (cfg.nx - 2) * (cfg.ny - 2) * cfg.batch * args.steps
         res = {"ms": ms, "value": updates / (ms * 1e-3) / 1e9, "launches": launches, "kernel_avg_ms": kavg,
-               "kernel_updates_per_launch": kupd / max(klaunch, 1), "clocks": clocks.stop() if clocks else None}
+               "kernel_updates_per_launch": kupd / max(klaunch, 1), "clocks": clocks.stop() if clocks else None,
+               "pass_levels": full_k, "pass_ms": pass_ms, "pass_updates": pass_upd,
+               "pass_count": int(sel.sum()), "timed_launch_levels": [int(x) for x in llev]}
         if full and not args.no_e2e:
             # e2e through the public API with host buffers: H2D of u0 (pinned), K steps (+ energy),
             # D2H of u^K — all inside the timed region.
@@ -569,10 +598,10 @@ def main():
             s.set_initial(u0_host.numpy(), None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
             done = 0
             while done < args.steps:
-                k = min(args.energy_every, args.steps - done) if args.energy_every > 0 else args.steps - done
+                k = min(cadence, args.steps - done) if cadence > 0 else args.steps - done
                 s.step(k)
                 done += k
-                if args.energy_every > 0 and done % args.energy_every == 0:
+                if cadence > 0 and done % cadence == 0:
                     s.energy()
             s.read(0, out_host.numpy())
             el = time.perf_counter() - t0
@@ -593,6 +622,7 @@ def main():
 
     # slabs exchange K ghost rows of both levels every K levels
     tblock = args.tblock or TB_DEFAULT[args.dtype]
+    roofs = {dt: alu_roof(dt, local) for dt in ("f64", "f32")}
     main_res = run(args.dtype, True, tblock)
     other = "f32" if args.dtype == "f64" else "f64"
     tblock_other = args.tblock or TB_DEFAULT[other]
@@ -606,23 +636,25 @@ def main():
         esz = ESZ[args.dtype]
         # algorithmic bytes per point-update: 3 words per step; with temporal
         # blocking, (2 reads + 2 writes) per pass (words_per_update)
-        words = words_per_update(args.steps, args.energy_every, tblock)
-        upd_s = main_res["kernel_updates_per_launch"] / (main_res["kernel_avg_ms"] * 1e-3)
-        achieved = upd_s * words * esz / 1e9
+        words = words_per_update(args.steps, cadence, tblock)
+        # the dominant kernel: the full-depth launches (K-level passes; a call's shallower remainder
+        # pass is not averaged in), live CUDA-event times on the ctx stream
+        kp = main_res["pass_levels"]
+        upd_s = main_res["pass_updates"] / (main_res["pass_ms"] * 1e-3)
+        words_pass = 4.0 / kp if kp > 1 else 3.0           # algorithmic words per update in one launch
+        achieved = upd_s * words_pass * esz / 1e9
         wl = workload_name(cfg, world)
         traffic = ncu_traffic(args.dtype, wl, tblock)
         hbm_frac = achieved / peak
-        # ALU roof: 64 fp64 / 128 fp32 non-FMA lanes per clock per SM x 148 SMs at the
-        # maximum SM clock; 14 non-contracted operations per update (canonical tree)
-        fp_peak = alu_peak(args.dtype)
+        # ALU roof: the measured non-contracted add/multiply rate of this GPU (tsw_alu_probe) against
+        # the 14 operations per update of the canonical tree (algorithmic count)
+        fp_peak, fp_src = roofs[args.dtype]
         alu_ach = upd_s * 14 / 1e12
         alu_frac = alu_ach / fp_peak
         hbm_obj = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": hbm_frac,
                    "traffic": traffic, "algorithmic_bytes_per_update": words * esz, "peak_source": peak_src}
         alu_obj = {"bound": "alu", "achieved": alu_ach, "peak": fp_peak, "unit": "TFLOP/s", "frac": alu_frac,
-                   "traffic": traffic, "ops_per_update": 14,
-                   "peak_source": "derived (DESIGN.md section 6): %d %s lanes/clk/SM x 148 SMs x %.0f MHz" %
-                                  (64 if args.dtype == "f64" else 128, args.dtype, SM_MAX_MHZ)}
+                   "traffic": traffic, "ops_per_update": 14, "peak_source": fp_src}
         # the binding roof is the one the kernel is closer to; the other is reported beside it
         roof, other_view = (alu_obj, hbm_obj) if alu_frac > hbm_frac else (hbm_obj, alu_obj)
         line = {
@@ -633,7 +665,7 @@ def main():
             "config": {"workload": wl, "nx": cfg.nx, "ny_global": cfg.ny, "rows_per_gpu": cfg.ny // world,
                        "batch": cfg.batch, "dx": cfg.dx, "dt": cfg.dt,
                        "eps": cfg.eps[0] if cfg.batch == 1 else [min(cfg.eps), max(cfg.eps)],
-                       "energy_every": args.energy_every,
+                       "energy_every": cadence,
                        "temporal_blocking": tblock,
                        "parallelism": (f"row-slab x{world} (" + ("peer-store ghost rows fused into the stencil, NVLink"
                                                                   if halo_used[0] == "peer" else "NCCL ghost rows") + ")")
@@ -645,7 +677,10 @@ def main():
             "roofline": {**roof,
                          "kernel": ("k_step2d_tma (S3 leapfrog, one level per pass)" if tblock == 1 else
                                     f"k_step2d_tb (S3 leapfrog, K={tblock} levels per HBM pass)"),
-                         "kernel_avg_ms": main_res["kernel_avg_ms"],
+                         "kernel_avg_ms": main_res["pass_ms"], "kernel_levels": kp,
+                         "kernel_launches_timed": main_res["pass_count"],
+                         "timed_launch_levels": main_res["timed_launch_levels"],
+                         "all_launches_avg_ms": main_res["kernel_avg_ms"],
                          "per_step_roofline_gpts": peak / (3 * esz),
                          ("alu_view" if roof is hbm_obj else "hbm_view"): other_view},
             "gpu_launches": main_res["launches"],
@@ -660,12 +695,14 @@ def main():
             line["e2e"] = main_res["e2e"]
         if also:
             e2 = ESZ[other]
-            words2 = words_per_update(args.steps, args.energy_every, tblock_other)
-            upd2 = also["kernel_updates_per_launch"] / (also["kernel_avg_ms"] * 1e-3)
-            ach2 = upd2 * words2 * e2 / 1e9
+            words2 = words_per_update(args.steps, cadence, tblock_other)
+            kp2 = also["pass_levels"]
+            upd2 = also["pass_updates"] / (also["pass_ms"] * 1e-3)
+            ach2 = upd2 * (4.0 / kp2 if kp2 > 1 else 3.0) * e2 / 1e9
             line["also"] = {"dtype": other, "value": also["value"], "unit": UNIT, "temporal_blocking": tblock_other,
                             "ms_per_step": also["ms"] / args.steps, "roofline_frac": ach2 / peak, "achieved_gbs": ach2,
-                            "alu_frac": upd2 * 14 / 1e12 / alu_peak(other)}
+                            "alu_frac": upd2 * 14 / 1e12 / roofs[other][0], "kernel_avg_ms": also["pass_ms"],
+                            "alu_peak": roofs[other][0]}
         if per_step:
             ach1 = per_step["kernel_updates_per_launch"] * 3 * esz / (per_step["kernel_avg_ms"] * 1e-3) / 1e9
             line["per_step_kernel"] = {"kernel": "k_step2d_tma", "value": per_step["value"], "unit": UNIT,

@@ -295,6 +295,19 @@ tsw_status tsw_check_guards(tsw_ctx* ctx, int64_t* bad_bytes, int64_t* checked_b
  * Synchronises.  Any pointer may be NULL. */
 tsw_status tsw_kernel_stats(tsw_ctx* ctx, double* total_ms, int64_t* launches, int64_t* updates);
 
+/* Per-launch view of the same timed launches: for launch k < min(count, cap), its device
+ * milliseconds ms[k], the levels it advanced levels[k] (K for a temporally blocked pass, 1 for a
+ * one-level step) and its interior point-updates updates[k]; *count = number of timed launches.
+ * cap = 0 only queries the count.  Synchronises. */
+tsw_status tsw_kernel_launches(tsw_ctx* ctx, int64_t cap, double* ms, int32_t* levels, int64_t* updates,
+                               int64_t* count);
+
+/* Measurement helper for the roofline (not a paper operation): the device's non-contracted
+ * add/multiply throughput in the given dtype (TSW_F64 / TSW_F32), operations per second, from a
+ * kernel of independent (x + b)·a − b chains (two adds per multiply, the stencil's mix) on every
+ * SM; best of three timed launches after a warm-up.  Allocates and frees its own memory. */
+tsw_status tsw_alu_probe(int device, int dtype, double* ops_per_s);
+
 /* NCCL row-slab plumbing.  tsw_nccl_unique_id writes a 128-byte ncclUniqueId
  * (call on rank 0, broadcast it, e.g. with torch.distributed); tsw_nccl_init creates the ctx's
  * communicator over grid.nranks ranks.  libnccl.so.2 is resolved at run time. */

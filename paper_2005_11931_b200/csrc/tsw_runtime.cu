@@ -237,6 +237,7 @@ struct tsw_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     int64_t timed_launches = 0, timed_updates = 0;
+    std::vector<std::pair<int32_t, int64_t>> timed_meta;  // per timed launch: levels, point-updates
     // slabs: exchange stream + events (boundary rows → exchange ∥ interior rows)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
@@ -273,6 +274,12 @@ void drop_graphs(tsw_ctx* c) {
 }
 
 // ---- live kernel timing ----------------------------------------------------------------------
+void note_timed(tsw_ctx* c, int32_t levels, int64_t updates) {
+    c->timed_launches++;
+    c->timed_updates += updates;
+    c->timed_meta.emplace_back(levels, updates);
+}
+
 tsw_status timing_events(tsw_ctx* c, cudaEvent_t* e0, cudaEvent_t* e1) {
     while (c->ev_pool.size() < c->ev_used + 2) {
         cudaEvent_t e;
@@ -428,8 +435,7 @@ tsw_status implicit_level_scan_t(tsw_ctx* c, bool start) {
         CKL();
         if (c->timing) {
             CK(cudaEventRecord(e1, c->stream));
-            c->timed_launches++;
-            c->timed_updates += int64_t(m) * my * c->g.batch;
+            note_timed(c, 1, int64_t(m) * my * c->g.batch);
         }
         c->launches += 4;
         std::swap(c->ic, c->ip);
@@ -481,8 +487,7 @@ tsw_status implicit_level_scan_t(tsw_ctx* c, bool start) {
             CKL();
             if (c->timing) {
                 CK(cudaEventRecord(e1, c->stream));
-                c->timed_launches++;
-                c->timed_updates += int64_t(m) * my * c->g.batch;
+                note_timed(c, 1, int64_t(m) * my * c->g.batch);
             }
             c->launches += 2;
             std::swap(c->ic, c->ip);
@@ -677,8 +682,7 @@ tsw_status launch_step2d_t(tsw_ctx* c, int32_t s_lo, int32_t s_hi) {
     CKL();
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
-        c->timed_launches++;
-        c->timed_updates += rows * (c->g.nx - 2) * c->g.batch;
+        note_timed(c, 1, rows * (c->g.nx - 2) * c->g.batch);
     }
     c->launches++;
     return TSW_OK;
@@ -697,11 +701,7 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
     const bool peer = peer_mode(c);
     int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K][NC == 8 ? 1 : 0];
     if (occ == 0) {
-        for (auto fn : {k_step2d_tb<T, K, false, NC>, k_step2d_tb<T, K, true, NC>}) {
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        }
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2d_tb<T, K, false, NC>, NC * 32, smem));
+        CK((tb_setup<T, K, NC>(smem, &occ)));
         if (occ < 1) return fail(TSW_ERR_ARG, "temporally blocked stencil (K=%d) does not fit on an SM", K);
     }
     TbArgs<T> a;
@@ -763,15 +763,10 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
     const bool top = s_lo <= a.push_top || (rows2 > 0 && s_lo2 <= a.push_top);
     const bool bot = s_hi - 1 >= a.push_bot || (rows2 > 0 && s_hi2 - 1 >= a.push_bot);
     const bool push = peer && ((has_nb(c, 0) && top) || (has_nb(c, 1) && bot));
-    if (push)
-        k_step2d_tb<T, K, true, NC><<<unsigned(blocks), NC * 32, smem, c->stream>>>(a, depth);
-    else
-        k_step2d_tb<T, K, false, NC><<<unsigned(blocks), NC * 32, smem, c->stream>>>(a, depth);
-    CKL();
+    CK((tb_launch<T, K, NC>(push, unsigned(blocks), smem, c->stream, a, depth)));
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
-        c->timed_launches++;
-        c->timed_updates += rows * (c->g.nx - 2) * c->g.batch * K;
+        note_timed(c, K, rows * (c->g.nx - 2) * c->g.batch * K);
     }
     c->launches++;
     return TSW_OK;
@@ -1012,8 +1007,7 @@ tsw_status step1d_t(tsw_ctx* c, int64_t k) {
         CKL();
         if (c->timing) {
             CK(cudaEventRecord(e1, c->stream));
-            c->timed_launches++;
-            c->timed_updates += k * (c->g.nx - 2) * c->g.batch;
+            note_timed(c, int32_t(k), k * (c->g.nx - 2) * c->g.batch);
         }
         c->launches++;
         c->n += k;  // the kernel writes the newest level back into buf[ic]
@@ -1532,6 +1526,43 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
 // =============================================================================================
 // ABI
 // =============================================================================================
+namespace {
+template <typename T>
+tsw_status alu_probe_t(int device, double* ops_per_s) {
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    T* out = nullptr;
+    CK(cudaMalloc(&out, 256 * sizeof(T)));
+    const int blocks = sms * 8, iters = sizeof(T) == 8 ? 20000 : 40000;
+    k_alu_probe<T><<<blocks, 256, 0, s>>>(out, iters / 10, T(1), T(0.5));   // warm-up, clocks ramp
+    CKL();
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaEventRecord(e0, s));
+        k_alu_probe<T><<<blocks, 256, 0, s>>>(out, iters, T(1), T(0.5));
+        CKL();
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    *ops_per_s = double(blocks) * 256.0 * iters * 24.0 / (double(best) * 1e-3);
+    cudaFree(out);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    return TSW_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* tsw_version(void) { return "tsw 0.1 (sm_100a)"; }
@@ -2560,6 +2591,7 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         c->ev_used = 0;
         c->timed_launches = 0;
         c->timed_updates = 0;
+        c->timed_meta.clear();
         return TSW_OK;
     }
     return fail(TSW_ERR_ARG, "unknown option %d", key);
@@ -2740,6 +2772,29 @@ tsw_status tsw_kernel_stats(tsw_ctx* c, double* total_ms, int64_t* launches, int
     if (launches) *launches = c->timed_launches;
     if (updates) *updates = c->timed_updates;
     return TSW_OK;
+}
+
+tsw_status tsw_kernel_launches(tsw_ctx* c, int64_t cap, double* ms, int32_t* levels, int64_t* updates,
+                               int64_t* count) {
+    if (!c || cap < 0 || (cap > 0 && (!ms || !levels || !updates))) return fail(TSW_ERR_ARG, "bad arguments");
+    tsw_status st = set_dev(c);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    const int64_t n = int64_t(c->timed_meta.size());
+    for (int64_t k = 0; k < std::min(n, cap); ++k) {
+        float m = 0.f;
+        CK(cudaEventElapsedTime(&m, c->ev_pool[2 * k], c->ev_pool[2 * k + 1]));
+        ms[k] = m;
+        levels[k] = c->timed_meta[k].first;
+        updates[k] = c->timed_meta[k].second;
+    }
+    if (count) *count = n;
+    return TSW_OK;
+}
+
+tsw_status tsw_alu_probe(int device, int dtype, double* ops_per_s) {
+    if (!ops_per_s || (dtype != TSW_F32 && dtype != TSW_F64)) return fail(TSW_ERR_ARG, "bad arguments");
+    return dtype == TSW_F64 ? alu_probe_t<double>(device, ops_per_s) : alu_probe_t<float>(device, ops_per_s);
 }
 
 tsw_status tsw_nccl_unique_id(void* out) {

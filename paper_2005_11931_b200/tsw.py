@@ -43,7 +43,7 @@ STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STA
 # every symbol include/tsw.h declares (tests check the library exports all of them)
 EXPORTS = ["tsw_create", "tsw_destroy", "tsw_set_coeff", "tsw_set_coeff_faces", "tsw_set_coeff_profile", "tsw_read_faces", "tsw_set_initial", "tsw_step",
            "tsw_group_step", "tsw_energy", "tsw_wave2", "tsw_read", "tsw_family_l2", "tsw_field_norms", "tsw_coeff_norms", "tsw_set_state", "tsw_info", "tsw_sync",
-           "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_check_guards", "tsw_peer_export", "tsw_peer_import", "tsw_peer_attach", "tsw_peer_state", "tsw_step_op", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
+           "tsw_launch_count", "tsw_set_option", "tsw_kernel_stats", "tsw_kernel_launches", "tsw_alu_probe", "tsw_check_guards", "tsw_peer_export", "tsw_peer_import", "tsw_peer_attach", "tsw_peer_state", "tsw_step_op", "tsw_nccl_unique_id", "tsw_nccl_init", "tsw_last_error",
            "tsw_version"]
 
 
@@ -109,6 +109,8 @@ def load(path: Optional[str] = None):
         "tsw_launch_count": (i64, [vp]),
         "tsw_set_option": (i32, [vp, i32, i64]),
         "tsw_kernel_stats": (i32, [vp, ctypes.POINTER(d), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "tsw_kernel_launches": (i32, [vp, i64, vp, vp, vp, ctypes.POINTER(i64)]),
+        "tsw_alu_probe": (i32, [i32, i32, ctypes.POINTER(d)]),
         "tsw_check_guards": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "tsw_nccl_unique_id": (i32, [vp]),
         "tsw_nccl_init": (i32, [vp, vp]),
@@ -313,6 +315,25 @@ def tsw_kernel_stats(ctx) -> Tuple[float, int, int]:
     return ms.value, n.value, u.value
 
 
+def tsw_kernel_launches(ctx):
+    """Per timed launch: (ms [n], levels [n], point-updates [n]) numpy arrays."""
+    n = ctypes.c_int64()
+    _check(load().tsw_kernel_launches(ctx, 0, None, None, None, ctypes.byref(n)), ctx)
+    ms = np.zeros(n.value, dtype=np.float64)
+    lv = np.zeros(n.value, dtype=np.int32)
+    up = np.zeros(n.value, dtype=np.int64)
+    _check(load().tsw_kernel_launches(ctx, n.value, ms.ctypes.data, lv.ctypes.data, up.ctypes.data,
+                                      ctypes.byref(n)), ctx)
+    return ms, lv, up
+
+
+def tsw_alu_probe(device: int, dtype: int) -> float:
+    """Measured non-contracted add/multiply throughput of the device in dtype (operations/s)."""
+    v = ctypes.c_double()
+    _check(load().tsw_alu_probe(int(device), int(dtype), ctypes.byref(v)))
+    return v.value
+
+
 def tsw_check_guards(ctx) -> Tuple[int, int]:
     """(guard bytes changed since TSW_OPT_GUARD_CHECK filled them, guard bytes inspected)."""
     n, m = ctypes.c_int64(), ctypes.c_int64()
@@ -470,6 +491,9 @@ class Solver:
 
     def kernel_stats(self):
         return tsw_kernel_stats(self.ctx)
+
+    def kernel_launches(self):
+        return tsw_kernel_launches(self.ctx)
 
     def check_guards(self) -> Tuple[int, int]:
         return tsw_check_guards(self.ctx)
