@@ -241,6 +241,11 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               (256-column strips: less redundant halo work on narrow grids), 0 (default):
                               4 where its strips compute ≥ 5 % fewer columns, and for a slab's launch of
                               its first / last K rows; else 8 */
+#define TSW_OPT_ENERGY_FUSE 14 /* 1 (default): on a single-rank 2D temporally blocked run, the last pass of
+                              every tsw_step call also reduces the discrete energy of the two levels it
+                              writes (S5 fused into S3: per-item fp64 partials, plus the faces across its
+                              strip / chunk seams from a small kernel); tsw_energy at that level then
+                              only reads the result.  0: tsw_energy always runs the standalone kernel */
 #define TSW_OPT_IMPLICIT_XROWS 12 /* rows per iteration of the implicit x-line solve: 1 (default; LU tables
                               in registers) or 2 (the two rows' scan chains interleave, tables in shared
                               memory — measured 4 % slower at 4096², kept for comparison) */

@@ -553,6 +553,9 @@ struct TbArgs {
     T* pd_km1 = nullptr;
     int64_t pu_mstride = 0, pd_mstride = 0;
     int32_t push_top = 0, push_bot = INT32_MAX;
+    // fused discrete energy (EN variant, S5 / R17, node form R30): one fp64 partial per item of
+    // Σ over its output nodes of (u^{n+K} − u^{n+K−1})² − u^{n+K}·L(u^{n+K−1})
+    double* en_part = nullptr;
 };
 
 // centre-row buffers are padded by one 16-byte vector on each side (zeros), so the left/right
@@ -635,6 +638,18 @@ struct TbState {
     bool colint[V];
 };
 
+// Fused energy (EN).  E^{n+½} = (dx·dy/dt²)·[Σ_nodes (u^{n+1} − u^n)² + Σ_faces c·Δu^{n+1}·Δu^n]
+// (R17) in its node form: with K̃ = −L symmetric and u = 0 on the Dirichlet ring, summation by parts
+// turns the face sum into ⟨u^{n+1}, K̃u^n⟩ = −Σ_nodes u^{n+1}·(L u^n) (reading R30).  At level K of a
+// pass the stencil has just evaluated L(u^{n+K−1}) at every node of u^{n+K}, so the energy of the
+// pass's outputs is a per-node sum — no neighbours, no seams.  fp64: the stencil's own L; fp32: L
+// re-evaluated in fp64 from the same fp32 values (an fp32 L loses digits to cancellation).
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // One input row of the wavefront.  `cr` / `cw`: this thread's element in the centre-row buffers
 // of the previous / current row parity (level m at offset m·2·WEP).  MASKED: force the Dirichlet
 // rows/columns to +0 (only items whose dependency cone touches them need it).
@@ -661,10 +676,11 @@ __device__ __forceinline__ void tb_edge_store(T* __restrict__ ew, int m, int lan
     ew[m * TbEdge<T, K, NC>::ES] = (lane == 0) ? v[0] : v[1];
 }
 
-template <typename T, int K, int PH, bool MASKED, int NC>
+template <typename T, int K, int PH, bool MASKED, int NC, bool EN = false>
 __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
                                        int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
-                                       T* __restrict__ yc, const T (&lr1)[2], int lane) {
+                                       T* __restrict__ yc, const T (&lr1)[2], int lane, bool en_on = false,
+                                       double* en_acc = nullptr) {
     constexpr int V = 2;
     constexpr bool SH = TbShfl<T>::on;
     constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
@@ -733,6 +749,24 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
             } else {
                 nv[k] = v;
             }
+            if constexpr (EN) {
+                if (m == K && en_on) {
+                    // node form of the energy of (u^{n+K}, u^{n+K−1}) = (nv, cu): (a − b)² − a·L(b)
+                    double lapd;
+                    if constexpr (sizeof(T) == 8) {
+                        lapd = (double)lap;
+                    } else {
+                        const double ul = (k == 0) ? (double)left : (double)S.w[m - 1][N][0];
+                        const double ur = (k == 0) ? (double)S.w[m - 1][N][1] : (double)right;
+                        const double uc = cu, uu = S.w[m - 1][O][k], ud = S.w[m - 1][C][k];
+                        const double cl = (k == 0) ? (double)S.c1l[0] : (double)S.c1r[0];
+                        const double crr = (double)S.c1r[k], c2 = (double)S.c2v[k];
+                        lapd = (crr * (ur - uc) - cl * (uc - ul)) + (c2 * (uu - uc) - c2 * (uc - ud));
+                    }
+                    const double A = (double)nv[k], B = (double)cu;
+                    *en_acc += (A - B) * (A - B) - A * lapd;
+                }
+            }
         }
         if (TbYCache<T>::smem) sts_v2(yc + m * TbGeom<T, K, NC>::NT * V, guv);
         if (m < K) {
@@ -757,7 +791,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
 // The producer is thread 0: after every second input row it refills the two stages consumed by
 // the previous rows (every thread has passed the per-row barrier, so they are free) with the next
 // stages of its stream (needs a ring of ≥ 3 stages).
-template <typename T, int K, bool PEER = false, int NC = TB_NC>
+template <typename T, int K, bool PEER = false, int NC = TB_NC, bool EN = false>
 __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K, NC>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
@@ -777,6 +811,7 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
     T* ycache = reinterpret_cast<T*>(reinterpret_cast<char*>(full) + ((size_t(depth) * sizeof(uint64_t) + 15) / 16) * 16) +
                 tid * V;
     for (int e = tid; e < int(CEN_ELEMS); e += blockDim.x) cenp[e] = (T)0;  // pads stay 0
+    __shared__ double en_red[EN ? NC : 1];   // EN: per-item warp sums
     if (tid == 0) {
         for (int k = 0; k < depth; ++k) mbar_init(&full[k], 1);
         fence_barrier_init();
@@ -839,6 +874,7 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
     uint32_t cphase = 0;
     int pending = 0;  // the previous row consumed a stage that is not yet refilled
     TbState<T, K> S;
+    double en_acc = 0.0;   // EN: this thread's sum over its output nodes of the current item
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
         int64_t cs;
         int s0, s1, b, in_lo, in_hi;
@@ -932,7 +968,9 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
                 for (int k = 0; k < V; ++k) nw[k] = pv_new[k] = (T)0;
             }
             T lastk[V];
-            tb_row<T, K, PH, MASKED, NC>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1, lane);
+            const bool en_on = EN && out_cols && (R - K >= s0) && (R - K < s1);
+            tb_row<T, K, PH, MASKED, NC, EN>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1, lane, en_on,
+                                            &en_acc);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
                 // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH
@@ -995,6 +1033,18 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             else
                 run_rows(std::integral_constant<bool, true>{}, lo, hi);
         }
+        if constexpr (EN) {
+            const double v = warp_sum_d(en_acc);
+            en_acc = 0.0;
+            if (lane == 0) en_red[warp] = v;
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < NC; ++w) t += en_red[w];
+                a.en_part[item] = t;
+            }
+        }
     }
 }
 
@@ -1002,7 +1052,8 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
 template <typename T, int K, int NC>
 cudaError_t tb_setup(size_t smem, int* occ);
 template <typename T, int K, int NC>
-cudaError_t tb_launch(bool push, unsigned blocks, size_t smem, cudaStream_t stream, const TbArgs<T>& a, int depth);
+cudaError_t tb_launch(bool push, bool energy, unsigned blocks, size_t smem, cudaStream_t stream, const TbArgs<T>& a,
+                      int depth);
 
 #ifndef TSW_TB_UNIT  // the rest is compiled in the runtime's translation unit only
 // ------------------------------------------------------------------------------------------
@@ -3219,6 +3270,19 @@ __global__ void k_zero_boundary(T* __restrict__ u, int dim, int64_t nx, int64_t 
         const bool bnd = (i == 0) || (i >= nx - 1) || (dim == 2 && (g == 0 || g == ny - 1));
         if (bnd) ub[s * pitch + i] = (T)0;
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// S5 fused into the temporally blocked pass (EN variant of k_step2d_tb): out[b] = w · Σ of member b's
+// item partials (the node form of the energy, R30), fixed order (one warp per member).
+// ------------------------------------------------------------------------------------------
+__global__ void k_tb_energy_final(const double* __restrict__ items, int64_t per_member, double w,
+                                  double* __restrict__ out) {
+    const int b = blockIdx.x;
+    double v = 0.0;
+    for (int64_t k = threadIdx.x; k < per_member; k += 32) v += items[b * per_member + k];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[b] = w * v;
 }
 
 // ------------------------------------------------------------------------------------------

@@ -238,6 +238,14 @@ struct tsw_ctx {
     size_t ev_used = 0;
     int64_t timed_launches = 0, timed_updates = 0;
     std::vector<std::pair<int32_t, int64_t>> timed_meta;  // per timed launch: levels, point-updates
+    // fused energy (TSW_OPT_ENERGY_FUSE): the last pass of a stepping call reduces E of its outputs
+    bool en_fuse = true;
+    bool en_now = false;          // the next pass carries the energy
+    int64_t en_level = -1;        // level n whose E^{n−½} d_en holds (−1: none)
+    double* d_en = nullptr;       // [items] item partials, then the [B] result
+    size_t en_cap = 0;
+    bool en_pass_done = false;    // set by the pass that reduced it
+    double* en_result = nullptr;  // where that pass left [B] (inside d_en)
     // slabs: exchange stream + events (boundary rows → exchange ∥ interior rows)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
@@ -763,12 +771,36 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
     const bool top = s_lo <= a.push_top || (rows2 > 0 && s_lo2 <= a.push_top);
     const bool bot = s_hi - 1 >= a.push_bot || (rows2 > 0 && s_hi2 - 1 >= a.push_bot);
     const bool push = peer && ((has_nb(c, 0) && top) || (has_nb(c, 1) && bot));
-    CK((tb_launch<T, K, NC>(push, unsigned(blocks), smem, c->stream, a, depth)));
+    const bool energy = c->en_now && c->g.nranks == 1 && rows2 == 0 && !push;
+    double* en_items = nullptr;
+    if (energy) {
+        const size_t need = size_t(a.items) + size_t(c->g.batch);
+        if (need > c->en_cap) {
+            if (c->d_en) CK(cudaFree(c->d_en));
+            c->d_en = nullptr;
+            c->en_cap = 0;
+            CK(cudaMalloc(&c->d_en, need * sizeof(double)));
+            c->en_cap = need;
+        }
+        en_items = c->d_en;
+        a.en_part = en_items;
+    }
+    CK((tb_launch<T, K, NC>(push, energy, unsigned(blocks), smem, c->stream, a, depth)));
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
         note_timed(c, K, rows * (c->g.nx - 2) * c->g.batch * K);
     }
     c->launches++;
+    if (energy) {
+        // fixed-order per-member sum of the item partials (node form of the energy, R30)
+        double* out = en_items + a.items;
+        const double w = c->g.dx * c->g.dy / (c->dt * c->dt);
+        k_tb_energy_final<<<unsigned(c->g.batch), 32, 0, c->stream>>>(en_items, a.strips * a.chunks, w, out);
+        CKL();
+        c->launches += 1;
+        c->en_pass_done = true;
+        c->en_result = out;
+    }
     return TSW_OK;
 }
 
@@ -967,6 +999,10 @@ tsw_status tb_pass(tsw_ctx* c) {
     c->ic = fk;
     c->ip = fkm1;
     c->n += K;
+    if (c->en_pass_done) {
+        c->en_level = c->n;
+        c->en_pass_done = false;
+    }
     return TSW_OK;
 }
 
@@ -1254,6 +1290,7 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
         c->ghosts_valid = true;
     }
     c->n = n;
+    c->en_level = -1;
     c->have_init = true;
     return TSW_OK;
 }
@@ -1502,11 +1539,20 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
         s = 1;
     }
     if (tb_usable(c)) {
-        for (; s + c->tblock <= k; s += c->tblock)
-            if ((st = tb_pass(c))) return st;
+        // the call's last pass (a full one with no remainder after it, or the remainder pass)
+        // carries the fused energy of the level it ends on
+        for (; s + c->tblock <= k; s += c->tblock) {
+            c->en_now = c->en_fuse && s + c->tblock == k;
+            st = tb_pass(c);
+            c->en_now = false;
+            if (st) return st;
+        }
         if (k - s >= 2) {
             DepthScope ds(c, int(k - s));
-            if ((st = tb_pass(c))) return st;
+            c->en_now = c->en_fuse;
+            st = tb_pass(c);
+            c->en_now = false;
+            if (st) return st;
             s = k;
         }
     }
@@ -1678,7 +1724,8 @@ void tsw_destroy(tsw_ctx* c) {
     dfree_guarded(c->h2, c->cshift_h);
     dfree_guarded(c->c1, c->cshift);
     dfree_guarded(c->c2, c->cshift);
-    void* ptrs[] = {c->d_eps, c->d_amp, c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64, c->d_prof, c->d_fam};
+    void* ptrs[] = {c->d_eps, c->d_amp, c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64, c->d_prof, c->d_fam,
+                    c->d_en};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -2087,6 +2134,12 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     if (!c->have_init || c->n < 1) return fail(TSW_ERR_STATE, "energy E^{n-1/2} needs n >= 1");
     tsw_status st = set_dev(c);
     if (st) return st;
+    if (c->en_level == c->n && c->g.nranks == 1 && c->en_result) {
+        // reduced by the pass that wrote u^n, u^{n−1} (TSW_OPT_ENERGY_FUSE)
+        CK(cudaMemcpyAsync(out_B, c->en_result, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return TSW_OK;
+    }
     // peer halos: a ghost-reading collective is an epoch of its own (no neighbour overwrites the
     // ghost rows while they are read)
     if (peer_mode(c) && (st = peer_begin(c, c->stream))) return st;
@@ -2517,6 +2570,12 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
             }
         }
         c->scheme = int(value);
+        return TSW_OK;
+    }
+    if (key == TSW_OPT_ENERGY_FUSE) {
+        if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "energy fuse must be 0 or 1");
+        c->en_fuse = value != 0;
+        c->en_level = -1;
         return TSW_OK;
     }
     if (key == TSW_OPT_HALO) {

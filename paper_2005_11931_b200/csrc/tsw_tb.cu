@@ -13,7 +13,7 @@ namespace tsw {
 
 template <typename T, int K, int NC>
 cudaError_t tb_setup(size_t smem, int* occ) {
-    for (auto fn : {k_step2d_tb<T, K, false, NC>, k_step2d_tb<T, K, true, NC>}) {
+    for (auto fn : {k_step2d_tb<T, K, false, NC>, k_step2d_tb<T, K, true, NC>, k_step2d_tb<T, K, false, NC, true>}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -23,8 +23,11 @@ cudaError_t tb_setup(size_t smem, int* occ) {
 }
 
 template <typename T, int K, int NC>
-cudaError_t tb_launch(bool push, unsigned blocks, size_t smem, cudaStream_t stream, const TbArgs<T>& a, int depth) {
-    if (push)
+cudaError_t tb_launch(bool push, bool energy, unsigned blocks, size_t smem, cudaStream_t stream, const TbArgs<T>& a,
+                      int depth) {
+    if (energy)   // the fused-energy variant (single-rank passes: no pushed rows)
+        k_step2d_tb<T, K, false, NC, true><<<blocks, NC * 32, smem, stream>>>(a, depth);
+    else if (push)
         k_step2d_tb<T, K, true, NC><<<blocks, NC * 32, smem, stream>>>(a, depth);
     else
         k_step2d_tb<T, K, false, NC><<<blocks, NC * 32, smem, stream>>>(a, depth);
@@ -33,7 +36,7 @@ cudaError_t tb_launch(bool push, unsigned blocks, size_t smem, cudaStream_t stre
 
 #define TSW_TB_INST(K, NC)                                                                                   \
     template cudaError_t tb_setup<TSW_TB_DTYPE, K, NC>(size_t, int*);                                        \
-    template cudaError_t tb_launch<TSW_TB_DTYPE, K, NC>(bool, unsigned, size_t, cudaStream_t,                \
+    template cudaError_t tb_launch<TSW_TB_DTYPE, K, NC>(bool, bool, unsigned, size_t, cudaStream_t,          \
                                                         const TbArgs<TSW_TB_DTYPE>&, int);
 #define TSW_TB_INST_K(K) TSW_TB_INST(K, 8) TSW_TB_INST(K, 4)
 TSW_TB_INST_K(2)
