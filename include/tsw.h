@@ -148,8 +148,11 @@ tsw_status tsw_set_initial(tsw_ctx* ctx, const void* u0, const void* u1, double 
 tsw_status tsw_step(tsw_ctx* ctx, int64_t nsteps);
 
 /* Loopback slabs on ONE device: advance ctxs[0..n−1] (ranks 0..n−1 of one decomposition, same
- * device and stream, no NCCL) by nsteps, exchanging ghost rows with device copies.  Test and
- * emulation path for the multi-GPU decomposition. */
+ * device and stream, no NCCL; 1 ≤ n ≤ 64) by nsteps.  Each level / pass runs the same per-rank
+ * phases as tsw_step's NCCL path (boundary rows, exchange on the aux stream after their event,
+ * interior rows, wait) with device copies in place of the NCCL messages; with peer halos
+ * (TSW_OPT_HALO = 1) the ranks' operations are issued epoch by epoch.  Test and emulation path for
+ * the multi-GPU decomposition.  Errors: TSW_ERR_ARG (group shape), TSW_ERR_STATE. */
 tsw_status tsw_group_step(tsw_ctx** ctxs, int32_t n, int64_t nsteps);
 
 /* S5 discrete energy E^{n−1/2} of the current levels (R17; discrete form of CL-01):

@@ -3274,13 +3274,17 @@ __global__ void k_zero_boundary(T* __restrict__ u, int dim, int64_t nx, int64_t 
 
 // ------------------------------------------------------------------------------------------
 // S5 fused into the temporally blocked pass (EN variant of k_step2d_tb): out[b] = w · Σ of member b's
-// item partials (the node form of the energy, R30), fixed order (one warp per member).
+// item partials (the node form of the energy, R30) over the pass's launches (segments: offset,
+// partials per member; a split slab pass has two), fixed order (one warp per member).
 // ------------------------------------------------------------------------------------------
-__global__ void k_tb_energy_final(const double* __restrict__ items, int64_t per_member, double w,
-                                  double* __restrict__ out) {
+__global__ void k_tb_energy_final(const double* __restrict__ part, int nseg, int64_t off0, int64_t pm0, int64_t off1,
+                                  int64_t pm1, double w, double* __restrict__ out) {
     const int b = blockIdx.x;
     double v = 0.0;
-    for (int64_t k = threadIdx.x; k < per_member; k += 32) v += items[b * per_member + k];
+    for (int sg = 0; sg < nseg; ++sg) {
+        const int64_t off = sg ? off1 : off0, pm = sg ? pm1 : pm0;
+        for (int64_t k = threadIdx.x; k < pm; k += 32) v += part[off + b * pm + k];
+    }
     v = warp_sum(v);
     if (threadIdx.x == 0) out[b] = w * v;
 }

@@ -107,6 +107,7 @@ int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
 // are never used and never written).
 constexpr size_t GUARD = 16384;
 constexpr int IMP_SCAN_MAX = 8192;  // unknowns per line of the implicit scan solvers
+constexpr int TSW_GROUP_MAX = 64;   // slabs of one tsw_group_step
 // `shift` bytes: the returned pointer is a VIEW that many bytes into the array (row-structured
 // arrays of slabs with G ghost rows per side are addressed so that storage row 1 is the first owned
 // row; ghost rows sit at rows 0, −1, …, 2 − G).
@@ -244,8 +245,9 @@ struct tsw_ctx {
     int64_t en_level = -1;        // level n whose E^{n−½} d_en holds (−1: none)
     double* d_en = nullptr;       // [items] item partials, then the [B] result
     size_t en_cap = 0;
-    bool en_pass_done = false;    // set by the pass that reduced it
-    double* en_result = nullptr;  // where that pass left [B] (inside d_en)
+    int en_nseg = 0;              // item-partial segments of the current pass (a split pass launches twice)
+    int64_t en_off[2] = {0, 0}, en_pm[2] = {0, 0};   // offset in d_en, partials per member
+    double* en_result = nullptr;  // [B]: E of level en_level (this slab's share before the all-reduce)
     // slabs: exchange stream + events (boundary rows → exchange ∥ interior rows)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
@@ -771,19 +773,25 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
     const bool top = s_lo <= a.push_top || (rows2 > 0 && s_lo2 <= a.push_top);
     const bool bot = s_hi - 1 >= a.push_bot || (rows2 > 0 && s_hi2 - 1 >= a.push_bot);
     const bool push = peer && ((has_nb(c, 0) && top) || (has_nb(c, 1) && bot));
-    const bool energy = c->en_now && c->g.nranks == 1 && rows2 == 0 && !push;
-    double* en_items = nullptr;
+    // fused energy: every launch of the pass writes its item partials as one segment of d_en
+    const bool energy = c->en_now;
     if (energy) {
-        const size_t need = size_t(a.items) + size_t(c->g.batch);
-        if (need > c->en_cap) {
+        if (c->en_nseg >= 2) return fail(TSW_ERR_STATE, "fused energy: more than two launches in a pass");
+        const int64_t off = c->en_nseg ? c->en_off[0] + c->en_pm[0] * c->g.batch : 0;
+        const size_t need = size_t(off + a.items);
+        if (need > c->en_cap) {   // grow, keeping the first segment (stream-ordered copy)
+            double* fresh = nullptr;
+            CK(cudaMalloc(&fresh, need * sizeof(double)));
+            if (off > 0) CK(cudaMemcpyAsync(fresh, c->d_en, size_t(off) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
             if (c->d_en) CK(cudaFree(c->d_en));
-            c->d_en = nullptr;
-            c->en_cap = 0;
-            CK(cudaMalloc(&c->d_en, need * sizeof(double)));
+            c->d_en = fresh;
             c->en_cap = need;
         }
-        en_items = c->d_en;
-        a.en_part = en_items;
+        a.en_part = c->d_en + off;
+        c->en_off[c->en_nseg] = off;
+        c->en_pm[c->en_nseg] = a.strips * a.chunks;
+        c->en_nseg++;
     }
     CK((tb_launch<T, K, NC>(push, energy, unsigned(blocks), smem, c->stream, a, depth)));
     if (c->timing) {
@@ -791,16 +799,6 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
         note_timed(c, K, rows * (c->g.nx - 2) * c->g.batch * K);
     }
     c->launches++;
-    if (energy) {
-        // fixed-order per-member sum of the item partials (node form of the energy, R30)
-        double* out = en_items + a.items;
-        const double w = c->g.dx * c->g.dy / (c->dt * c->dt);
-        k_tb_energy_final<<<unsigned(c->g.batch), 32, 0, c->stream>>>(en_items, a.strips * a.chunks, w, out);
-        CKL();
-        c->launches += 1;
-        c->en_pass_done = true;
-        c->en_result = out;
-    }
     return TSW_OK;
 }
 
@@ -952,58 +950,80 @@ TbSplit tb_split(const tsw_ctx* c) {
     return p;
 }
 
-// One pass of K levels; afterwards u^n = buf[fk], u^{n−1} = buf[fkm1].  Slabs: the first/last K
-// owned rows first, then their K-row exchange (both levels) on the aux stream concurrently with
-// the interior rows (k-deep halos, one exchange per K levels).
-tsw_status tb_pass(tsw_ctx* c) {
-    int fk, fkm1;
-    free_pair(c, &fk, &fkm1);
+// Fused energy of a pass (TSW_OPT_ENERGY_FUSE): the launches of the pass wrote their item partials
+// as segments of d_en; one fixed-order sum per member gives this slab's E (node form, R30).
+tsw_status en_pass_finish(tsw_ctx* c) {
+    if (!c->en_now || c->en_nseg == 0) return TSW_OK;
+    if (!c->en_result) CK(cudaMalloc(&c->en_result, sizeof(double) * size_t(c->g.batch)));
+    const double w = c->g.dx * c->g.dy / (c->dt * c->dt);
+    k_tb_energy_final<<<unsigned(c->g.batch), 32, 0, c->stream>>>(c->d_en, c->en_nseg, c->en_off[0], c->en_pm[0],
+                                                                   c->en_off[1], c->en_pm[1], w, c->en_result);
+    CKL();
+    c->launches++;
+    c->en_level = c->n;   // called after the level advanced
+    return TSW_OK;
+}
+
+// A pass of K levels in two phases around the halo exchange (S4): begin launches the
+// rows the neighbours need first — a slab's first / last K owned rows when the slab has ≥ 3K rows
+// (tb_split), else all rows — and records ev_bnd; the caller exchanges K boundary rows of both new
+// levels after ev_bnd (NCCL messages on the aux stream, loopback copies for a group of slabs in one
+// process, nothing for peer halos: the kernel pushed them); end launches the interior rows, makes
+// the ctx stream wait for the exchange's event (if any) and advances to u^n = buf[fk],
+// u^{n−1} = buf[fkm1].  Single rank: begin launches everything, end only advances.
+struct TbPassState {
+    int fk = 0, fkm1 = 0;
+    TbSplit p;
+};
+tsw_status tb_pass_begin(tsw_ctx* c, TbPassState& ps) {
+    free_pair(c, &ps.fk, &ps.fkm1);
+    ps.p = tb_split(c);
+    c->en_nseg = 0;
+    tsw_status st;
+    if (ps.p.split)
+        st = launch_tb_rows(c, ps.fk, ps.fkm1, ps.p.top_lo, ps.p.top_hi, ps.p.bot_lo, ps.p.bot_hi);
+    else
+        st = launch_tb_rows(c, ps.fk, ps.fkm1, c->s_lo, c->s_hi);
+    if (st) return st;
+    if (c->g.nranks > 1) CK(cudaEventRecord(c->ev_bnd, c->stream));
+    return TSW_OK;
+}
+tsw_status tb_pass_end(tsw_ctx* c, const TbPassState& ps, cudaEvent_t comm_done) {
+    tsw_status st;
+    if (ps.p.split && (st = launch_tb_rows(c, ps.fk, ps.fkm1, ps.p.ilo, ps.p.ihi))) return st;
+    if (comm_done) CK(cudaStreamWaitEvent(c->stream, comm_done, 0));
     const int K = c->tblock;
+    if (c->g.nranks > 1) c->gdepth[ps.fk] = c->gdepth[ps.fkm1] = K;
+    c->ic = ps.fk;
+    c->ip = ps.fkm1;
+    c->n += K;
+    return en_pass_finish(c);
+}
+
+// One pass of K levels of one rank: single rank; peer halos (the kernel stores the boundary rows
+// into the neighbours' ghost rows; with a split pass the epoch is published after the first / last
+// K rows, before the interior, which reads no ghost rows — so the neighbours' next pass may start
+// while the interior still runs); NCCL (the K-row exchange of both levels on the aux stream,
+// concurrently with the interior rows: SURVEY §8(f) NEXT 4, one exchange per K levels).
+tsw_status tb_pass(tsw_ctx* c) {
+    TbPassState ps;
     tsw_status st;
     if (c->g.nranks == 1) {
-        if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
-    } else if (peer_mode(c)) {
-        // the kernel itself stores the boundary rows into the neighbours' ghost rows.  With a slab
-        // of ≥ 3K rows the first / last K rows go first and the epoch is published before the
-        // interior rows: those read no ghost rows, so the neighbours' next pass may start (and push
-        // into the other buffer pair's ghost rows) while the interior is still running
-        const TbSplit p = tb_split(c);
+        if ((st = tb_pass_begin(c, ps))) return st;
+        return tb_pass_end(c, ps, nullptr);
+    }
+    if (peer_mode(c)) {
         if ((st = peer_begin(c, c->stream))) return st;
-        if (p.split) {
-            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi, p.bot_lo, p.bot_hi))) return st;
-            if ((st = peer_end(c, c->stream))) return st;
-            if ((st = launch_tb_rows(c, fk, fkm1, p.ilo, p.ihi))) return st;
-        } else {
-            if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
-            if ((st = peer_end(c, c->stream))) return st;
-        }
-        c->gdepth[fk] = c->gdepth[fkm1] = K;
-    } else {
-        const TbSplit p = tb_split(c);
-        if (p.split) {
-            if ((st = launch_tb_rows(c, fk, fkm1, p.top_lo, p.top_hi, p.bot_lo, p.bot_hi))) return st;
-            CK(cudaEventRecord(c->ev_bnd, c->stream));
-            CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
-            if ((st = exchange_nccl(c, c->buf[fk], c->aux, K))) return st;
-            if ((st = exchange_nccl(c, c->buf[fkm1], c->aux, K))) return st;
-            CK(cudaEventRecord(c->ev_comm, c->aux));
-            if ((st = launch_tb_rows(c, fk, fkm1, p.ilo, p.ihi))) return st;
-            CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
-        } else {
-            if ((st = launch_tb_rows(c, fk, fkm1, c->s_lo, c->s_hi))) return st;
-            if ((st = exchange_nccl(c, c->buf[fk], c->stream, K))) return st;
-            if ((st = exchange_nccl(c, c->buf[fkm1], c->stream, K))) return st;
-        }
-        c->gdepth[fk] = c->gdepth[fkm1] = K;
+        if ((st = tb_pass_begin(c, ps))) return st;
+        if ((st = peer_end(c, c->stream))) return st;
+        return tb_pass_end(c, ps, nullptr);
     }
-    c->ic = fk;
-    c->ip = fkm1;
-    c->n += K;
-    if (c->en_pass_done) {
-        c->en_level = c->n;
-        c->en_pass_done = false;
-    }
-    return TSW_OK;
+    if ((st = tb_pass_begin(c, ps))) return st;
+    CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
+    if ((st = exchange_nccl(c, c->buf[ps.fk], c->aux, c->tblock))) return st;
+    if ((st = exchange_nccl(c, c->buf[ps.fkm1], c->aux, c->tblock))) return st;
+    CK(cudaEventRecord(c->ev_comm, c->aux));
+    return tb_pass_end(c, ps, c->ev_comm);
 }
 
 tsw_status launch_step2d(tsw_ctx* c, bool start, int32_t s_lo, int32_t s_hi) {
@@ -1333,20 +1353,34 @@ tsw_status launch_interior_rows(tsw_ctx* c, bool start) {
 // One slab level with overlap: boundary rows on the ctx stream, then the NCCL
 // ghost-row exchange of the new level on the aux stream, concurrently with the interior rows;
 // the ctx stream waits for the exchange before the next level reads the ghost rows.
-tsw_status step_slab_overlapped(tsw_ctx* c) {
-    const bool start = (c->n == 0);
-    tsw_status st;
-    if ((st = launch_boundary_rows(c, start))) return st;
+// One level of a slab in two phases around the exchange of its new boundary rows (S4): begin
+// launches the first / last owned rows the neighbours need and records ev_bnd; end launches the
+// interior rows, waits for the exchange's event and advances the level (the new level overwrote
+// u^{n−1} in place: buf[ip]).  step_slab_overlapped (NCCL, one rank per process) and
+// tsw_group_step (loopback copies, P slabs of one process) run the same phases.
+tsw_status slab_level_begin(tsw_ctx* c, bool start) {
+    tsw_status st = launch_boundary_rows(c, start);
+    if (st) return st;
     CK(cudaEventRecord(c->ev_bnd, c->stream));
-    CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
-    if ((st = exchange_nccl(c, c->buf[c->ip], c->aux, 1))) return st;
-    CK(cudaEventRecord(c->ev_comm, c->aux));
-    if ((st = launch_interior_rows(c, start))) return st;
-    CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+    return TSW_OK;
+}
+tsw_status slab_level_end(tsw_ctx* c, bool start, cudaEvent_t comm_done) {
+    tsw_status st = launch_interior_rows(c, start);
+    if (st) return st;
+    if (comm_done) CK(cudaStreamWaitEvent(c->stream, comm_done, 0));
     std::swap(c->ic, c->ip);
     c->gdepth[c->ic] = 1;
     c->n++;
     return TSW_OK;
+}
+tsw_status step_slab_overlapped(tsw_ctx* c) {
+    const bool start = (c->n == 0);
+    tsw_status st;
+    if ((st = slab_level_begin(c, start))) return st;
+    CK(cudaStreamWaitEvent(c->aux, c->ev_bnd, 0));
+    if ((st = exchange_nccl(c, c->buf[c->ip], c->aux, 1))) return st;
+    CK(cudaEventRecord(c->ev_comm, c->aux));
+    return slab_level_end(c, start, c->ev_comm);
 }
 
 // One slab level, peer mode: boundary rows, their push into the neighbours' ghost rows, then the
@@ -1442,7 +1476,10 @@ tsw_status run_peer_op(tsw_ctx* c, PeerOp op, int64_t remaining, int64_t* consum
         case PEER_PASS: {
             DepthScope ds(c, pass_depth(c, remaining));
             *consumed = c->tblock;
-            return tb_pass(c);
+            c->en_now = c->en_fuse && c->tblock == remaining;   // the call's last pass
+            const tsw_status st = tb_pass(c);
+            c->en_now = false;
+            return st;
         }
         default: return TSW_OK;
     }
@@ -1519,11 +1556,18 @@ tsw_status do_steps(tsw_ctx* c, int64_t k) {
         }
         if (tb_usable(c) && pass_depth(c, k - s) >= 2) {
             if ((st = ensure_ghosts_nccl(c, c->tblock))) return st;
-            for (; s + c->tblock <= k; s += c->tblock)
-                if ((st = tb_pass(c))) return st;
+            for (; s + c->tblock <= k; s += c->tblock) {
+                c->en_now = c->en_fuse && s + c->tblock == k;
+                st = tb_pass(c);
+                c->en_now = false;
+                if (st) return st;
+            }
             if (k - s >= 2) {
                 DepthScope ds(c, int(k - s));
-                if ((st = tb_pass(c))) return st;
+                c->en_now = c->en_fuse;
+                st = tb_pass(c);
+                c->en_now = false;
+                if (st) return st;
                 s = k;
             }
         }
@@ -1725,7 +1769,7 @@ void tsw_destroy(tsw_ctx* c) {
     dfree_guarded(c->c1, c->cshift);
     dfree_guarded(c->c2, c->cshift);
     void* ptrs[] = {c->d_eps, c->d_amp, c->d_partial, c->d_out, c->d_argpart, c->d_idx, c->d_u64, c->d_prof, c->d_fam,
-                    c->d_en};
+                    c->d_en, c->en_result};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -2007,7 +2051,7 @@ tsw_status tsw_step_op(tsw_ctx* c, int64_t nsteps, int64_t* consumed) {
 }
 
 tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
-    if (!cs || n < 1) return fail(TSW_ERR_ARG, "bad ctx group");
+    if (!cs || n < 1 || n > TSW_GROUP_MAX) return fail(TSW_ERR_ARG, "bad ctx group (1..%d slabs)", TSW_GROUP_MAX);
     for (int r = 0; r < n; ++r) {
         if (!cs[r] || !cs[r]->have_init) return fail(TSW_ERR_STATE, "group member %d not initialised", r);
         if (cs[r]->g.dim != 2 || cs[r]->g.nranks != n || cs[r]->g.rank != r)
@@ -2045,29 +2089,19 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
             cs[r]->gdepth[cs[r]->ic] = cs[r]->gdepth[cs[r]->ip] = c0->G;
         }
     }
-    auto advance = [&](int nic, int nip, int levels, int depth) {
-        for (int r = 0; r < n; ++r) {
-            cs[r]->ic = nic;
-            cs[r]->ip = nip;
-            cs[r]->n += levels;
-            cs[r]->gdepth[nic] = depth;
-            if (levels > 1) cs[r]->gdepth[nip] = depth;
-        }
-    };
-    // one level with the schedule of step_slab_overlapped, device copies on the aux stream
+    // one level: every slab's boundary rows, the loopback copies of the new rows on the aux stream,
+    // every slab's interior rows — the phases of step_slab_overlapped with the copies in place of
+    // the NCCL messages
     auto single = [&]() -> tsw_status {
         const bool start = (c0->n == 0);
         tsw_status e;
         for (int r = 0; r < n; ++r)
-            if ((e = launch_boundary_rows(cs[r], start))) return e;
-        CK(cudaEventRecord(c0->ev_bnd, c0->stream));
-        CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
+            if ((e = slab_level_begin(cs[r], start))) return e;
+        CK(cudaStreamWaitEvent(c0->aux, cs[n - 1]->ev_bnd, 0));   // one stream: covers every slab's rows
         if ((e = exchange_loopback(cs, n, 1, c0->aux, 1))) return e;
         CK(cudaEventRecord(c0->ev_comm, c0->aux));
         for (int r = 0; r < n; ++r)
-            if ((e = launch_interior_rows(cs[r], start))) return e;
-        CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
-        advance(c0->ip, c0->ic, 1, 1);
+            if ((e = slab_level_end(cs[r], start, c0->ev_comm))) return e;
         return TSW_OK;
     };
     int64_t s = 0;
@@ -2075,8 +2109,9 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
         if ((st = single())) return st;
         s = 1;
     }
-    // one pass of K levels (every member's depth set to K for its duration)
-    auto pass = [&](int K) -> tsw_status {
+    // one pass of K levels (every member's depth set to K for its duration): the phases of tb_pass
+    // (tb_pass_begin / tb_pass_end) with loopback copies of the K boundary rows of both new levels
+    auto pass = [&](int K, bool last) -> tsw_status {
         GroupDepth gd(cs, n, K);
         for (int lv = 0; lv < 2; ++lv) {
             const int bi = lv ? c0->ip : c0->ic;
@@ -2086,41 +2121,26 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
                 for (int r = 0; r < n; ++r) cs[r]->gdepth[bi] = K;
             }
         }
-        bool split = true;
-        for (int r = 0; r < n; ++r) split = split && tb_split(cs[r]).split;
-        int fk, fkm1;
-        free_pair(c0, &fk, &fkm1);
-        tsw_status e;
-        if (split) {
-            for (int r = 0; r < n; ++r) {
-                const TbSplit p = tb_split(cs[r]);
-                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.top_lo, p.top_hi, p.bot_lo, p.bot_hi))) return e;
-            }
-            CK(cudaEventRecord(c0->ev_bnd, c0->stream));
-            CK(cudaStreamWaitEvent(c0->aux, c0->ev_bnd, 0));
-            if ((e = exchange_loopback_buf(cs, n, fk, c0->aux, K))) return e;
-            if ((e = exchange_loopback_buf(cs, n, fkm1, c0->aux, K))) return e;
-            CK(cudaEventRecord(c0->ev_comm, c0->aux));
-            for (int r = 0; r < n; ++r) {
-                const TbSplit p = tb_split(cs[r]);
-                if ((e = launch_tb_rows(cs[r], fk, fkm1, p.ilo, p.ihi))) return e;
-            }
-            CK(cudaStreamWaitEvent(c0->stream, c0->ev_comm, 0));
-        } else {
-            for (int r = 0; r < n; ++r)
-                if ((e = launch_tb_rows(cs[r], fk, fkm1, cs[r]->s_lo, cs[r]->s_hi))) return e;
-            if ((e = exchange_loopback_buf(cs, n, fk, c0->stream, K))) return e;
-            if ((e = exchange_loopback_buf(cs, n, fkm1, c0->stream, K))) return e;
+        TbPassState ps[TSW_GROUP_MAX];
+        tsw_status e = TSW_OK;
+        for (int r = 0; r < n; ++r) cs[r]->en_now = cs[r]->en_fuse && last;
+        for (int r = 0; r < n && !e; ++r) e = tb_pass_begin(cs[r], ps[r]);
+        if (!e) {
+            CK(cudaStreamWaitEvent(c0->aux, cs[n - 1]->ev_bnd, 0));
+            e = exchange_loopback_buf(cs, n, ps[0].fk, c0->aux, K);
+            if (!e) e = exchange_loopback_buf(cs, n, ps[0].fkm1, c0->aux, K);
+            if (!e) CK(cudaEventRecord(c0->ev_comm, c0->aux));
         }
-        advance(fk, fkm1, K, K);
-        return TSW_OK;
+        for (int r = 0; r < n && !e; ++r) e = tb_pass_end(cs[r], ps[r], c0->ev_comm);
+        for (int r = 0; r < n; ++r) cs[r]->en_now = false;
+        return e;
     };
     if (tb_usable(c0)) {
         const int K = c0->tblock;
         for (; s + K <= nsteps; s += K)
-            if ((st = pass(K))) return st;
+            if ((st = pass(K, s + K == nsteps))) return st;
         if (nsteps - s >= 2) {  // the remainder as one shallower pass (see DepthScope)
-            if ((st = pass(int(nsteps - s)))) return st;
+            if ((st = pass(int(nsteps - s), true))) return st;
             s = nsteps;
         }
     }
@@ -2134,9 +2154,15 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     if (!c->have_init || c->n < 1) return fail(TSW_ERR_STATE, "energy E^{n-1/2} needs n >= 1");
     tsw_status st = set_dev(c);
     if (st) return st;
-    if (c->en_level == c->n && c->g.nranks == 1 && c->en_result) {
-        // reduced by the pass that wrote u^n, u^{n−1} (TSW_OPT_ENERGY_FUSE)
-        CK(cudaMemcpyAsync(out_B, c->en_result, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
+    if (c->en_level == c->n && c->en_result) {
+        // reduced by the pass that wrote u^n, u^{n−1} (TSW_OPT_ENERGY_FUSE); the node form reads no
+        // ghost row, so slabs need no halo epoch — only the sum over ranks
+        const double* src = c->en_result;
+        if (c->g.nranks > 1 && c->comm) {
+            NK(nccl().AllReduce(c->en_result, c->d_out, size_t(c->g.batch), NCCL_F64, NCCL_SUM, c->comm, c->stream));
+            src = c->d_out;
+        }
+        CK(cudaMemcpyAsync(out_B, src, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         return TSW_OK;
     }

@@ -89,3 +89,41 @@ def test_fused_energy_invalidated_by_new_state():
     s.set_state(s.read(1), s.read(0), 10, cfg.dt)                  # swapped levels: another energy
     assert abs(s.energy()[0] - _oracle_energy(s, cfg, 0, "f64")) <= 1e-12 * E9[0]
     s.close()
+
+
+@pytest.mark.parametrize("halo", ["loopback", "peer"])
+@pytest.mark.parametrize("P,K,nsteps", [(2, 8, 17), (3, 4, 13), (2, 5, 12)])
+def test_fused_energy_slabs(halo, P, K, nsteps):
+    """Row slabs (one process, one GPU): with loopback copies (the phases of the NCCL pass) or peer
+    halos, each slab's fused energy is its share of E (the node form reads no ghost row); the shares
+    sum to the single-domain oracle energy ≤ 1e−12."""
+    import torch
+    cfg = inputs.config(3, nx=700, ny=151, dx=0.01, dy=0.01, eps=[0.1, 0.3], amp=[1.0, 2.0], dt=2e-3)
+    u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny)
+    stream = torch.cuda.Stream()
+    parts = [tsw.Solver.from_config(cfg, "f64", rank=r, nranks=P, stream=stream.cuda_stream) for r in range(P)]
+    for p in parts:
+        p.set_option(tsw.TSW_OPT_TBLOCK, K)
+        if halo == "peer":
+            p.set_option(tsw.TSW_OPT_HALO, 1)
+    if halo == "peer":
+        for r, p in enumerate(parts):
+            if r > 0:
+                p.peer_attach(0, parts[r - 1])
+            if r < P - 1:
+                p.peer_attach(1, parts[r + 1])
+    for p in parts:
+        p.set_initial(np.ascontiguousarray(u0[p.r0:p.r0 + p.ny_local]), None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    ctxs = [p.ctx for p in parts]
+    tsw.tsw_group_step(ctxs, 1)
+    tsw.tsw_group_step(ctxs, nsteps)
+    E = sum(p.energy() for p in parts)
+    one = tsw.Solver.from_config(cfg, "f64")
+    one.set_initial(u0, None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    one.step(1 + nsteps)
+    for b in range(cfg.batch):
+        Eo = _oracle_energy(one, cfg, b, "f64")
+        assert abs(E[b] - Eo) <= 1e-12 * Eo, (b, E[b], Eo)
+    for p in parts:
+        p.close()
+    one.close()
