@@ -45,7 +45,7 @@ typedef enum {
     TSW_ERR_CUDA = 4,     /* CUDA runtime error or no device */
     TSW_ERR_NCCL = 5,     /* NCCL unavailable or failed */
     TSW_ERR_OOM = 6,      /* device allocation failed */
-    TSW_ERR_UNSTABLE = 7  /* reserved: non-finite energy */
+    TSW_ERR_UNSTABLE = 7  /* tsw_energy: non-finite energy, or drift beyond TSW_OPT_ENERGY_DRIFT (blow-up) */
 } tsw_status;
 
 typedef enum { TSW_F32 = 0, TSW_F64 = 1 } tsw_dtype;
@@ -158,8 +158,13 @@ tsw_status tsw_group_step(tsw_ctx** ctxs, int32_t n, int64_t nsteps);
 /* S5 discrete energy E^{n−1/2} of the current levels (R17; discrete form of CL-01):
  *   E = (dx·dy/dt²)·[Σ_interior (u^n − u^{n−1})² + Σ_faces c·(Δu^n)(Δu^{n−1})]   (1D: dx/dt²)
  * accumulated in fp64 with the stepper's own rounded c; summed over ranks (NCCL) when nranks > 1
- * and tsw_nccl_init was called (a loopback-group member returns its slab's share).
- *   out_B: host double[batch].  Errors: TSW_ERR_STATE if n < 1. */
+ * and tsw_nccl_init was called (a loopback-group member returns its slab's share).  When the last
+ * temporally blocked pass of the preceding tsw_step produced this level (TSW_OPT_ENERGY_FUSE), the
+ * value it reduced in the node form Σ(u^n − u^{n−1})² − Σ u^n·L(u^{n−1}) (the same bilinear form
+ * by summation by parts, reading R30) is returned without another pass over the fields.
+ *   out_B: host double[batch].  Errors: TSW_ERR_STATE if n < 1; TSW_ERR_UNSTABLE (values still
+ *   written) on a non-finite energy or a drift beyond TSW_OPT_ENERGY_DRIFT; TSW_ERR_NCCL when the
+ *   communicator reports an asynchronous error (it is aborted). */
 tsw_status tsw_energy(tsw_ctx* ctx, double* out_B);
 
 /* S6 second-wave amplitude (R18; §3.2.3, qualitative): for every member b
@@ -249,6 +254,13 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               writes (S5 fused into S3: per-item fp64 partials, plus the faces across its
                               strip / chunk seams from a small kernel); tsw_energy at that level then
                               only reads the result.  0: tsw_energy always runs the standalone kernel */
+#define TSW_OPT_ENERGY_DRIFT 15 /* blow-up detection in tsw_energy: k (default 2) — TSW_ERR_UNSTABLE
+                              when the energy is non-finite or has drifted from the first energy measured
+                              after tsw_set_initial / tsw_set_state by more than 10^−k relative (R17: the
+                              scheme conserves it to round-off while stable; above the CFL bound it grows
+                              without limit).  0: only the finiteness check.  The energies are still
+                              written to out_B.  Checked on the whole grid's energy (nranks = 1, or a
+                              communicator); a slab's share is not conserved */
 #define TSW_OPT_IMPLICIT_XROWS 12 /* rows per iteration of the implicit x-line solve: 1 (default; LU tables
                               in registers) or 2 (the two rows' scan chains interleave, tables in shared
                               memory — measured 4 % slower at 4096², kept for comparison) */

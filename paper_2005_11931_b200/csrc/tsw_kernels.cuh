@@ -570,7 +570,10 @@ struct TbPad {
 // registers and keeps it in shared memory (one 16-byte load + store per level and thread, each
 // thread touching only its own slots — no barrier).
 // fp64 y-flux cache in shared memory: measured 15 % slower on B200 (K = 4: 569 vs 657 Gpt/s,
-// interleaved A/B on one box) — the load sits in the dependency chain — so it is off by default
+// interleaved A/B on one box) — the load sits in the dependency chain — so it is off by default.
+// Round 2: the same cache with the load issued one level ahead (with the next level's neighbours):
+// K = 6 630 vs 812 Gpt/s, K = 8 613 vs 903 — its (K+1)·NT·V words of shared memory (37 KB at K = 8)
+// leave room for one CTA per SM instead of two; rejected again.
 #ifndef TSW_TB_YCACHE_SMEM
 #define TSW_TB_YCACHE_SMEM 0
 #endif
@@ -1699,15 +1702,16 @@ __global__ void __launch_bounds__(256) k_family_l2(const FamilyArgs a, double* _
 }
 
 // out[i][j] = out[j][i] = sqrt(w · Σ_cta partial[cta][i][j]) (fixed order), diagonal 0.
-__global__ void k_family_final(const double* __restrict__ partial, int ncta, int B, double w, double* __restrict__ out) {
+// out[i][j] = Σ_k partial[k][i][j] (fixed order) for i < j, mirrored; 0 on the diagonal — the
+// unweighted sums Σ (u_i − u_j)² (summed over ranks, weighted and rooted by the caller)
+__global__ void k_family_final(const double* __restrict__ partial, int ncta, int B, double* __restrict__ out) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B * B; e += gridDim.x * blockDim.x) {
         const int i = e / B, j = e % B;
         if (i >= j) continue;
         double s = 0.0;
         for (int k = 0; k < ncta; ++k) s += partial[size_t(k) * B * B + e];
-        const double v = sqrt(w * s);
-        out[i * B + j] = v;
-        out[j * B + i] = v;
+        out[i * B + j] = s;
+        out[j * B + i] = s;
     }
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < B; i += blockDim.x) out[i * B + i] = 0.0;

@@ -5,6 +5,7 @@
 #include "tsw_kernels.cuh"
 
 #include <dlfcn.h>
+#include <time.h>
 
 #include <algorithm>
 #include <climits>
@@ -64,6 +65,8 @@ struct Nccl {
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(int) = nullptr;
+    int (*CommGetAsyncError)(void*, int*) = nullptr;   // optional: failure detection
+    int (*CommAbort)(void*) = nullptr;
 };
 enum { NCCL_INT64 = 4, NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0, NCCL_MAX = 2, NCCL_MIN = 3 };
 
@@ -87,6 +90,8 @@ Nccl& nccl() {
     NSYM(GroupStart, "ncclGroupStart");
     NSYM(GroupEnd, "ncclGroupEnd");
     NSYM(GetErrorString, "ncclGetErrorString");
+    NSYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    NSYM(CommAbort, "ncclCommAbort");
 #undef NSYM
     n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Send && n.Recv && n.AllReduce && n.GroupStart &&
            n.GroupEnd && n.GetErrorString;
@@ -248,6 +253,12 @@ struct tsw_ctx {
     int en_nseg = 0;              // item-partial segments of the current pass (a split pass launches twice)
     int64_t en_off[2] = {0, 0}, en_pm[2] = {0, 0};   // offset in d_en, partials per member
     double* en_result = nullptr;  // [B]: E of level en_level (this slab's share before the all-reduce)
+    // blow-up detection: E^{n−½} must stay finite and, while the scheme is stable,
+    // conserved (R17) — relative drift beyond 10^{−en_drift_k} from the first energy after the
+    // state was set is reported as TSW_ERR_UNSTABLE (0: drift check off)
+    int en_drift_k = 2;
+    std::vector<double> en_ref;
+    int64_t en_ref_n = -1;
     // slabs: exchange stream + events (boundary rows → exchange ∥ interior rows)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
@@ -266,6 +277,45 @@ tsw_status set_dev(tsw_ctx* c) {
     CK(cudaSetDevice(c->device));
     return TSW_OK;
 }
+
+// NCCL failure detection: a peer that died or a network fault surfaces as an
+// asynchronous communicator error; the communicator is then aborted (its pending operations are
+// cancelled, nothing waits forever) and the call fails with TSW_ERR_NCCL.  Non-blocking.
+tsw_status nccl_watch(tsw_ctx* c) {
+    if (!c->comm) return TSW_OK;
+    Nccl& N = nccl();
+    if (!N.CommGetAsyncError) return TSW_OK;
+    int r = 0;
+    const int q = N.CommGetAsyncError(c->comm, &r);
+    if (q == 0 && (r == 0 || r == 7 /* ncclInProgress */)) return TSW_OK;
+    const int err = q ? q : r;
+    if (N.CommAbort) N.CommAbort(c->comm);
+    c->comm = nullptr;
+    return fail(TSW_ERR_NCCL, "NCCL communicator error: %s; communicator aborted", N.GetErrorString(err));
+}
+
+// Synchronise the ctx stream; with a communicator, poll its asynchronous error while waiting
+// (a hung collective is detected and aborted instead of blocking the host).
+tsw_status ctx_sync(tsw_ctx* c) {
+    if (!(c->g.nranks > 1 && c->comm)) {
+        CK(cudaStreamSynchronize(c->stream));
+        return TSW_OK;
+    }
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(c->stream);
+        if (e == cudaSuccess) return TSW_OK;
+        if (e != cudaErrorNotReady) CK(e);
+        tsw_status st = nccl_watch(c);
+        if (st) return st;
+        struct timespec ts = {0, 20000};
+        nanosleep(&ts, nullptr);
+    }
+}
+#define CSYNC(c)                                                                                   \
+    do {                                                                                           \
+        tsw_status s_ = ctx_sync(c);                                                               \
+        if (s_) return s_;                                                                         \
+    } while (0)
 
 int grid_for(int64_t n, int threads, int cap) {
     int64_t b = (n + threads - 1) / threads;
@@ -783,7 +833,7 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
             double* fresh = nullptr;
             CK(cudaMalloc(&fresh, need * sizeof(double)));
             if (off > 0) CK(cudaMemcpyAsync(fresh, c->d_en, size_t(off) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
+            CSYNC(c);
             if (c->d_en) CK(cudaFree(c->d_en));
             c->d_en = fresh;
             c->en_cap = need;
@@ -901,7 +951,7 @@ tsw_status peer_check(tsw_ctx* c) {
     if (!peer_mode(c) || !c->mbox) return TSW_OK;
     unsigned int e = 0;
     CK(cudaMemcpyAsync(&e, c->mbox + 2, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     if (e) return fail(TSW_ERR_STATE, "peer halos: a wait for a neighbour timed out (epochs out of step)");
     return TSW_OK;
 }
@@ -1170,7 +1220,7 @@ tsw_status prescale_all(tsw_ctx* c) {
 
 tsw_status alloc_coeff(tsw_ctx* c, int mode) {
     if (c->have_coeff && c->mode == mode) return TSW_OK;
-    CK(cudaStreamSynchronize(c->stream));  // queued work may still read the old arrays
+    CSYNC(c);  // queued work may still read the old arrays
     dfree_guarded(c->h1, c->cshift_h);
     dfree_guarded(c->h2, c->cshift_h);
     dfree_guarded(c->c1, c->cshift);
@@ -1224,7 +1274,7 @@ tsw_status check_faces(tsw_ctx* c) {
     }
     unsigned long long rho_bits = 0;
     CK(cudaMemcpyAsync(&rho_bits, c->d_u64, sizeof(rho_bits), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     double rho;
     memcpy(&rho, &rho_bits, sizeof(rho));
     if (c->g.nranks > 1 && c->comm) {
@@ -1232,7 +1282,7 @@ tsw_status check_faces(tsw_ctx* c) {
         CK(cudaMemcpyAsync(d, &rho, sizeof(double), cudaMemcpyHostToDevice, c->stream));
         NK(nccl().AllReduce(d, d, 1, NCCL_F64, NCCL_MAX, c->comm, c->stream));
         CK(cudaMemcpyAsync(&rho, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CSYNC(c);
     }
     if (!(rho > 0.0) || !std::isfinite(rho)) return fail(TSW_ERR_ARG, "non-finite or zero Gershgorin radius (%g)", rho);
     c->dt_max = 2.0 / std::sqrt(rho);
@@ -1311,6 +1361,7 @@ tsw_status set_levels(tsw_ctx* c, const void* a, const void* b, double dt, int o
     }
     c->n = n;
     c->en_level = -1;
+    c->en_ref.clear();
     c->have_init = true;
     return TSW_OK;
 }
@@ -1944,7 +1995,7 @@ tsw_status tsw_set_coeff_faces(tsw_ctx* c, const double* h1, const double* h2, i
                              B, kind, c->stream));
         std::vector<double> hb(B * c->cstride2, 1.0);  // unused in 1D (no y faces)
         CK(cudaMemcpyAsync(c->h2, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaStreamSynchronize(c->stream));  // hb is a local
+        CSYNC(c);  // hb is a local
     } else {
         CK(cudaMemsetAsync(reinterpret_cast<char*>(c->h1) - c->cshift_h, 0, B * c->cstride1 * sizeof(double), c->stream));
         CK(cudaMemsetAsync(reinterpret_cast<char*>(c->h2) - c->cshift_h, 0, B * c->cstride2 * sizeof(double), c->stream));
@@ -1977,7 +2028,7 @@ tsw_status tsw_read_faces(tsw_ctx* c, double* h1, double* h2) {
         std::vector<double> line(B * c->cstride1), hy(B * c->cstride2);
         CK(cudaMemcpyAsync(line.data(), c->h1, line.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(hy.data(), c->h2, hy.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CSYNC(c);
         const size_t nrow = (c->g.dim == 1) ? 1 : rows;
         for (size_t b = 0; b < B; ++b)
             for (size_t j = 0; j < nrow; ++j)
@@ -1998,7 +2049,7 @@ tsw_status tsw_read_faces(tsw_ctx* c, double* h1, double* h2) {
             CK(cudaMemcpy2DAsync(h2 + b * (rows + 1) * nx, nx * sizeof(double), c->h2 + b * c->mstride + c->pitch,
                                  c->pitch * sizeof(double), nx * sizeof(double), rows + 1, cudaMemcpyDeviceToHost, c->stream));
     }
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     if (h2) {
         // storage row s = face (g−1)+1/2 between storage rows s−1 and s; layout row k ↔ storage row k+1
         for (size_t b = 0; b < B; ++b)
@@ -2036,7 +2087,8 @@ tsw_status tsw_step(tsw_ctx* c, int64_t nsteps) {
         return fail(TSW_ERR_STATE, "nranks > 1: call tsw_nccl_init, enable peer halos, or step the slabs with tsw_group_step");
     tsw_status st = set_dev(c);
     if (st) return st;
-    return do_steps(c, nsteps);
+    if ((st = do_steps(c, nsteps))) return st;
+    return nccl_watch(c);   // an asynchronous communicator error surfaced by the halo traffic
 }
 
 tsw_status tsw_step_op(tsw_ctx* c, int64_t nsteps, int64_t* consumed) {
@@ -2149,6 +2201,27 @@ tsw_status tsw_group_step(tsw_ctx** cs, int32_t n, int64_t nsteps) {
     return TSW_OK;
 }
 
+tsw_status energy_guard(tsw_ctx* c, const double* E) {
+    const int B = c->g.batch;
+    for (int b = 0; b < B; ++b)
+        if (!std::isfinite(E[b]))
+            return fail(TSW_ERR_UNSTABLE, "member %d: non-finite energy at level %lld (unstable: dt above the CFL bound? R16/R17)",
+                        b, (long long)c->n);
+    // drift: only for the whole grid's energy (a slab's share is not conserved: energy crosses slabs)
+    if (c->en_drift_k <= 0 || (c->g.nranks > 1 && !c->comm)) return TSW_OK;
+    if (c->en_ref.empty()) {
+        c->en_ref.assign(E, E + B);
+        c->en_ref_n = c->n;
+        return TSW_OK;
+    }
+    const double tol = std::pow(10.0, -double(c->en_drift_k));
+    for (int b = 0; b < B; ++b)
+        if (c->en_ref[b] > 0.0 && !(std::fabs(E[b] - c->en_ref[b]) <= tol * c->en_ref[b]))
+            return fail(TSW_ERR_UNSTABLE, "member %d: energy %.17g at level %lld drifted from %.17g at level %lld by more than %g relative (blow-up)",
+                        b, E[b], (long long)c->n, c->en_ref[b], (long long)c->en_ref_n, tol);
+    return TSW_OK;
+}
+
 tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     if (!c || !out_B) return fail(TSW_ERR_ARG, "NULL argument");
     if (!c->have_init || c->n < 1) return fail(TSW_ERR_STATE, "energy E^{n-1/2} needs n >= 1");
@@ -2163,8 +2236,8 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
             src = c->d_out;
         }
         CK(cudaMemcpyAsync(out_B, src, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        return TSW_OK;
+        CSYNC(c);
+        return energy_guard(c, out_B);
     }
     // peer halos: a ghost-reading collective is an epoch of its own (no neighbour overwrites the
     // ghost rows while they are read)
@@ -2239,8 +2312,8 @@ tsw_status tsw_energy(tsw_ctx* c, double* out_B) {
     if (c->g.nranks > 1 && c->comm)  // without a communicator (loopback / peer group): this slab's share
         NK(nccl().AllReduce(c->d_out, c->d_out, size_t(c->g.batch), NCCL_F64, NCCL_SUM, c->comm, c->stream));
     CK(cudaMemcpyAsync(out_B, c->d_out, sizeof(double) * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    return TSW_OK;
+    CSYNC(c);
+    return energy_guard(c, out_B);
 }
 
 tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
@@ -2286,7 +2359,7 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
     std::vector<long long> ix(2 * size_t(B));
     CK(cudaMemcpyAsync(v.data(), c->d_out, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(ix.data(), c->d_idx, sizeof(long long) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     if (c->g.nranks > 1 && c->comm) {  // without a communicator (loopback group): this slab's extrema
         // values: empty local regions must not win → ±inf; indices: first global extremum
         std::vector<double> mx(B), mn(B);
@@ -2302,7 +2375,7 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
         std::vector<double> gmx(B), gmn(B);
         CK(cudaMemcpyAsync(gmx.data(), d, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(gmn.data(), d + B, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CSYNC(c);
         std::vector<long long> li(2 * size_t(B));
         for (int b = 0; b < B; ++b) {
             li[2 * b] = (ix[2 * b] >= 0 && mx[b] == gmx[b]) ? ix[2 * b] : LLONG_MAX;
@@ -2311,7 +2384,7 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
         CK(cudaMemcpyAsync(c->d_idx, li.data(), sizeof(long long) * 2 * B, cudaMemcpyHostToDevice, c->stream));
         NK(nccl().AllReduce(c->d_idx, c->d_idx, size_t(2 * B), NCCL_INT64, NCCL_MIN, c->comm, c->stream));
         CK(cudaMemcpyAsync(li.data(), c->d_idx, sizeof(long long) * 2 * B, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CSYNC(c);
         for (int b = 0; b < B; ++b) {
             const bool e1 = li[2 * b] == LLONG_MAX, e2 = li[2 * b + 1] == LLONG_MAX;
             v[2 * b] = e1 ? 0.0 : gmx[b];
@@ -2347,7 +2420,8 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
     if (a.nblk * (a.nblk + 1) / 2 > 256) return fail(TSW_ERR_ARG, "too many members for one CTA of pair blocks");
     const int64_t ntiles = int64_t(a.rows) * a.tiles_per_row;
     const int ncta = int(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * c->sm_count)));
-    const size_t need = size_t(ncta) * B * B;
+    // partials [ncta][B][B], then the per-pair sums [B][B] (one allocation, grown once)
+    const size_t need = size_t(ncta + 1) * B * B;
     if (c->fam_cap < need) {
         if (c->d_fam) cudaFree(c->d_fam);
         c->d_fam = nullptr;
@@ -2355,7 +2429,8 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
         CK(cudaMalloc(&c->d_fam, need * sizeof(double)));
         c->fam_cap = need;
     }
-    CK(cudaMemsetAsync(c->d_fam, 0, need * sizeof(double), c->stream));
+    double* d_sum = c->d_fam + size_t(ncta) * B * B;
+    CK(cudaMemsetAsync(c->d_fam, 0, size_t(ncta) * B * B * sizeof(double), c->stream));
     const size_t smem = size_t(B) * (FAM_TN + 1) * sizeof(double);
     if (smem > 48 * 1024) {
         if (is_f64(c)) CK(cudaFuncSetAttribute(k_family_l2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -2366,37 +2441,16 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
     else
         k_family_l2<float><<<ncta, 256, smem, c->stream>>>(a, c->d_fam);
     CKL();
-    // root of the sums Σ (u_i − u_j)² (weight applied below); with ranks: re-square, sum, root
-    double* d_sum = nullptr;
-    CK(cudaMalloc(&d_sum, sizeof(double) * B * B));
-    k_family_final<<<std::max(1, (B * B + 255) / 256), 256, 0, c->stream>>>(c->d_fam, ncta, B, 1.0, d_sum);
-    cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess && c->g.nranks > 1 && c->comm) {
-        // square, sum over ranks, take the root again on the host
-        std::vector<double> h(size_t(B) * B);
-        e = cudaMemcpyAsync(h.data(), d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-        for (double& v : h) v = v * v;
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_sum, h.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice, c->stream);
-        int r = (e == cudaSuccess) ? nccl().AllReduce(d_sum, d_sum, size_t(B) * B, NCCL_F64, NCCL_SUM, c->comm, c->stream) : 0;
-        if (r != 0) {
-            cudaFree(d_sum);
-            return fail(TSW_ERR_NCCL, "family allreduce: %s", nccl().GetErrorString(r));
-        }
-        std::vector<double> g(size_t(B) * B);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(g.data(), d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-        for (size_t k = 0; k < g.size(); ++k) g[k] = std::sqrt(g[k]);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_sum, g.data(), sizeof(double) * B * B, cudaMemcpyHostToDevice, c->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);  // g is a local
-    }
-    if (e == cudaSuccess) e = cudaMemcpyAsync(out_BB, d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    cudaFree(d_sum);
-    if (e != cudaSuccess) return fail(TSW_ERR_CUDA, "family distances: %s", cudaGetErrorString(e));
+    k_family_final<<<std::max(1, (B * B + 255) / 256), 256, 0, c->stream>>>(c->d_fam, ncta, B, d_sum);
+    CKL();
     c->launches += 2;
+    // the sums Σ (u_i − u_j)² add over ranks on the device; weight and root on the host
+    if (c->g.nranks > 1 && c->comm)
+        NK(nccl().AllReduce(d_sum, d_sum, size_t(B) * B, NCCL_F64, NCCL_SUM, c->comm, c->stream));
+    CK(cudaMemcpyAsync(out_BB, d_sum, sizeof(double) * B * B, cudaMemcpyDeviceToHost, c->stream));
+    CSYNC(c);
     const double w = (c->g.dim == 1) ? c->g.dx : c->g.dx * c->g.dy;
-    for (int k = 0; k < B * B; ++k) out_BB[k] *= std::sqrt(w);
+    for (int k = 0; k < B * B; ++k) out_BB[k] = std::sqrt(w * out_BB[k]);
     return TSW_OK;
 }
 
@@ -2430,7 +2484,7 @@ tsw_status tsw_field_norms(tsw_ctx* c, double* out_B4) {
     if (peer_mode(c) && (st = peer_end(c, c->stream))) return st;
     if (c->g.nranks > 1 && c->comm) NK(nccl().AllReduce(d4, d4, size_t(4) * c->g.batch, NCCL_F64, NCCL_SUM, c->comm, c->stream));
     CK(cudaMemcpyAsync(out_B4, d4, sizeof(double) * 4 * c->g.batch, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     const double w = (c->g.dim == 1) ? c->g.dx : c->g.dx * c->g.dy;
     for (int b = 0; b < c->g.batch; ++b) {
         double* o = out_B4 + 4 * b;
@@ -2480,14 +2534,14 @@ tsw_status tsw_coeff_norms(tsw_ctx* c, double* out_B3) {
     c->launches++;
     std::vector<unsigned long long> bits(size_t(3) * c->g.batch);
     CK(cudaMemcpyAsync(bits.data(), d, sizeof(unsigned long long) * bits.size(), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     for (size_t k = 0; k < bits.size(); ++k) memcpy(&out_B3[k], &bits[k], sizeof(double));
     if (c->g.nranks > 1 && c->comm) {
         double* dd = reinterpret_cast<double*>(d);
         CK(cudaMemcpyAsync(dd, out_B3, sizeof(double) * bits.size(), cudaMemcpyHostToDevice, c->stream));
         NK(nccl().AllReduce(dd, dd, bits.size(), NCCL_F64, NCCL_MAX, c->comm, c->stream));
         CK(cudaMemcpyAsync(out_B3, dd, sizeof(double) * bits.size(), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CSYNC(c);
     }
     return TSW_OK;
 }
@@ -2508,7 +2562,7 @@ tsw_status tsw_read(tsw_ctx* c, int32_t which, void* dst, int32_t to_device) {
         CK(cudaMemcpy2DAsync(d, w, s, size_t(c->pitch) * c->esz, w, rows, kind, c->stream));
     }
     if (!to_device) {
-        CK(cudaStreamSynchronize(c->stream));
+        CSYNC(c);
         if ((st = peer_check(c))) return st;
     }
     return TSW_OK;
@@ -2518,7 +2572,7 @@ tsw_status tsw_info(tsw_ctx* c, int64_t* n, double* t, double* dt_max) {
     if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
     tsw_status st = set_dev(c);
     if (st) return st;
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     if (n) *n = c->n;
     if (t) *t = double(c->n) * c->dt;
     if (dt_max) *dt_max = c->have_coeff ? c->dt_max : 0.0;
@@ -2529,7 +2583,7 @@ tsw_status tsw_sync(tsw_ctx* c) {
     if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
     tsw_status st = set_dev(c);
     if (st) return st;
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     return TSW_OK;
 }
 
@@ -2598,6 +2652,12 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         c->scheme = int(value);
         return TSW_OK;
     }
+    if (key == TSW_OPT_ENERGY_DRIFT) {
+        if (value < 0 || value > 16) return fail(TSW_ERR_ARG, "energy drift exponent must be 0..16");
+        c->en_drift_k = int(value);
+        c->en_ref.clear();
+        return TSW_OK;
+    }
     if (key == TSW_OPT_ENERGY_FUSE) {
         if (value != 0 && value != 1) return fail(TSW_ERR_ARG, "energy fuse must be 0 or 1");
         c->en_fuse = value != 0;
@@ -2613,7 +2673,7 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
             if (!c->mbox) {
                 CK(cudaMalloc(reinterpret_cast<void**>(&c->mbox), 256));
                 CK(cudaMemsetAsync(c->mbox, 0, 256, c->stream));
-                CK(cudaStreamSynchronize(c->stream));
+                CSYNC(c);
             }
         }
         c->halo_mode = int(value);
@@ -2817,7 +2877,7 @@ tsw_status guard_fill(tsw_ctx* c) {
         CK(cudaMemsetAsync(g.first, 0xFF, GUARD, c->stream));
         CK(cudaMemsetAsync(g.first + GUARD + g.second, 0xFF, GUARD, c->stream));
     }
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     return TSW_OK;
 }
 
@@ -2825,7 +2885,7 @@ tsw_status tsw_check_guards(tsw_ctx* c, int64_t* bad_bytes, int64_t* checked_byt
     if (!c || !bad_bytes) return fail(TSW_ERR_ARG, "NULL argument");
     tsw_status st = set_dev(c);
     if (st) return st;
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     std::vector<unsigned char> h(GUARD);
     int64_t bad = 0, checked = 0;
     for (auto& g : ctx_guarded(c)) {
@@ -2833,7 +2893,7 @@ tsw_status tsw_check_guards(tsw_ctx* c, int64_t* bad_bytes, int64_t* checked_byt
         for (int side = 0; side < 2; ++side) {
             CK(cudaMemcpyAsync(h.data(), side ? g.first + GUARD + g.second : g.first, GUARD, cudaMemcpyDeviceToHost,
                                c->stream));
-            CK(cudaStreamSynchronize(c->stream));
+            CSYNC(c);
             for (unsigned char v : h) bad += (v != 0xFF);
         }
     }
@@ -2846,7 +2906,7 @@ tsw_status tsw_kernel_stats(tsw_ctx* c, double* total_ms, int64_t* launches, int
     if (!c) return fail(TSW_ERR_ARG, "NULL ctx");
     tsw_status st = set_dev(c);
     if (st) return st;
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     double ms = 0.0;
     for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
         float m = 0.f;
@@ -2864,7 +2924,7 @@ tsw_status tsw_kernel_launches(tsw_ctx* c, int64_t cap, double* ms, int32_t* lev
     if (!c || cap < 0 || (cap > 0 && (!ms || !levels || !updates))) return fail(TSW_ERR_ARG, "bad arguments");
     tsw_status st = set_dev(c);
     if (st) return st;
-    CK(cudaStreamSynchronize(c->stream));
+    CSYNC(c);
     const int64_t n = int64_t(c->timed_meta.size());
     for (int64_t k = 0; k < std::min(n, cap); ++k) {
         float m = 0.f;

@@ -37,6 +37,7 @@ TSW_OPT_HALO = 11
 TSW_OPT_IMPLICIT_XROWS = 12
 TSW_OPT_TB_WARPS = 13
 TSW_OPT_ENERGY_FUSE = 14
+TSW_OPT_ENERGY_DRIFT = 15
 
 STATUS_NAMES = {0: "TSW_OK", 1: "TSW_ERR_ARG", 2: "TSW_ERR_CFL", 3: "TSW_ERR_STATE", 4: "TSW_ERR_CUDA",
                 5: "TSW_ERR_NCCL", 6: "TSW_ERR_OOM", 7: "TSW_ERR_UNSTABLE"}

@@ -88,3 +88,37 @@ def test_no_out_of_bounds_writes(name, make, nsteps, diag):
     assert bad == 0, f"{name}: {bad} guard bytes overwritten"
     for a, b in zip(ref, got):
         assert np.array_equal(a, b), name
+
+
+@pytest.mark.parametrize("K", [1, 4])
+def test_blow_up_reported_unstable(K):
+    """SURVEY §5 blow-up detection: above the leapfrog stability bound (TSW_ALLOW_UNSTABLE skips the
+    R16 check) the discrete energy (R17) is not conserved — tsw_energy reports TSW_ERR_UNSTABLE once
+    it drifts past 10^−k (TSW_OPT_ENERGY_DRIFT, default k = 2) and, with the drift check off, once it
+    is no longer finite; below the bound the same run never raises."""
+    cfg = inputs.config(3, nx=130, ny=90, dx=0.02, dy=0.02, eps=[0.2], amp=[1.0], dt=1e-3)
+    u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny)
+
+    def run(factor, drift):
+        s = tsw.Solver.from_config(cfg, "f64")
+        if K > 1:
+            s.set_option(tsw.TSW_OPT_TBLOCK, K)
+        s.set_option(tsw.TSW_OPT_ENERGY_DRIFT, drift)
+        dt = factor * s.info()[2]
+        s.set_initial(u0, None, dt, flags=tsw.TSW_INIT_SHARED | tsw.TSW_ALLOW_UNSTABLE)
+        for it in range(200):
+            s.step(8)
+            try:
+                s.energy()
+            except tsw.TswError as e:
+                assert e.status == tsw.TSW_ERR_UNSTABLE
+                s.close()
+                return it
+        s.close()
+        return None
+
+    assert run(0.9, 2) is None                       # stable: conserved to round-off, never flagged
+    first = run(1.5, 2)                              # the Gershgorin bound is sufficient, not sharp:
+    assert first is not None                         # 1.5× is past the exact threshold here
+    late = run(1.5, 0)                               # finiteness only: flagged when it overflows
+    assert late is not None and late >= first

@@ -38,6 +38,27 @@ def main():
             s.step(2 * K + 3)
             s.energy()
             s.close()
+        # row slabs of one process: loopback copies (the NCCL pass's phases) and peer halos, with the
+        # fused energy of the last pass
+        import torch
+        for halo in (0, 1):
+            stream = torch.cuda.Stream()
+            parts = [tsw.Solver.from_config(cfg, dtype, rank=r, nranks=2, stream=stream.cuda_stream) for r in range(2)]
+            for p in parts:
+                p.set_option(tsw.TSW_OPT_TBLOCK, 4)
+                if halo:
+                    p.set_option(tsw.TSW_OPT_HALO, 1)
+            if halo:
+                parts[0].peer_attach(1, parts[1])
+                parts[1].peer_attach(0, parts[0])
+            u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(np.float64 if dtype == "f64" else np.float32)
+            for p in parts:
+                p.set_initial(np.ascontiguousarray(u0[p.r0:p.r0 + p.ny_local]), None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+            tsw.tsw_group_step([p.ctx for p in parts], 1)
+            tsw.tsw_group_step([p.ctx for p in parts], 11)
+            for p in parts:
+                p.energy()
+                p.close()
         # profile coefficients + implicit (both solvers), 2D and 1D
         sc = inputs.paper_2d(dx=0.5)
         for solver in (0, 1):
