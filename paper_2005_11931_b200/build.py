@@ -9,10 +9,13 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 # translation units: the runtime (all other kernels) and the temporally blocked stencil's launch
-# wrappers once per precision — compiled in parallel, then linked into one shared library
+# wrappers once per precision and variant (plain / fused energy) — compiled in parallel, then
+# linked into one shared library
 UNITS = [("tsw_runtime", "tsw_runtime.cu", ()),
-         ("tsw_tb_f64", "tsw_tb.cu", ("-DTSW_TB_DTYPE=double",)),
-         ("tsw_tb_f32", "tsw_tb.cu", ("-DTSW_TB_DTYPE=float",))]
+         ("tsw_tb_f64", "tsw_tb.cu", ("-DTSW_TB_DTYPE=double", "-DTSW_TB_EN=0")),
+         ("tsw_tb_f64_en", "tsw_tb.cu", ("-DTSW_TB_DTYPE=double", "-DTSW_TB_EN=1")),
+         ("tsw_tb_f32", "tsw_tb.cu", ("-DTSW_TB_DTYPE=float", "-DTSW_TB_EN=0")),
+         ("tsw_tb_f32_en", "tsw_tb.cu", ("-DTSW_TB_DTYPE=float", "-DTSW_TB_EN=1"))]
 SRC = [os.path.join(CSRC, u[1]) for u in UNITS]
 DEPS = sorted(set(SRC)) + [os.path.join(CSRC, "tsw_kernels.cuh"), os.path.join(ROOT, "include", "tsw.h")]
 LIB = os.path.join(PKG, "libtsw.so")

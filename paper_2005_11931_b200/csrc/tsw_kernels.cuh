@@ -582,6 +582,21 @@ template <typename T> struct TbYCache {
     static constexpr bool smem = sizeof(T) == 8 && TSW_TB_YCACHE_SMEM;     // shared memory
 };
 
+// TSW_TB_JITTER=1 (debug builds only): a pseudo-random per-(CTA, warp, row) delay of up to ~2 µs
+// before and after every row barrier, so warps reach the barrier, read the centre rows and the
+// stages, and issue the refills in changing orders — a race-perturbation test (compute-sanitizer's
+// racecheck is unavailable on this GPU pool): results must stay bitwise those of the plain build.
+#ifndef TSW_TB_JITTER
+#define TSW_TB_JITTER 0
+#endif
+__device__ __forceinline__ void tb_jitter(int R, int warp, int where) {
+    uint32_t h = uint32_t(blockIdx.x) * 0x9E3779B1u ^ uint32_t(R) * 0x85EBCA77u ^ uint32_t(warp * 2 + where) * 0xC2B2AE3Du;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if ((h & 7u) == 0u) __nanosleep(h % 2048u);   // one row in eight, per warp
+}
+
 // TSW_TB_WAIT1=1: only thread 0 waits on a stage's "full" mbarrier, before the per-row CTA barrier
 // (the others see the stage through that barrier).  Measured 5 % slower than every warp waiting
 // after the barrier (f64 K = 4: 655 vs 693 Gpt/s; f32 K = 8: 1234 vs 1293): the waits of the 8
@@ -899,6 +914,14 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         // running output pointers: row ro = R − K of the current input row R = in_lo + i
         T* okp = a.out_k + b * a.mstride + gc0 + int64_t(in_lo - K) * a.pitch;
         T* okm1p = a.out_km1 + b * a.mstride + gc0 + int64_t(in_lo - K) * a.pitch;
+        // PEER: element distances from the local outputs to the neighbours' ghost rows (uniform)
+        int64_t pdist[4] = {0, 0, 0, 0};
+        if constexpr (PEER) {
+            pdist[0] = (a.pu_k + b * a.pu_mstride) - (a.out_k + b * a.mstride);
+            pdist[1] = (a.pu_km1 + b * a.pu_mstride) - (a.out_km1 + b * a.mstride);
+            pdist[2] = (a.pd_k + b * a.pd_mstride) - (a.out_k + b * a.mstride);
+            pdist[3] = (a.pd_km1 + b * a.pd_mstride) - (a.out_km1 + b * a.mstride);
+        }
         // Dirichlet masking is only needed where the item's dependency cone (rows in_lo − K ..
         // s1 + K − 1, the extended strip's columns) touches a boundary row/column or the grid edge
         const bool col_clear = (cs - H >= 1) && (cs - H + WE <= a.nx - 1);
@@ -930,7 +953,9 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             constexpr bool MASKED = decltype(msk)::value;
             const int R = in_lo + i;
             if (TSW_TB_WAIT1 && tid == 0 && i < nload) mbar_wait(&full[cslot], cphase);
+            if (TSW_TB_JITTER) tb_jitter(R, warp, 0);
             __syncthreads();  // the previous rows' stages and centre rows are consumed / published
+            if (TSW_TB_JITTER) tb_jitter(R, warp, 1);
             // refill the stage consumed by the previous row (its shared-memory reads completed
             // before this barrier: the values were used in that row's arithmetic)
             if (pending) {
@@ -984,15 +1009,15 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
                 stg_v2(okp, lastk);
                 stg_v2(okm1p, o2);
                 if constexpr (PEER) {
-                    if (ro <= a.push_top) {   // peer stores over NVLink (rare rows)
-                        const int64_t off = int64_t(ro) * a.pitch + gc0;
-                        stg_v2(a.pu_k + b * a.pu_mstride + off, lastk);
-                        stg_v2(a.pu_km1 + b * a.pu_mstride + off, o2);
+                    // peer stores over NVLink (rare rows): the neighbour's element is the local
+                    // output element plus an item-uniform distance (no per-thread pointer is held)
+                    if (ro <= a.push_top) {
+                        stg_v2(okp + pdist[0], lastk);
+                        stg_v2(okm1p + pdist[1], o2);
                     }
                     if (ro >= a.push_bot) {
-                        const int64_t off = int64_t(ro) * a.pitch + gc0;
-                        stg_v2(a.pd_k + b * a.pd_mstride + off, lastk);
-                        stg_v2(a.pd_km1 + b * a.pd_mstride + off, o2);
+                        stg_v2(okp + pdist[2], lastk);
+                        stg_v2(okm1p + pdist[3], o2);
                     }
                 }
             }
@@ -1052,11 +1077,10 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
 }
 
 // Launch wrappers, defined and instantiated in tsw_tb.cu (one translation unit per precision).
-template <typename T, int K, int NC>
+template <typename T, int K, int NC, bool EN>
 cudaError_t tb_setup(size_t smem, int* occ);
-template <typename T, int K, int NC>
-cudaError_t tb_launch(bool push, bool energy, unsigned blocks, size_t smem, cudaStream_t stream, const TbArgs<T>& a,
-                      int depth);
+template <typename T, int K, int NC, bool EN>
+cudaError_t tb_launch(bool push, unsigned blocks, size_t smem, cudaStream_t stream, const TbArgs<T>& a, int depth);
 
 #ifndef TSW_TB_UNIT  // the rest is compiled in the runtime's translation unit only
 // ------------------------------------------------------------------------------------------

@@ -761,7 +761,10 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
     const bool peer = peer_mode(c);
     int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K][NC == 8 ? 1 : 0];
     if (occ == 0) {
-        CK((tb_setup<T, K, NC>(smem, &occ)));
+        CK((tb_setup<T, K, NC, false>(smem, &occ)));
+        int occ_en = 0;
+        CK((tb_setup<T, K, NC, true>(smem, &occ_en)));
+        occ = std::min(occ, occ_en);   // the fused-energy pass launches the same grid
         if (occ < 1) return fail(TSW_ERR_ARG, "temporally blocked stencil (K=%d) does not fit on an SM", K);
     }
     TbArgs<T> a;
@@ -843,7 +846,10 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
         c->en_pm[c->en_nseg] = a.strips * a.chunks;
         c->en_nseg++;
     }
-    CK((tb_launch<T, K, NC>(push, energy, unsigned(blocks), smem, c->stream, a, depth)));
+    if (energy)
+        CK((tb_launch<T, K, NC, true>(push, unsigned(blocks), smem, c->stream, a, depth)));
+    else
+        CK((tb_launch<T, K, NC, false>(push, unsigned(blocks), smem, c->stream, a, depth)));
     if (c->timing) {
         CK(cudaEventRecord(e1, c->stream));
         note_timed(c, K, rows * (c->g.nx - 2) * c->g.batch * K);

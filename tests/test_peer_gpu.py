@@ -82,3 +82,34 @@ def test_peer_halo_bench_shape_sampled(K, n):
     for p in parts:
         p.close()
     ref.close()
+
+
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("K", [4, 8])
+def test_slabs_several_calls_ending_in_passes(halo, K):
+    """Every stepping call ends on a pass that also reduces the energy (TSW_OPT_ENERGY_FUSE); with
+    peer halos that pass must still push its boundary rows (the fused-energy kernel has a peer-store
+    variant), with loopback / NCCL-phase halos its rows must still be exchanged — so the NEXT call
+    reads correct ghost rows.  Several such calls, energies in between, fields against the oracle."""
+    import torch
+    from tests.helpers import check_slabs_against_oracle
+    cfg = inputs.config(3, nx=700, ny=151, dx=0.01, dy=0.01, eps=[0.1, 0.3], amp=[1.0, 2.0], dt=2e-3)
+    u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny)
+    if halo:
+        parts, _ = _group(cfg, 2, K)
+    else:
+        stream = torch.cuda.Stream()
+        parts = [tsw.Solver.from_config(cfg, "f64", rank=r, nranks=2, stream=stream.cuda_stream) for r in range(2)]
+        for p in parts:
+            p.set_option(tsw.TSW_OPT_TBLOCK, K)
+    for p in parts:
+        p.set_initial(np.ascontiguousarray(u0[p.r0:p.r0 + p.ny_local]), None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    ctxs = [p.ctx for p in parts]
+    tsw.tsw_group_step(ctxs, 1)
+    for _ in range(3):
+        tsw.tsw_group_step(ctxs, K)
+        for p in parts:
+            p.energy()
+    check_slabs_against_oracle(parts, cfg, "f64", 1 + 3 * K, u0)
+    for p in parts:
+        p.close()
