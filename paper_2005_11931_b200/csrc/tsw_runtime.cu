@@ -2342,10 +2342,13 @@ tsw_status tsw_wave2(tsw_ctx* c, int32_t bg, double* out_B2, int64_t* idx_B2) {
     a.dx = c->g.dx;
     a.xs = c->xs;
     a.eps = c->d_eps;
-    // column tiles × row chunks: ≈ 8 CTAs per SM over the batch, ≤ nblk_red partials per member
+    // column tiles × row chunks: ≈ 8 (fp64) / 16 (fp32: 1024-column tiles, few of them) CTAs per SM
+    // over the batch — tiles outside the region exit at once (about half of them for the configs'
+    // x ≤ −ε region) — ≤ nblk_red partials per member
     const int64_t rows = (c->g.dim == 1) ? 1 : c->ny_local;
     a.tiles = (c->g.nx + 256 * int64_t(16 / c->esz) - 1) / (256 * int64_t(16 / c->esz));
-    int64_t chunks = (int64_t(8) * c->sm_count + a.tiles * c->g.batch - 1) / (a.tiles * c->g.batch);
+    const int64_t per_sm = is_f64(c) ? 8 : 16;
+    int64_t chunks = (per_sm * c->sm_count + a.tiles * c->g.batch - 1) / (a.tiles * c->g.batch);
     chunks = std::max<int64_t>(1, std::min<int64_t>({chunks, rows, std::max<int64_t>(1, c->nblk_red / a.tiles)}));
     a.rows_per_chunk = int32_t((rows + chunks - 1) / chunks);
     chunks = (rows + a.rows_per_chunk - 1) / a.rows_per_chunk;
