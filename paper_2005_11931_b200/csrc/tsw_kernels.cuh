@@ -605,37 +605,15 @@ __device__ __forceinline__ void tb_jitter(int R, int warp, int where) {
 #define TSW_TB_WAIT1 0
 #endif
 
-// TSW_TB_SHFL (per precision): the left/right neighbours of every level's centre row come from the
-// neighbouring lanes' registers (__shfl_up/down_sync); only the warp-edge columns go through shared
-// memory (lane 0 / 31 store their edge value per level, the neighbouring warp's lane 31 / 0 reads
-// it after the per-row barrier).  Replaces the full centre-row store + two conflicting 8-byte loads
-// per level (4-way bank conflicts at the 16-byte thread stride in fp64) by shuffles.
-// Measured and rejected (interleaved A/B, bench workload, K = 8): fp64 909 → 815 Gpt/s, fp32
-// 1531 → 1355 — the shuffles and the edge selects cost more issue slots and latency than the
-// conflicts they remove (ncu: MIO throttle ≈ 0 in the baseline; the stalls are fixed-latency fp64
-// dependencies and the fp64 pipe itself).  Off by default in both precisions.
-#ifndef TSW_TB_SHFL_F64
-#define TSW_TB_SHFL_F64 0
-#endif
-#ifndef TSW_TB_SHFL_F32
-#define TSW_TB_SHFL_F32 0
-#endif
-template <typename T> struct TbShfl {
-    static constexpr bool on = sizeof(T) == 8 ? TSW_TB_SHFL_F64 : TSW_TB_SHFL_F32;
-};
-// edge buffers of the shuffle variant: [2 parities][K levels][NC + 2 warps][4 slots]; the warps at
-// index 0 and NC + 1 are the zero pads outside the extended strip
-template <typename T, int K, int NC>
-struct TbEdge {
-    static constexpr int ES = (NC + 2) * 4;       // one level of one parity: per warp {left, right, trash, pad}
-    static constexpr int N = 2 * K * ES;
-};
+// Measured and rejected (round 2): the left/right neighbours of every level from the
+// adjacent lanes' registers (__shfl_up/down_sync), only warp edges through shared memory —
+// fp64 909 → 815 Gpt/s, fp32 1531 → 1355 (the baseline's MIO throttle is ≈ 0; the shuffles and
+// edge selects add issue slots).
 
 template <typename T, int K, int NC = TB_NC>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
     return size_t(depth) * 2 * TbGeom<T, K, NC>::WE * sizeof(T) +
-           (TbShfl<T>::on ? (size_t(TbEdge<T, K, NC>::N) * sizeof(T) + 15) / 16 * 16
-                          : size_t(K) * 2 * (TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P) * sizeof(T)) +
+           size_t(K) * 2 * (TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P) * sizeof(T) +
            (size_t(depth) * sizeof(uint64_t) + 15) / 16 * 16 +
            (TbYCache<T>::smem ? size_t(K + 1) * TbGeom<T, K, NC>::NT * TbGeom<T, K, NC>::V * sizeof(T) : 0);
 }
@@ -671,38 +649,13 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // One input row of the wavefront.  `cr` / `cw`: this thread's element in the centre-row buffers
 // of the previous / current row parity (level m at offset m·2·WEP).  MASKED: force the Dirichlet
 // rows/columns to +0 (only items whose dependency cone touches them need it).
-// Shuffle variant: left/right neighbours of level m's centre row (slot N of phase PH: written in the
-// previous input row, not touched by this row's updates) — lanes' registers, warp edges from the
-// edge buffer of the previous parity.  Branch-free: every lane loads er[m·ES] (er is pre-offset per
-// lane: lane 0 → the left warp's right edge, every other lane → the right warp's left edge, the one
-// lane 31 needs) and selects.
-template <typename T, int K, int PH, int NC>
-__device__ __forceinline__ void tb_nbr_shfl(const TbState<T, K>& S, const T* __restrict__ er, int m, int lane,
-                                            T& left, T& right) {
-    constexpr int N = (PH + 2) % 3;
-    const T sl = __shfl_up_sync(0xffffffffu, S.w[m][N][1], 1);
-    const T sr = __shfl_down_sync(0xffffffffu, S.w[m][N][0], 1);
-    const T ev = er[m * TbEdge<T, K, NC>::ES];
-    left = (lane == 0) ? ev : sl;
-    right = (lane == 31) ? ev : sr;
-}
-
-// Edge store of a level's new row: lane 0 its column 0 (slot 0), lane 31 its column 1 (slot 1),
-// every other lane the warp's trash slot 2 (ew is pre-offset per lane) — one branch-free STS.
-template <typename T, int K, int NC>
-__device__ __forceinline__ void tb_edge_store(T* __restrict__ ew, int m, int lane, const T (&v)[2]) {
-    ew[m * TbEdge<T, K, NC>::ES] = (lane == 0) ? v[0] : v[1];
-}
-
 template <typename T, int K, int PH, bool MASKED, int NC, bool EN = false>
 __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
                                        int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
                                        T* __restrict__ yc, const T (&lr1)[2], int lane, bool en_on = false,
                                        double* en_acc = nullptr) {
     constexpr int V = 2;
-    constexpr bool SH = TbShfl<T>::on;
     constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
-    constexpr int ES = TbEdge<T, K, NC>::ES;
     constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
     // level 0
 #pragma unroll
@@ -716,20 +669,11 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
         // level m−1 after its update: rows (r−1, r, r+1) in slots (C, N, O); level m−2: row r in C
         T nleft = (T)0, nright = (T)0;
         if (m < K) {
-            if constexpr (SH) {
-                tb_nbr_shfl<T, K, PH, NC>(S, cr, m, lane, nleft, nright);
-            } else {
-                const T* cn = cr + m * 2 * WEP;
-                nleft = cn[-1];
-                nright = cn[V];
-            }
+            const T* cn = cr + m * 2 * WEP;
+            nleft = cn[-1];
+            nright = cn[V];
         }
-        if (m == 1) {
-            if constexpr (SH)
-                tb_edge_store<T, K, NC>(cw, 0, lane, nw);
-            else
-                sts_v2(cw, nw);
-        }
+        if (m == 1) sts_v2(cw, nw);
         // canonical tree with shared face fluxes:
         //   F_{i+1/2} = c1_{i+1/2}·(u_{i+1} − u_i) is node i's right and node i+1's left x-flux,
         //   G_{j+1/2} = c2·(u_{j+1} − u_j) is row j's upper and row j+1's lower y-flux
@@ -790,11 +734,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
         if (m < K) {
 #pragma unroll
             for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
-            if constexpr (SH) {
-                tb_edge_store<T, K, NC>(cw, m, lane, nv);
-            } else {
-                sts_v2(cw + m * 2 * WEP, nv);
-            }
+            sts_v2(cw + m * 2 * WEP, nv);
         } else {
 #pragma unroll
             for (int k = 0; k < V; ++k) lastk[k] = nv[k];
@@ -815,11 +755,9 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
     constexpr int PAD = TbPad<T>::P, WEP = WE + 2 * PAD;
     extern __shared__ __align__(128) unsigned char smem[];
-    constexpr bool SH = TbShfl<T>::on;
-    using EG = TbEdge<T, K, NC>;
     T* ring = reinterpret_cast<T*>(smem);                    // [depth][2][WE]
-    T* cenp = ring + size_t(depth) * 2 * WE;                 // [K][2][WEP], row data at +PAD (SH: edges [2][K][NC+2][2])
-    constexpr size_t CEN_ELEMS = SH ? (size_t(EG::N) * sizeof(T) + 15) / 16 * 16 / sizeof(T) : size_t(K) * 2 * WEP;
+    T* cenp = ring + size_t(depth) * 2 * WE;                 // [K][2][WEP], row data at +PAD
+    constexpr size_t CEN_ELEMS = size_t(K) * 2 * WEP;
     uint64_t* full = reinterpret_cast<uint64_t*>(cenp + CEN_ELEMS);
     T* cen = cenp + PAD;
     const int tid = threadIdx.x;
@@ -967,18 +905,10 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             T* cw;
             const T* cr;
             T lr1[V];  // level 1's left/right neighbours, before the stage wait
-            if constexpr (SH) {
-                // per-lane offsets: loads (lane 0: left warp's slot 1; others: right warp's slot 0),
-                // stores (lane 0: slot 0; lane 31: slot 1; others: trash slot 2)
-                cw = cenp + par * K * EG::ES + (warp + 1) * 4 + (lane == 0 ? 0 : (lane == 31 ? 1 : 2));
-                cr = cenp + (par ^ 1) * K * EG::ES + (lane == 0 ? warp * 4 + 1 : (warp + 2) * 4);
-                tb_nbr_shfl<T, K, decltype(ph)::value, NC>(S, cr, 0, lane, lr1[0], lr1[1]);
-            } else {
-                cw = cen + par * WEP + e0;
-                cr = cen + (par ^ 1) * WEP + e0;
-                lr1[0] = cr[-1];
-                lr1[1] = cr[V];
-            }
+            cw = cen + par * WEP + e0;
+            cr = cen + (par ^ 1) * WEP + e0;
+            lr1[0] = cr[-1];
+            lr1[1] = cr[V];
             T nw[V], pv_new[V];
             const bool refill = (i < nload);
             pending = refill ? 1 : 0;
