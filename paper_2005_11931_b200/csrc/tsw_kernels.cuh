@@ -791,44 +791,27 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         in_hi = min(s1 + K, a.smax + 1);
     };
 
-    // ---- producer state: the stream of (item, input row) stages.  Every thread tracks it (the
-    // values are CTA-uniform, so they live in uniform registers); one elected lane of a rotating
-    // warp issues each refill, so no warp carries the producer's instructions on every row.
-    int64_t p_item = blockIdx.x;
-    int p_R = 0, p_hi = 0, p_slot = 0;
-    int64_t p_e = 0;            // element offset of the next stage's rows in u^n and u^{n−1}
-    auto p_start = [&]() {
-        int64_t cs;
-        int s0, s1, b;
-        geom(p_item, cs, s0, s1, b, p_R, p_hi);
-        p_e = b * a.mstride + int64_t(p_R) * a.pitch + cs - H;
-    };
-    if (p_item < a.items) p_start();
+    // ---- producer: stages are issued per item — its first `depth` loaded rows at the item's start
+    // (after a barrier: every stage of the previous item is consumed), then, after each row's
+    // barrier, the stage the previous row consumed is refilled with the row `depth` further on by
+    // one elected lane of a rotating warp.  No cross-item prefetch: a CTA holds one or a few items
+    // of hundreds of rows, so the refill drain at an item start (one load latency) is ≪ 1 %, and no
+    // thread carries a stream position across items on every row.
     const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform by construction
-    auto produce = [&](bool issue) {
-        if (p_item >= a.items) return;
-        if (issue && elect_one()) {
-            T* st = ring + size_t(p_slot) * 2 * WE;
-            mbar_arrive_expect_tx(&full[p_slot], 2 * WE * sizeof(T));
-            bulk_g2s(st, a.un + p_e, WE * sizeof(T), &full[p_slot]);
-            bulk_g2s(st + WE, a.unm1 + p_e, WE * sizeof(T), &full[p_slot]);
-        }
-        if (++p_slot == depth) p_slot = 0;
-        p_e += a.pitch;
-        if (++p_R == p_hi) {
-            p_item += gridDim.x;
-            if (p_item < a.items) p_start();
-        }
+    auto issue_stage = [&](int slot, int64_t e) {
+        T* st = ring + size_t(slot) * 2 * WE;
+        mbar_arrive_expect_tx(&full[slot], 2 * WE * sizeof(T));
+        bulk_g2s(st, a.un + e, WE * sizeof(T), &full[slot]);
+        bulk_g2s(st + WE, a.unm1 + e, WE * sizeof(T), &full[slot]);
     };
-    for (int k = 0; k < depth; ++k) produce(warp == 0);
     int rot = 0;  // the warp that issues the next refill
 
     const int e0 = tid * V;  // my first column of the extended strip
     // interior storage rows of the global grid: g ∈ [1, ny−2] ⇔ storage s ∈ [rowlo, rowhi]
     const int rowlo = int(1 - a.r0 + 1), rowhi = int(a.ny - 2 - a.r0 + 1);
-    int cslot = 0;
+    int cslot = 0;      // ring slot of the next loaded row, and its mbarrier phase parity
     uint32_t cphase = 0;
-    int pending = 0;  // the previous row consumed a stage that is not yet refilled
+    int lslot = 0;      // the slot the previous row consumed
     TbState<T, K> S;
     double en_acc = 0.0;   // EN: this thread's sum over its output nodes of the current item
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
@@ -884,6 +867,17 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         }
         const int nload = in_hi - in_lo;
         const int L = s1 + K - in_lo;
+        // this item's stage stream: input row in_lo + j at element ibase + j·pitch; prefill
+        const int64_t ibase = b * a.mstride + int64_t(in_lo) * a.pitch + cs - H;
+        __syncthreads();
+        if (warp == 0 && elect_one()) {
+            int sl = cslot;
+            const int pre = min(depth, nload);
+            for (int r = 0; r < pre; ++r) {
+                issue_stage(sl, ibase + int64_t(r) * a.pitch);
+                if (++sl == depth) sl = 0;
+            }
+        }
 
         // one input row: barrier, refill, stage read, wavefront (phase PH), output
         auto row = [&](auto ph, auto msk, int i) {
@@ -895,11 +889,11 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             __syncthreads();  // the previous rows' stages and centre rows are consumed / published
             if (TSW_TB_JITTER) tb_jitter(R, warp, 1);
             // refill the stage consumed by the previous row (its shared-memory reads completed
-            // before this barrier: the values were used in that row's arithmetic)
-            if (pending) {
-                produce(warp == rot);
+            // before this barrier: the values were used in that row's arithmetic) with the item's
+            // row `depth` further on
+            if (i >= 1 && i - 1 + depth < nload) {
+                if (warp == rot && elect_one()) issue_stage(lslot, ibase + int64_t(i - 1 + depth) * a.pitch);
                 if (++rot == NC) rot = 0;
-                pending = 0;
             }
             const int par = R & 1;
             T* cw;
@@ -911,12 +905,12 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             lr1[1] = cr[V];
             T nw[V], pv_new[V];
             const bool refill = (i < nload);
-            pending = refill ? 1 : 0;
             if (refill) {
                 if (!TSW_TB_WAIT1) mbar_wait(&full[cslot], cphase);
                 const T* st = ring + size_t(cslot) * 2 * WE;
                 lds_v2(st + e0, nw);
                 lds_v2(st + WE + e0, pv_new);
+                lslot = cslot;
                 if (++cslot == depth) {
                     cslot = 0;
                     cphase ^= 1u;
