@@ -833,15 +833,16 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         }
         const bool out_cols = (e0 >= H) && (e0 < H + WO) && (cs - H + e0 < a.pitch);
         // running output pointers: row ro = R − K of the current input row R = in_lo + i
+        // (u^{n+K−1} at the same element: an item-uniform distance from u^{n+K})
         T* okp = a.out_k + b * a.mstride + gc0 + int64_t(in_lo - K) * a.pitch;
-        T* okm1p = a.out_km1 + b * a.mstride + gc0 + int64_t(in_lo - K) * a.pitch;
+        const int64_t dkm1 = a.out_km1 - a.out_k;
         // PEER: element distances from the local outputs to the neighbours' ghost rows (uniform)
         int64_t pdist[4] = {0, 0, 0, 0};
         if constexpr (PEER) {
             pdist[0] = (a.pu_k + b * a.pu_mstride) - (a.out_k + b * a.mstride);
-            pdist[1] = (a.pu_km1 + b * a.pu_mstride) - (a.out_km1 + b * a.mstride);
+            pdist[1] = (a.pu_km1 + b * a.pu_mstride) - (a.out_k + b * a.mstride);
             pdist[2] = (a.pd_k + b * a.pd_mstride) - (a.out_k + b * a.mstride);
-            pdist[3] = (a.pd_km1 + b * a.pd_mstride) - (a.out_km1 + b * a.mstride);
+            pdist[3] = (a.pd_km1 + b * a.pd_mstride) - (a.out_k + b * a.mstride);
         }
         // Dirichlet masking is only needed where the item's dependency cone (rows in_lo − K ..
         // s1 + K − 1, the extended strip's columns) touches a boundary row/column or the grid edge
@@ -931,22 +932,21 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
 #pragma unroll
                 for (int k = 0; k < V; ++k) o2[k] = S.w[K - 1][NS][k];
                 stg_v2(okp, lastk);
-                stg_v2(okm1p, o2);
+                stg_v2(okp + dkm1, o2);
                 if constexpr (PEER) {
                     // peer stores over NVLink (rare rows): the neighbour's element is the local
                     // output element plus an item-uniform distance (no per-thread pointer is held)
                     if (ro <= a.push_top) {
                         stg_v2(okp + pdist[0], lastk);
-                        stg_v2(okm1p + pdist[1], o2);
+                        stg_v2(okp + pdist[1], o2);
                     }
                     if (ro >= a.push_bot) {
                         stg_v2(okp + pdist[2], lastk);
-                        stg_v2(okm1p + pdist[3], o2);
+                        stg_v2(okp + pdist[3], o2);
                     }
                 }
             }
             okp += a.pitch;
-            okm1p += a.pitch;
         };
         // rows [i0, i1) of the item; i0 is a multiple of 3 (the window phase is i mod 3)
         auto run_rows = [&](auto msk, int i0, int i1) {
