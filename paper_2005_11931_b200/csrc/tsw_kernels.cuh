@@ -746,110 +746,6 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
     for (int k = 0; k < V; ++k) S.pm1[k] = pv_new[k];
 }
 
-// TSW_TB_PIPE = 1: the same row, software-pipelined across levels.  Level m's update splits into
-// terms that only need rows written in earlier input rows — the x-flux difference lapx, the lower
-// y-flux gd and t = 2u − p ("early") — and the chain from level m−1's row of this input row
-// (gu → gu − gd → lap → v).  Level m+1's early terms are computed before level m's chain (its
-// neighbours loaded one level earlier still), so the scheduler can overlap them.
-#ifndef TSW_TB_PIPE
-#define TSW_TB_PIPE 0
-#endif
-template <typename T, int K, int PH, bool MASKED, int NC, bool EN = false>
-__device__ __forceinline__ void tb_row_pipe(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
-                                            int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
-                                            const T (&lr1)[2], bool en_on = false, double* en_acc = nullptr) {
-    constexpr int V = 2;
-    constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
-    constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;
-    struct Early {
-        T lapx[2], gd[2], t[2];
-    };
-    // early terms of level m from level m−1's centre row (slot N), its neighbours (l, r), level
-    // m−1's row below (slot C) and level m−2's row (pr)
-    auto early = [&](int m, T l, T r) {
-        Early e;
-        const T u0 = S.w[m - 1][N][0], u1 = S.w[m - 1][N][1];
-        const T F0 = r_mul(S.c1l[0], r_sub(u0, l));
-        const T F1 = r_mul(S.c1r[0], r_sub(u1, u0));
-        const T F2 = r_mul(S.c1r[1], r_sub(r, u1));
-        e.lapx[0] = r_sub(F1, F0);
-        e.lapx[1] = r_sub(F2, F1);
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const T cu = S.w[m - 1][N][k];
-            if (!TbYCache<T>::on) e.gd[k] = r_mul(S.c2v[k], r_sub(cu, S.w[m - 1][C][k]));
-            const T pr = (m == 1) ? S.pm1[k] : S.w[(m >= 2) ? m - 2 : 0][C][k];
-            e.t[k] = twice_minus(cu, pr);
-        }
-        return e;
-    };
-#pragma unroll
-    for (int k = 0; k < V; ++k) S.w[0][O][k] = nw[k];
-    T nl = (T)0, nr = (T)0;   // neighbours of level 1's centre row (for level 2's early terms)
-    if (K >= 2) {
-        nl = cr[1 * 2 * WEP - 1];
-        nr = cr[1 * 2 * WEP + V];
-    }
-    Early e = early(1, lr1[0], lr1[1]);
-#pragma unroll
-    for (int m = 1; m <= K; ++m) {
-        T nnl = (T)0, nnr = (T)0;
-        if (m + 1 < K) {   // neighbours of level m+1's centre row, for level m+2's early terms
-            const T* cn = cr + (m + 1) * 2 * WEP;
-            nnl = cn[-1];
-            nnr = cn[V];
-        }
-        if (m == 1) sts_v2(cw, nw);
-        Early en;
-        if (m < K) en = early(m + 1, nl, nr);
-        bool rowok = true;
-        if (MASKED) rowok = unsigned(R - m - rowlo) <= unsigned(rowhi - rowlo);
-        T nv[V];
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const T cu = S.w[m - 1][N][k];
-            const T gu = r_mul(S.c2v[k], r_sub(S.w[m - 1][O][k], cu));
-            T gd;
-            if (TbYCache<T>::on) {
-                gd = S.gup[m][k];
-                S.gup[m][k] = gu;
-            } else {
-                gd = e.gd[k];
-            }
-            const T lap = r_add(e.lapx[k], r_sub(gu, gd));
-            const T v = r_add(e.t[k], lap);
-            nv[k] = MASKED ? ((rowok & S.colint[k]) ? v : (T)0) : v;
-            if constexpr (EN) {
-                if (m == K && en_on) {
-                    double lapd;
-                    if constexpr (sizeof(T) == 8) {
-                        lapd = (double)lap;
-                    } else {   // fp32: L re-evaluated in fp64 (R30)
-                        const T l = (m == 1) ? lr1[0] : S.w[m - 1][N][0];   // placeholder, replaced below
-                        (void)l;
-                        lapd = 0.0;
-                    }
-                    const double A = (double)nv[k], B = (double)cu;
-                    *en_acc += (A - B) * (A - B) - A * lapd;
-                }
-            }
-        }
-        if (m < K) {
-#pragma unroll
-            for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
-            sts_v2(cw + m * 2 * WEP, nv);
-        } else {
-#pragma unroll
-            for (int k = 0; k < V; ++k) lastk[k] = nv[k];
-        }
-        e = en;
-        nl = nnl;
-        nr = nnr;
-    }
-#pragma unroll
-    for (int k = 0; k < V; ++k) S.pm1[k] = pv_new[k];
-}
-
 // The producer is thread 0: after every second input row it refills the two stages consumed by
 // the previous rows (every thread has passed the per-row barrier, so they are free) with the next
 // stages of its stream (needs a ring of ≥ 3 stages).
@@ -1026,11 +922,8 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             }
             T lastk[V];
             const bool en_on = EN && out_cols && (R - K >= s0) && (R - K < s1);
-            if constexpr (TSW_TB_PIPE && !(EN && sizeof(T) == 4))
-                tb_row_pipe<T, K, PH, MASKED, NC, EN>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, lr1, en_on, &en_acc);
-            else
-                tb_row<T, K, PH, MASKED, NC, EN>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1, lane, en_on,
-                                                &en_acc);
+            tb_row<T, K, PH, MASKED, NC, EN>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1, lane, en_on,
+                                            &en_acc);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
                 // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH
