@@ -453,8 +453,10 @@ def main():
                          "table1: the paper's implicit method on its Table 1 set-up (4096^2, dt 0.05)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: 32768 x rows-per-gpu per GPU (default); strong: the 32768^2 grid split over the GPUs (R22)")
-    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
-                    help="ghost rows of the row slabs at N > 1: peer stores fused into the stencil (default) or NCCL")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="nccl",
+                    help="ghost rows of the row slabs at N > 1: NCCL send/recv of the K boundary rows on the aux "
+                         "stream, overlapped with the interior rows (default, the north_star path) or peer stores "
+                         "fused into the stencil over NVLink (CUDA IPC)")
     ap.add_argument("--tblock", type=int, default=0,
                     help="levels per HBM pass of the temporally blocked stencil (1 = per-step TMA kernel; "
                          "0 = per dtype: 4 for f64, 8 for f32 — the sweep optimum, tools/sweep.py)")
