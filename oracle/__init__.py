@@ -8,8 +8,11 @@ written from PAPER.md; this module only marshals numpy arrays through ctypes
 and composes those C functions in the paper's order.
 
 Every function states the passage it follows.  Pins: tests/test_oracle_pins.py.
-"parity unpinned" (no value printed in the paper, pinned only structurally):
-wave2 (R18).
+Every function is pinned to something other than itself (tests/test_oracle_pins.py,
+tests/test_scenarios_pins.py, tests/test_implicit_pins.py).  The second-wave amplitude (R18, our
+definition: the paper prints no A₂ value) is pinned by brute force, by invariants and by two
+closed forms — the impedance-mismatch reflection coefficient of a depth jump and the thin-layer
+(Born) limit of the δ-line.
 """
 from __future__ import annotations
 
@@ -259,7 +262,8 @@ def energy(dim: int, c1, c2, unp1: np.ndarray, un: np.ndarray, dx: float, dy: fl
 
 
 def wave2(dim: int, u: np.ndarray, ubg: np.ndarray, dx: float, xs: float, eps: float):
-    """O7 / R18: (A₂⁺, A₂⁻) and their row-major indices over {x_i ≤ xs − ε}.  Parity unpinned vs paper."""
+    """O7 / R18: (A₂⁺, A₂⁻) and their row-major indices over {x_i ≤ xs − ε} (pins: brute force,
+    A = 0 ⇒ 0, Born linearity, impedance-mismatch and thin-layer closed forms)."""
     dtype = u.dtype
     u, ubg = _c(u, dtype), _c(ubg, dtype)
     nx, ny = _shape(dim, u)

@@ -24,11 +24,12 @@
  * step, so the window centre is exact while the window half-width exceeds the
  * step count (SURVEY §8(c) "exact lattice speed").
  *
- * Parity status: every function below is pinned by tests/test_oracle_pins.py
- * (closed forms, invariants, brute force, the paper's constant c).  The
- * wave2 diagnostic's definition itself (R18) has no value in the paper:
- * "parity unpinned" against the paper; pinned only by structure (A = 0 ⇒ 0,
- * Born linearity, brute-force max/min).
+ * Parity status: every function below is pinned by tests/test_oracle_pins.py,
+ * tests/test_scenarios_pins.py and tests/test_implicit_pins.py (closed forms, invariants, brute
+ * force, the paper's constant c).  The wave2 diagnostic's definition (R18) has no value printed
+ * in the paper; it is pinned by brute-force max/min, A = 0 ⇒ 0, Born linearity, and two closed
+ * forms: the impedance-mismatch reflection coefficient R = (√h1 − √h2)/(√h1 + √h2) of the paper's
+ * Case-1 jump and the thin-layer limit (Δ/2)·∂f of the δ-line.
  */
 #include <math.h>
 #include <stdint.h>

@@ -190,3 +190,85 @@ def test_paper_difference_kernel_H():
         assert abs(H - ref) < 1e-11
     far = np.array([10.0, 24.79, 25.21, 40.0])
     assert np.all(P.eval(far, e1) - P.eval(far, e2) == 0.0)
+
+
+def _case1_reflection(eps, dx, T=5.0):
+    """Oracle leapfrog runs of Case 1 (h_0 = 100 | 10 at x_p = 75, mollified with ε) and
+    of the uniform h = 100 background, both from the paper's Gaussian u0 = 40 e^{−(x_p−40)²/8}
+    (P:809); A₂± of R18 over x ≤ 75 − ε, and the transmitted peak beyond the jump."""
+    sc = inputs.paper_case("1", eps=eps, dx=dx)
+    hj, _ = oracle.build_faces_profile(1, oracle.Profile(sc.seg_value, sc.seg_break), eps, sc.nx, 1, sc.dx)
+    hu, _ = oracle.build_faces_profile(1, oracle.Profile([100.0]), eps, sc.nx, 1, sc.dx)
+    dt = 0.9 * oracle.gershgorin_dt_max(1, hu, None, sc.dx, sc.dx)
+    n = int(math.ceil(T / dt))
+    dt = T / n
+    u0 = sc.initial()
+    a, _ = oracle.run(1, oracle.prescale(hj, dt, sc.dx, np.float64), None, u0, None, dt, n)
+    b, _ = oracle.run(1, oracle.prescale(hu, dt, sc.dx, np.float64), None, u0, None, dt, n)
+    w, idx = oracle.wave2(1, a, b, sc.dx, 25.0, eps)
+    x = inputs.node_coords(sc.nx, sc.dx)
+    trans = float(np.max(a[x > 25.0 + eps]))
+    return w, float(x[idx[0]]), trans
+
+
+def test_case1_reflection_is_the_impedance_mismatch():
+    """S6 (A₂, R18) pinned to a textbook closed form: for u_tt = (h u_x)_x a wave crossing a jump of
+    h from h1 to h2 is reflected with R = (Z1 − Z2)/(Z1 + Z2) and transmitted with T = 2Z1/(Z1 + Z2),
+    Z = √h (impedance of unit density), in the limit of a transition short against the pulse.
+    Case 1 (h1 = 100, h2 = 10): R = 0.5195, T = 1.5195; the right-going half of u0 has amplitude 20,
+    reaches the jump at t = 3.5 (speed √100) and at t = 5 the reflected pulse is centred at
+    x_p = 60.  The oracle's A₂⁺ against the uniform-depth run converges to 20R as ε → 0 (second
+    order: the error shrinks ×4 per halving of ε), A₂⁻ is round-off (one positive
+    component only), and the transmitted peak is 20T."""
+    R = (10.0 - math.sqrt(10.0)) / (10.0 + math.sqrt(10.0))
+    Tt = 2.0 * 10.0 / (10.0 + math.sqrt(10.0))
+    w2, xm2, tr2 = _case1_reflection(0.2, 0.005)
+    w1, xm1, tr1 = _case1_reflection(0.1, 0.005)
+    e2, e1 = abs(w2[0] / (20 * R) - 1), abs(w1[0] / (20 * R) - 1)
+    assert e2 < 1e-2 and e1 < 3e-3
+    assert 3.0 < e2 / e1 < 5.0                                   # O(ε²) approach to the closed form
+    assert abs(xm1 - 10.0) < 0.15 and abs(xm2 - 10.0) < 0.25     # x_p = 60 (centred x = 10)
+    for w in (w1, w2):
+        assert w[1] > -1e-9 * w[0]                               # no negative component
+    assert abs(tr1 / (20 * Tt) - 1) < 1e-2
+
+
+def _thin_layer_reflection(eps, dx, sigma=0.5, L=4.0, T=6.0, a=2.0):
+    """Oracle runs of the configs' δ-line depth h = 1 + φ_ε(x) (R6/R7, 1D) and of the background
+    h = 1, from a Gaussian u0 of amplitude a and width σ centred at x = −L, to t = T; A₂± (R18)."""
+    nx = int(round(2 * (L + T + 2) / dx)) + 1
+    nx += nx % 2                                     # even: x_s = 0 is a face (R9)
+    x = inputs.node_coords(nx, dx)
+    u0 = a * np.exp(-(x + L) ** 2 / (2 * sigma ** 2))
+    u0[0] = u0[-1] = 0.0
+    hl, _ = oracle.build_faces(1, 1, 1, 1.0, 1.0, 0.0, 0.0, eps, nx, 1, dx, dx)
+    hb, _ = oracle.build_faces(1, 1, 1, 1.0, 0.0, 0.0, 0.0, eps, nx, 1, dx, dx)
+    dt = 0.9 * oracle.gershgorin_dt_max(1, hl, None, dx, dx)
+    n = int(math.ceil(T / dt))
+    dt = T / n
+    A, _ = oracle.run(1, oracle.prescale(hl, dt, dx, np.float64), None, u0, None, dt, n)
+    B, _ = oracle.run(1, oracle.prescale(hb, dt, dx, np.float64), None, u0, None, dt, n)
+    w, idx = oracle.wave2(1, A, B, dx, 0.0, eps)
+    return w, x[idx]
+
+
+def test_delta_line_reflection_thin_layer_limit():
+    """S6 (A₂, R18) on the configs' δ-line pinned to the thin-layer (Born) limit of
+    u_tt = (h u_x)_x: a layer much thinner than the pulse reflects u_r = (Δ/2)·∂_s f of the incident
+    right-going wave f (amplitude a/2, here a Gaussian: max |f′| = (a/2)e^{−1/2}/σ), with
+    Δ = ∫(1 − h_b/h_ε) dx (mpmath quadrature here).  So A₂⁺ → +(Δ/2)·max|f′| and A₂⁻ → −(Δ/2)·max|f′|
+    — both signs, as the paper states for the δ singularity — with the positive lobe
+    nearer the layer: at t = 6 the reflected pulse is centred at x = −2 (the layer at 0 reached at
+    t = 4), its lobes at −2 ± σ.  The approach is second order in ε/σ."""
+    sigma, a = 0.5, 2.0
+    fmax = (a / 2) / sigma * math.exp(-0.5)
+    errs = []
+    for eps, dx in ((0.1, 0.002), (0.05, 0.001)):
+        w, xi = _thin_layer_reflection(eps, dx, sigma=sigma, a=a)
+        Delta = float(mpmath.quad(lambda s: 1 - 1 / (1 + C_MP / eps * mpmath.exp(1 / ((s / eps) ** 2 - 1))),
+                                  [-eps, 0, eps]))
+        pred = Delta / 2 * fmax
+        errs.append(max(abs(w[0] / pred - 1), abs(-w[1] / pred - 1)))
+        assert abs(xi[0] - (-2.0 + sigma)) < 0.1 and abs(xi[1] - (-2.0 - sigma)) < 0.1
+    assert errs[0] < 3e-2 and errs[1] < 1e-2
+    assert 3.0 < errs[0] / errs[1] < 5.0
