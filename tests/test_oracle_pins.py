@@ -488,3 +488,29 @@ def test_row_band_windows_match_full_run():
                                    np.ascontiguousarray(u0[w0:w1]), None, cfg.dt, n)
                 same &= bool(np.array_equal(un[j0 - w0:j1 - w0], full[j0:j1]))
             assert same == exact, (npdt, halo)
+
+
+def test_energy_node_form_summation_by_parts():
+    """Reading R30: with K̃ = −L symmetric and u = 0 on the Dirichlet ring, the face sum of R17 equals
+    the node form ⟨u^{n+1}, K̃u^n⟩ = −Σ u^{n+1}·L(u^n) (summation by parts), so
+    E = (dx·dy/dt²)·[Σ (u^{n+1} − u^n)² − Σ u^{n+1}·L(u^n)] — the form the fused GPU energy
+    evaluates.  Checked on random faces and fields (2D and 1D), using the oracle's own L and energy."""
+    rng = np.random.default_rng(21)
+    for dim, shape in ((2, (23, 31)), (1, (40,))):
+        ny, nx = (shape[0], shape[1]) if dim == 2 else (1, shape[0])
+        dx, dy, dt = 0.03, 0.05, 0.004
+        h1 = rng.uniform(0.5, 2.0, (ny, nx - 1) if dim == 2 else (nx - 1,))
+        h2 = rng.uniform(0.5, 2.0, (ny - 1, nx)) if dim == 2 else None
+        c1 = oracle.prescale(h1, dt, dx, np.float64)
+        c2 = oracle.prescale(h2, dt, dy, np.float64) if dim == 2 else None
+        a = rng.standard_normal(shape)
+        b = rng.standard_normal(shape)
+        for u in (a, b):
+            if dim == 2:
+                u[0, :] = u[-1, :] = u[:, 0] = u[:, -1] = 0.0
+            else:
+                u[0] = u[-1] = 0.0
+        E = oracle.energy(dim, c1, c2, a, b, dx, dy, dt)
+        w = (dx * dy if dim == 2 else dx) / dt ** 2
+        node = w * (np.sum((a - b) ** 2) - np.sum(a * oracle.lap(dim, c1, c2, b)))
+        assert abs(node - E) <= 1e-12 * abs(E)
