@@ -228,7 +228,7 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                             allocates two more levels; results are bitwise those of K = 1).  A
                             tsw_step call's remainder of r levels (2 ≤ r < K) runs as one pass of
                             depth r.  Default 1. */
-#define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil, 3..16 (default 4) */
+#define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil: 4 (default), 8 or 16 */
 #define TSW_OPT_SCHEME 8   /* 0 (default): explicit leapfrog (north_star).  1: the paper's implicit method
                               (§3.3, reading R26): factorised three-level Crank–Nicolson
                               (I − ½L_x)(I − ½L_y)(u^{n+1} + u^{n−1}) = 2u^n, start u¹ = B⁻¹u⁰ + dt·u₁ (R27),

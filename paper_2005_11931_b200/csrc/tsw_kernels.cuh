@@ -804,14 +804,16 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         bulk_g2s(st, a.un + e, WE * sizeof(T), &full[slot]);
         bulk_g2s(st + WE, a.unm1 + e, WE * sizeof(T), &full[slot]);
     };
-    int rot = 0;  // the warp that issues the next refill
+    // the ring depth is a power of two (the runtime checks): slot = loaded-row count & dmask
+    const int dmask = depth - 1;
+    const int dlog = __ffs(depth) - 1;
 
     const int e0 = tid * V;  // my first column of the extended strip
+    T* const cen0 = cen + e0;          // my element in the centre-row buffers of parity 0 / 1
+    T* const cen1 = cen + WEP + e0;
     // interior storage rows of the global grid: g ∈ [1, ny−2] ⇔ storage s ∈ [rowlo, rowhi]
     const int rowlo = int(1 - a.r0 + 1), rowhi = int(a.ny - 2 - a.r0 + 1);
-    int cslot = 0;      // ring slot of the next loaded row, and its mbarrier phase parity
-    uint32_t cphase = 0;
-    int lslot = 0;      // the slot the previous row consumed
+    int gs = 0;         // rows loaded from the ring so far: slot gs & dmask, phase parity (gs >> dlog) & 1
     TbState<T, K> S;
     double en_acc = 0.0;   // EN: this thread's sum over its output nodes of the current item
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
@@ -872,12 +874,8 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
         const int64_t ibase = b * a.mstride + int64_t(in_lo) * a.pitch + cs - H;
         __syncthreads();
         if (warp == 0 && elect_one()) {
-            int sl = cslot;
             const int pre = min(depth, nload);
-            for (int r = 0; r < pre; ++r) {
-                issue_stage(sl, ibase + int64_t(r) * a.pitch);
-                if (++sl == depth) sl = 0;
-            }
+            for (int r = 0; r < pre; ++r) issue_stage((gs + r) & dmask, ibase + int64_t(r) * a.pitch);
         }
 
         // one input row: barrier, refill, stage read, wavefront (phase PH), output
@@ -885,37 +883,39 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             constexpr int PH = decltype(ph)::value;
             constexpr bool MASKED = decltype(msk)::value;
             const int R = in_lo + i;
-            if (TSW_TB_WAIT1 && tid == 0 && i < nload) mbar_wait(&full[cslot], cphase);
+            if (TSW_TB_WAIT1 && tid == 0 && i < nload) mbar_wait(&full[gs & dmask], uint32_t(gs >> dlog) & 1u);
             if (TSW_TB_JITTER) tb_jitter(R, warp, 0);
             __syncthreads();  // the previous rows' stages and centre rows are consumed / published
             if (TSW_TB_JITTER) tb_jitter(R, warp, 1);
             // refill the stage consumed by the previous row (its shared-memory reads completed
             // before this barrier: the values were used in that row's arithmetic) with the item's
             // row `depth` further on
-            if (i >= 1 && i - 1 + depth < nload) {
-                if (warp == rot && elect_one()) issue_stage(lslot, ibase + int64_t(i - 1 + depth) * a.pitch);
-                if (++rot == NC) rot = 0;
+            if (i >= 1 && i - 1 + depth < nload) {   // row i − 1 consumed slot (gs − 1) & dmask
+                if (warp == (i & (NC - 1)) && elect_one())
+                    issue_stage((gs - 1) & dmask, ibase + int64_t(i - 1 + depth) * a.pitch);
             }
             const int par = R & 1;
             T* cw;
             const T* cr;
             T lr1[V];  // level 1's left/right neighbours, before the stage wait
-            cw = cen + par * WEP + e0;
-            cr = cen + (par ^ 1) * WEP + e0;
+            if constexpr (sizeof(T) == 4) {   // fp32 (issue-bound): two precomputed bases
+                cw = par ? cen1 : cen0;
+                cr = par ? cen0 : cen1;
+            } else {                            // fp64 (no spare registers): recomputed per row
+                cw = cen + par * WEP + e0;
+                cr = cen + (par ^ 1) * WEP + e0;
+            }
             lr1[0] = cr[-1];
             lr1[1] = cr[V];
             T nw[V], pv_new[V];
             const bool refill = (i < nload);
             if (refill) {
-                if (!TSW_TB_WAIT1) mbar_wait(&full[cslot], cphase);
+                const int cslot = gs & dmask;
+                if (!TSW_TB_WAIT1) mbar_wait(&full[cslot], uint32_t(gs >> dlog) & 1u);
                 const T* st = ring + size_t(cslot) * 2 * WE;
                 lds_v2(st + e0, nw);
                 lds_v2(st + WE + e0, pv_new);
-                lslot = cslot;
-                if (++cslot == depth) {
-                    cslot = 0;
-                    cphase ^= 1u;
-                }
+                ++gs;
             } else {
 #pragma unroll
                 for (int k = 0; k < V; ++k) nw[k] = pv_new[k] = (T)0;

@@ -2713,7 +2713,7 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     if (key == TSW_OPT_TB_DEPTH) {
-        if (value < 3 || value > 16) return fail(TSW_ERR_ARG, "TB ring depth must be in [3, 16]");
+        if (!(value == 4 || value == 8 || value == 16)) return fail(TSW_ERR_ARG, "TB ring depth must be 4, 8 or 16");
         c->tb_depth = int(value);
         for (auto& r : c->tb_occ)
             for (auto& q : r)
