@@ -228,7 +228,8 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                             allocates two more levels; results are bitwise those of K = 1).  A
                             tsw_step call's remainder of r levels (2 ≤ r < K) runs as one pass of
                             depth r.  Default 1. */
-#define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil: 4 (default), 8 or 16 */
+#define TSW_OPT_TB_DEPTH 7 /* input ring stages of the temporally blocked stencil: 4, 8 or 16; 0 (default):
+                              8 for the one-CTA-per-SM variants (the 12-warp fp64 passes), else 4 */
 #define TSW_OPT_SCHEME 8   /* 0 (default): explicit leapfrog (north_star).  1: the paper's implicit method
                               (§3.3, reading R26): factorised three-level Crank–Nicolson
                               (I − ½L_x)(I − ½L_y)(u^{n+1} + u^{n−1}) = 2u^n, start u¹ = B⁻¹u⁰ + dt·u₁ (R27),
@@ -245,10 +246,12 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               0 (default): auto — 2 for fp64 grids of ≥ 8 M nodes, else 3.
                               1: cyclic reduction per line in shared memory with tiled transposes
                               (the paper's solver), ≤ 4095 (fp64) / 8191 (fp32) unknowns per line. */
-#define TSW_OPT_TB_WARPS 13 /* CTA width of the temporally blocked stencil: 8 warps (512-column strips), 4
-                              (256-column strips: less redundant halo work on narrow grids), 0 (default):
-                              4 where its strips compute ≥ 5 % fewer columns, and for a slab's launch of
-                              its first / last K rows; else 8 */
+#define TSW_OPT_TB_WARPS 13 /* CTA width of the temporally blocked stencil: 8 = the wide CTA (8 warps,
+                              512-column strips, two CTAs per SM; fp64 passes of depth ≥ 7: 12 warps,
+                              768-column strips, one CTA per SM), 4 (256-column strips: less redundant
+                              halo work on narrow grids), 0 (default): 4 where its strips compute ≥ 5 %
+                              fewer columns, and for a slab's launch of its first / last K rows; else
+                              the wide CTA */
 #define TSW_OPT_ENERGY_FUSE 14 /* 1 (default): on a single-rank 2D temporally blocked run, the last pass of
                               every tsw_step call also reduces the discrete energy of the two levels it
                               writes (S5 fused into S3: per-item fp64 partials, plus the faces across its

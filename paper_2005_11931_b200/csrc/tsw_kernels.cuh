@@ -577,10 +577,38 @@ struct TbPad {
 #ifndef TSW_TB_YCACHE_SMEM
 #define TSW_TB_YCACHE_SMEM 0
 #endif
+#ifndef TSW_TB_YCACHE_F64
+#define TSW_TB_YCACHE_F64 0
+#endif
 template <typename T> struct TbYCache {
-    static constexpr bool on = sizeof(T) == 4;                             // registers
+    static constexpr bool on = sizeof(T) == 4 || TSW_TB_YCACHE_F64;      // registers
     static constexpr bool smem = sizeof(T) == 8 && TSW_TB_YCACHE_SMEM;     // shared memory
 };
+
+// Register budget and CTA width.  A CTA of NC warps is sized for 16 / NC CTAs per SM (at least
+// one): 8 warps → two CTAs of 128 registers per thread; TSW_TB_NCW_F64 = 12 (default) → one
+// 12-warp CTA per SM with up to 170 registers per thread (768-column strips) for the deep fp64
+// passes (K ≥ TSW_TB_NCW_KMIN): measured fp64 K = 8 918 → 976 Gpt/s (985 with an 8-stage ring),
+// K = 7 905 → 943 — the compiler schedules the K-level chain better with the larger budget, and
+// 12 warps per SM hide the fp64 latency (10, 11, 14 or 16 warps, or 8 warps at 198 registers
+// with the y-flux cache in registers, were slower).  TSW_TB_MINB_F64 = 1 forces one CTA per SM
+// for every fp64 width; TSW_TB_YCACHE_F64 = 1 keeps the fp64 y-flux cache in registers.
+#ifndef TSW_TB_MINB_F64
+#define TSW_TB_MINB_F64 0
+#endif
+#ifndef TSW_TB_NCW_F64
+#define TSW_TB_NCW_F64 12
+#endif
+#define TSW_TB_MINB(T, NC) ((sizeof(T) == 8 && TSW_TB_MINB_F64) ? TSW_TB_MINB_F64 : (16 / (NC) > 0 ? 16 / (NC) : 1))
+#ifndef TSW_TB_NCW_KMIN
+#define TSW_TB_NCW_KMIN 7   // the wide fp64 CTA for passes of depth ≥ this (shallower: 8 warps, 2 CTAs/SM)
+#endif
+#ifndef TSW_TB_NCW_F32
+#define TSW_TB_NCW_F32 8
+#endif
+template <typename T, int K = 8> constexpr int tb_wide_nc() {
+    return K < TSW_TB_NCW_KMIN ? 8 : (sizeof(T) == 8 ? TSW_TB_NCW_F64 : TSW_TB_NCW_F32);
+}
 
 // TSW_TB_JITTER=1 (debug builds only): a pseudo-random per-(CTA, warp, row) delay of up to ~2 µs
 // before and after every row barrier, so warps reach the barrier, read the centre rows and the
@@ -750,7 +778,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
 // the previous rows (every thread has passed the per-row barrier, so they are free) with the next
 // stages of its stream (needs a ring of ≥ 3 stages).
 template <typename T, int K, bool PEER = false, int NC = TB_NC, bool EN = false>
-__global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> a, int depth) {
+__global__ void __launch_bounds__(NC * 32, TSW_TB_MINB(T, NC)) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K, NC>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
     constexpr int PAD = TbPad<T>::P, WEP = WE + 2 * PAD;
@@ -891,7 +919,7 @@ __global__ void __launch_bounds__(NC * 32, 16 / NC) k_step2d_tb(const TbArgs<T> 
             // before this barrier: the values were used in that row's arithmetic) with the item's
             // row `depth` further on
             if (i >= 1 && i - 1 + depth < nload) {   // row i − 1 consumed slot (gs − 1) & dmask
-                if (warp == (i & (NC - 1)) && elect_one())
+                if (warp == (i % NC) && elect_one())
                     issue_stage((gs - 1) & dmask, ibase + int64_t(i - 1 + depth) * a.pitch);
             }
             const int par = R & 1;

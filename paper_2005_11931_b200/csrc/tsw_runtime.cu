@@ -232,7 +232,7 @@ struct tsw_ctx {
     void* imp_cB = nullptr;
     void* imp_ccon = nullptr;   //   βz₁, A₂' [B][2][ncolp]
     bool imp_ycol_stale = true;
-    int tb_depth = 4;     // its input ring stages
+    int tb_depth = 0;     // its input ring stages (0: 8 for one-CTA-per-SM variants, else 4)
     int tb_occ[2][9][2] = {};  // [f64][K][8 warps] resident CTAs per SM (cached)
     int tb_warps = 0;          // CTA width of the temporally blocked stencil: 0 auto, 4 or 8 warps
     int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
@@ -756,10 +756,10 @@ bool peer_mode(const tsw_ctx* c) { return c->g.nranks > 1 && c->g.dim == 2 && c-
 template <typename T, int K, int NC>
 tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi, int32_t s_lo2, int32_t s_hi2) {
     using G = TbGeom<T, K, NC>;
-    const int depth = c->tb_depth;
+    const int depth = c->tb_depth ? c->tb_depth : (TSW_TB_MINB(T, NC) == 1 ? 8 : 4);
     const size_t smem = tb_smem_bytes<T, K, NC>(depth);
     const bool peer = peer_mode(c);
-    int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K][NC == 8 ? 1 : 0];
+    int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K][NC == 4 ? 0 : 1];
     if (occ == 0) {
         CK((tb_setup<T, K, NC, false>(smem, &occ)));
         int occ_en = 0;
@@ -858,7 +858,8 @@ tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi
     return TSW_OK;
 }
 
-// CTA width: 8 warps (512-column strips) or 4 (256-column strips).  Auto (TSW_OPT_TB_WARPS = 0):
+// CTA width: the wide CTA (8 warps, 512-column strips; fp64 passes of depth ≥ 7: 12 warps,
+// 768-column strips, one CTA per SM — tb_wide_nc) or 4 (256-column strips).  Auto (TSW_OPT_TB_WARPS = 0):
 // 4 warps only where its strips compute ≥ 5 % fewer columns (narrow grids, e.g. config 5's 2048:
 // +12 % fp64, +17 % fp32 measured; at 4096 columns 8 warps are as fast or faster)
 template <typename T, int K>
@@ -874,12 +875,13 @@ tsw_status launch_tb_t(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi,
     if (!nc && (s_hi - s_lo) + (s_hi2 - s_lo2) <= 2 * K) {
         nc = 4;  // a slab's boundary rows: few rows, so twice the CTAs (256-column strips)
     } else if (!nc) {
-        const int64_t cols8 = (c->pitch + TbGeom<T, K, 8>::WO - 1) / TbGeom<T, K, 8>::WO * TbGeom<T, K, 8>::WE;
+        constexpr int W = tb_wide_nc<T, K>();
+        const int64_t cols8 = (c->pitch + TbGeom<T, K, W>::WO - 1) / TbGeom<T, K, W>::WO * TbGeom<T, K, W>::WE;
         const int64_t cols4 = (c->pitch + TbGeom<T, K, 4>::WO - 1) / TbGeom<T, K, 4>::WO * TbGeom<T, K, 4>::WE;
         nc = (double(cols4) < 0.95 * double(cols8)) ? 4 : 8;
     }
     return nc == 4 ? launch_tb_nc<T, K, 4>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2)
-                   : launch_tb_nc<T, K, 8>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+                   : launch_tb_nc<T, K, tb_wide_nc<T, K>()>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
 }
 
 template <typename T>
@@ -2713,7 +2715,8 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     if (key == TSW_OPT_TB_DEPTH) {
-        if (!(value == 4 || value == 8 || value == 16)) return fail(TSW_ERR_ARG, "TB ring depth must be 4, 8 or 16");
+        if (!(value == 0 || value == 4 || value == 8 || value == 16))
+            return fail(TSW_ERR_ARG, "TB ring depth must be 0 (auto), 4, 8 or 16");
         c->tb_depth = int(value);
         for (auto& r : c->tb_occ)
             for (auto& q : r)

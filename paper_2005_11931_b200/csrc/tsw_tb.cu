@@ -39,7 +39,7 @@ cudaError_t tb_launch(bool push, unsigned blocks, size_t smem, cudaStream_t stre
     template cudaError_t tb_setup<TSW_TB_DTYPE, K, NC, bool(TSW_TB_EN)>(size_t, int*);                       \
     template cudaError_t tb_launch<TSW_TB_DTYPE, K, NC, bool(TSW_TB_EN)>(bool, unsigned, size_t, cudaStream_t, \
                                                                          const TbArgs<TSW_TB_DTYPE>&, int);
-#define TSW_TB_INST_K(K) TSW_TB_INST(K, 8) TSW_TB_INST(K, 4)
+#define TSW_TB_INST_K(K) TSW_TB_INST(K, (tb_wide_nc<TSW_TB_DTYPE, K>())) TSW_TB_INST(K, 4)
 TSW_TB_INST_K(2)
 TSW_TB_INST_K(3)
 TSW_TB_INST_K(4)

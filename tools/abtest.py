@@ -19,6 +19,8 @@ def main():
     s = tsw.Solver.from_config(cfg, dtype)
     if os.environ.get("TSW_AB_WARPS"):   # CTA width of the TB stencil (TSW_OPT_TB_WARPS)
         s.set_option(tsw.TSW_OPT_TB_WARPS, int(os.environ["TSW_AB_WARPS"]))
+    if os.environ.get("TSW_AB_DEPTH"):   # input ring stages (TSW_OPT_TB_DEPTH)
+        s.set_option(tsw.TSW_OPT_TB_DEPTH, int(os.environ["TSW_AB_DEPTH"]))
     s.set_initial(inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(npdt), None, cfg.dt,
                   flags=tsw.TSW_INIT_SHARED)
     s.step(1)
