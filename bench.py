@@ -35,7 +35,8 @@ sys.path.insert(0, ROOT)
 METRIC = "2D stencil Gpoint-updates/s & HBM GB/s vs 8 TB/s peak, at 1/2/4/8 B200"
 UNIT = "Gpt/s"
 ESZ = {"f64": 8, "f32": 4}
-TB_DEFAULT = {"f64": 8, "f32": 8}   # levels per HBM pass (sweep optimum on B200, profiles/r01)
+TB_DEFAULT = {"f64": 10, "f32": 10}   # levels per HBM pass (round-2 sweep on B200: 10 ≥ 8 per pass, and a
+                                      # 20- or 100-level call needs no shallower remainder pass)
 
 
 def words_per_update(steps: int, cadence: int, K: int) -> float:

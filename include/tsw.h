@@ -223,7 +223,7 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
 #define TSW_OPT_KERNEL 3 /* 0: CTA-wide TMA bulk-copy row pipeline (default); 1: register-prefetch kernel */
 #define TSW_OPT_DEPTH 4  /* TMA ring stages per CTA, 2..32 (default 4) */
 #define TSW_OPT_GRAPHS 5 /* 1 (default): single-rank steps replay a CUDA graph of two levels; 0: plain launches */
-#define TSW_OPT_TBLOCK 6 /* K ∈ {1,…,8}: levels per HBM pass of the temporally blocked stencil
+#define TSW_OPT_TBLOCK 6 /* K ∈ {1,…,10}: levels per HBM pass of the temporally blocked stencil
                             (2D, δ-line / constant / profile kinds; slabs use K-deep ghost rows;
                             allocates two more levels; results are bitwise those of K = 1).  A
                             tsw_step call's remainder of r levels (2 ≤ r < K) runs as one pass of

@@ -493,8 +493,9 @@ __global__ void __launch_bounds__((TMA_NC + 1) * 32) k_step2d_tma(const StepArgs
 // Every node value is the same canonical expression as k_step2d (bitwise identical results);
 // Dirichlet rows/columns are forced to +0 at every level.
 constexpr int TB_NC = 8;
-// ghost rows per side of a slab: the deepest temporal blocking (K = 8) exchanges 8 rows every 8 levels
-constexpr int TSW_MAX_GHOST = 8;
+// deepest temporal blocking, and ghost rows per side of a slab (a pass of K levels exchanges K rows)
+constexpr int TSW_MAX_TB = 10;
+constexpr int TSW_MAX_GHOST = TSW_MAX_TB;
 
 template <typename T, int K, int NC = TB_NC>
 struct TbGeom {

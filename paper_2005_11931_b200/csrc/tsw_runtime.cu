@@ -233,7 +233,7 @@ struct tsw_ctx {
     void* imp_ccon = nullptr;   //   βz₁, A₂' [B][2][ncolp]
     bool imp_ycol_stale = true;
     int tb_depth = 0;     // its input ring stages (0: 8 for one-CTA-per-SM variants, else 4)
-    int tb_occ[2][9][2] = {};  // [f64][K][8 warps] resident CTAs per SM (cached)
+    int tb_occ[2][TSW_MAX_TB + 1][2] = {};  // [f64][K][wide CTA] resident CTAs per SM (cached)
     int tb_warps = 0;          // CTA width of the temporally blocked stencil: 0 auto, 4 or 8 warps
     int bulk_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
     int bulk_occ_key[2][2] = {{0, 0}, {0, 0}};
@@ -894,6 +894,8 @@ tsw_status launch_tb_k(tsw_ctx* c, int K, int fk, int fkm1, int32_t s_lo, int32_
         case 6: return launch_tb_t<T, 6>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
         case 7: return launch_tb_t<T, 7>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
         case 8: return launch_tb_t<T, 8>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 9: return launch_tb_t<T, 9>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
+        case 10: return launch_tb_t<T, 10>(c, fk, fkm1, s_lo, s_hi, s_lo2, s_hi2);
         default: return fail(TSW_ERR_ARG, "unsupported temporal blocking depth %d", K);
     }
 }
@@ -2610,8 +2612,8 @@ tsw_status tsw_set_option(tsw_ctx* c, int32_t key, int64_t value) {
         return TSW_OK;
     }
     if (key == TSW_OPT_TBLOCK) {
-        if (!(value >= 1 && value <= 8))
-            return fail(TSW_ERR_ARG, "temporal blocking depth must be 1..8");
+        if (!(value >= 1 && value <= TSW_MAX_TB))
+            return fail(TSW_ERR_ARG, "temporal blocking depth must be 1..%d", TSW_MAX_TB);
         if (value > 1 && c->g.dim != 2) return fail(TSW_ERR_ARG, "temporal blocking needs a 2D grid");
         if (value > 1 && c->g.nranks > 1 && value > c->G)
             return fail(TSW_ERR_ARG, "temporal blocking depth %d exceeds the %d ghost rows of a slab", int(value), c->G);

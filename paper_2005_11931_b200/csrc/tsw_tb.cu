@@ -47,5 +47,7 @@ TSW_TB_INST_K(5)
 TSW_TB_INST_K(6)
 TSW_TB_INST_K(7)
 TSW_TB_INST_K(8)
+TSW_TB_INST_K(9)
+TSW_TB_INST_K(10)
 
 }  // namespace tsw

@@ -22,7 +22,7 @@ def _oracle_energy(s, cfg, b, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("K,nsteps", [(8, 17), (8, 16), (4, 13), (5, 11), (7, 15), (2, 9), (3, 7), (6, 13)])
+@pytest.mark.parametrize("K,nsteps", [(8, 17), (8, 16), (4, 13), (5, 11), (7, 15), (2, 9), (3, 7), (6, 13), (10, 20), (9, 13)])
 @pytest.mark.parametrize("shape", [(97, 700), (300, 2049), (7, 515)])
 def test_fused_energy_matches_oracle(dtype, K, nsteps, shape):
     """Every pass depth (the call's last pass is a full K pass or the remainder), both CTA widths

@@ -31,7 +31,7 @@ def _group(cfg, P, K, dtype="f64"):
 
 
 @pytest.mark.parametrize("P", [2, 3])
-@pytest.mark.parametrize("K", [1, 4, 5, 8])
+@pytest.mark.parametrize("K", [1, 4, 5, 8, 10])
 @pytest.mark.parametrize("ny", [151, 29])
 def test_peer_halo_slabs_bitwise(P, K, ny):
     cfg = inputs.config(3, nx=700, ny=ny, dx=0.01, dy=0.01, eps=[0.1, 0.3], amp=[1.0, 2.0], dt=2e-3)
@@ -62,7 +62,7 @@ def test_peer_halo_slabs_bitwise(P, K, ny):
     ref.close()
 
 
-@pytest.mark.parametrize("K,n", [(4, 41), (8, 45)])
+@pytest.mark.parametrize("K,n", [(4, 41), (8, 45), (10, 41)])
 def test_peer_halo_bench_shape_sampled(K, n):
     """The bench workload split into 2 slabs with K-deep peer halos (K = 8: a 4-level remainder
     pass): the slabs ≡ the single domain stepped one level at a time."""

@@ -25,7 +25,7 @@ def _run(cfg, dtype, K, nsteps, u0, rows_per_item=0, profile=None):
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("K", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("K", [2, 3, 4, 5, 6, 7, 8, 9, 10])
 def test_tblock_bitwise_vs_oracle(dtype, K):
     cfg = inputs.config(3, nx=1300, ny=211, dx=0.01, dy=0.01, eps=[0.05, 0.3], amp=[1.0, 0.0], dt=2e-3)
     u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(NP[dtype])
@@ -48,7 +48,7 @@ def test_tblock_bitwise_vs_oracle(dtype, K):
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("K,levels", [(8, 13), (8, 10), (5, 7), (4, 3)])
+@pytest.mark.parametrize("K,levels", [(8, 13), (8, 10), (5, 7), (4, 3), (10, 23), (9, 9)])
 def test_tblock_remainder_is_one_shallower_pass(dtype, K, levels):
     """A stepping call of q·K + r levels (2 ≤ r < K) runs q passes of depth K and ONE pass of depth r
     (not r one-level steps) — one launch per pass — with the bits of one-level stepping."""
@@ -114,7 +114,7 @@ def test_tblock_bench_shape_sampled(K):
 
 
 @pytest.mark.parametrize("P", [2, 3])
-@pytest.mark.parametrize("K", [2, 5, 8])
+@pytest.mark.parametrize("K", [2, 5, 8, 10])
 @pytest.mark.parametrize("ny", [151, 31])
 def test_tblock_loopback_slabs_bitwise(P, K, ny):
     """k-deep ghost rows: P slabs on one GPU (tsw_group_step, K-row exchanges of both levels every
@@ -158,7 +158,7 @@ def test_concurrent_contexts_do_not_interfere():
         busy.close()
 
 
-@pytest.mark.parametrize("K", [2, 4, 8])
+@pytest.mark.parametrize("K", [2, 4, 8, 10])
 @pytest.mark.parametrize("shape", [(3, 3), (4, 5), (5, 67), (6, 2000)])
 def test_tblock_degenerate_grids(K, shape):
     """One interior node, a single interior row or column, a strip narrower than the halo: the

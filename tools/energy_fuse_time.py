@@ -16,12 +16,13 @@ def main():
     cfg = inputs.weak_unit(1)
     npdt = np.float64 if dtype == "f64" else np.float32
     s = tsw.Solver.from_config(cfg, dtype)
-    s.set_option(tsw.TSW_OPT_TBLOCK, 8)
+    s.set_option(tsw.TSW_OPT_TBLOCK, max(Ks))
     s.set_initial(inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny).astype(npdt), None, cfg.dt,
                   flags=tsw.TSW_INIT_SHARED)
     s.step(17)
     out = {"dtype": dtype}
     for K in Ks:
+        s.set_option(tsw.TSW_OPT_TBLOCK, K)
         res = {0: [], 1: []}
         for rep in range(6):
             for fuse in (0, 1):
