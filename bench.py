@@ -7,7 +7,7 @@ GPU (global grid 32768 × 4096·N, dx = dy = 0.0025, ε = 0.05, dt = 4e−4), de
 data (SURVEY §8(d) data-independence guard), fp64 by default.  One "step" = one pass of the
 hot path over the slab: the leapfrog stencil (S3), the NCCL ghost-row exchange at N > 1 (S4),
 and the discrete-energy reduction every `--energy-every` steps (S5).  By default the stencil is
-temporally blocked (K = 8 levels per HBM pass in both precisions by default; a stepping call's
+temporally blocked (K = 10 levels per HBM pass in both precisions by default; a stepping call's
 remainder of r < K levels is one pass of depth r; K-deep ghost rows on slabs); `--tblock 1` times
 the one-level-per-pass kernel.  Inputs (2 × 1.07 GB per
 GPU in fp64) exceed the 126 MB L2, so no flush is needed between steps.
