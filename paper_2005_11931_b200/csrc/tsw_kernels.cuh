@@ -754,8 +754,10 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
                         const double crr = (double)S.c1r[k], c2 = (double)S.c2v[k];
                         lapd = (crr * (ur - uc) - cl * (uc - ul)) + (c2 * (uu - uc) - c2 * (uc - ud));
                     }
-                    const double A = (double)nv[k], B = (double)cu;
-                    *en_acc += (A - B) * (A - B) - A * lapd;
+                    // accumulated with two fused multiply-adds (the energy is a diagnostic, not the
+                    // canonical stepping tree): acc + (a − b)² − a·L(b)
+                    const double A = (double)nv[k], D = A - (double)cu;
+                    *en_acc = __fma_rn(-A, lapd, __fma_rn(D, D, *en_acc));
                 }
             }
         }
