@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-for L in w12 w16; do TSW_LIB=abl/$L.so timeout 900 python -m pytest tests/test_tblock_gpu.py tests/test_energy_fused_gpu.py -q -x -p no:cacheprovider -k "not f32" > gpurun_out/pytest_$L.log 2>&1; echo "$L pytest=$? $(tail -1 gpurun_out/pytest_$L.log)"; done
-bash tools/abdepth.sh "cur w10 w12 w16" "f64:8 f64:4 f64:7" 2 "4"
+bash tools/ablibs.sh "cur lu0 lu1" "f64:10" 1
