@@ -601,6 +601,12 @@ template <typename T> struct TbYCache {
 #define TSW_TB_NCW_F64 12
 #endif
 #define TSW_TB_MINB(T, NC) ((sizeof(T) == 8 && TSW_TB_MINB_F64) ? TSW_TB_MINB_F64 : (16 / (NC) > 0 ? 16 / (NC) : 1))
+// per pass depth: the narrow fp64 CTA (4 warps: slab boundary rows, narrow grids) of depth ≥ 8 is
+// sized for 3 CTAs per SM (170 registers, as the wide CTA) — at 4 CTAs (128 registers) K = 10
+// spilled 1.3 KB
+template <typename T, int K, int NC> constexpr int tb_minb() {
+    return (sizeof(T) == 8 && NC == 4 && K >= 8 && !TSW_TB_MINB_F64) ? 3 : TSW_TB_MINB(T, NC);
+}
 #ifndef TSW_TB_NCW_KMIN
 #define TSW_TB_NCW_KMIN 7   // the wide fp64 CTA for passes of depth ≥ this (shallower: 8 warps, 2 CTAs/SM)
 #endif
@@ -781,7 +787,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
 // the previous rows (every thread has passed the per-row barrier, so they are free) with the next
 // stages of its stream (needs a ring of ≥ 3 stages).
 template <typename T, int K, bool PEER = false, int NC = TB_NC, bool EN = false>
-__global__ void __launch_bounds__(NC * 32, TSW_TB_MINB(T, NC)) k_step2d_tb(const TbArgs<T> a, int depth) {
+__global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K, NC>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
     constexpr int PAD = TbPad<T>::P, WEP = WE + 2 * PAD;
@@ -846,7 +852,10 @@ __global__ void __launch_bounds__(NC * 32, TSW_TB_MINB(T, NC)) k_step2d_tb(const
     const int rowlo = int(1 - a.r0 + 1), rowhi = int(a.ny - 2 - a.r0 + 1);
     int gs = 0;         // rows loaded from the ring so far: slot gs & dmask, phase parity (gs >> dlog) & 1
     TbState<T, K> S;
-    double en_acc = 0.0;   // EN: this thread's sum over its output nodes of the current item
+    // EN: this thread's sum over its output nodes of the current item.  In registers: a running
+    // sum in a shared-memory slot (one read-modify-write per row) removed the 16-byte spill of the
+    // fp64 K = 10 EN pass but raised its cost over the plain pass from 5.1 % to 8.5 % (measured).
+    double en_acc = 0.0;
     for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
         int64_t cs;
         int s0, s1, b, in_lo, in_hi;
@@ -1636,10 +1645,20 @@ __global__ void k_wave2_final(const ArgVal* __restrict__ partial, int nblk, doub
 // P:831–838 ‖u_{ε1}(t) − u_{ε2}(t)‖_{L²}), the L² pieces of Theorem lem 1's energy estimate
 // and the W^{1,∞} norms of the regularised depth (Assumption).
 // ------------------------------------------------------------------------------------------
-// Pairwise Σ_nodes (u_i − u_j)²: a CTA stages TN consecutive nodes of one row of ALL members in
-// shared memory; each thread owns a 4×4 block of member pairs (register blocking: 8 loads for 16
-// differences).  Partial sums per CTA, summed in a fixed order by k_family_final.
-constexpr int FAM_TN = 64;
+// Pairwise Σ_nodes (u_i − u_j)²: a dense all-pairs reduction, bound by the fp64 pipe (a
+// subtraction and a fused multiply-add per member pair and node), not by HBM.  A thread owns the
+// 4 × 4 accumulators of one block of member pairs (I ≤ J; register blocking: 8 shared-memory
+// loads for 16 pairs); a CTA holds up to 512 consecutive blocks (blockIdx.y: the group of blocks,
+// for batches above 88) and a contiguous range of node tiles (blockIdx.x).  Tiles of FAM_TN nodes
+// of all B members are double-buffered in shared memory, the next one prefetched into registers
+// while the current one is consumed (one barrier per tile).  Member m's row starts at
+// m·FAM_TP + (m >> 2): consecutive pair blocks of a warp read rows 4J + k whose starts differ by
+// 4·FAM_TP + 1 ≡ 1 (mod 16) doubles, i.e. distinct banks; lanes of one I share x (broadcast).
+// Member rows B .. 4·nblk − 1 stay zero.
+constexpr int FAM_TN = 32;                 // nodes per tile
+constexpr int FAM_TP = FAM_TN;             // row pitch (a multiple of 4: see the skew above)
+constexpr int FAM_EPT = 16;                // prefetch registers per thread: B · FAM_TN ≤ 16 · threads
+constexpr int FAM_MAXT = 512;              // threads per CTA (≤ 512 blocks per group)
 struct FamilyArgs {
     const void* u;
     int64_t nx, pitch, mstride;
@@ -1647,56 +1666,126 @@ struct FamilyArgs {
     int32_t row0;      // first storage row (2D: 1, 1D: 0)
     int32_t B, nblk;   // members, member blocks of 4
     int64_t tiles_per_row;
+    int64_t ntiles, tiles_per_cta;
 };
+__host__ __device__ constexpr int fam_rows_elems(int nblk) { return 4 * nblk * FAM_TP + nblk; }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_family_l2(const FamilyArgs a, double* __restrict__ partial) {
-    extern __shared__ __align__(16) double tile[];  // [B][FAM_TN + 1]
+__global__ void __launch_bounds__(FAM_MAXT) k_family_l2(const FamilyArgs a, double* __restrict__ partial) {
+    extern __shared__ __align__(16) double fam_smem[];   // [2][fam_rows_elems(nblk)]
+    const int nt = blockDim.x;
+    const int tid = threadIdx.x;
+    const int BUF = fam_rows_elems(a.nblk);
     const int npairs = a.nblk * (a.nblk + 1) / 2;
-    double acc[4][4];
-    // this thread's block pair (I ≤ J); threads beyond npairs only help loading
+    const int p = blockIdx.y * nt + tid;                  // my pair block
+    const bool owner = p < npairs;
     int I = 0, J = 0;
-    const bool owner = threadIdx.x < npairs;
     if (owner) {
-        int p = threadIdx.x, row = 0;
-        while (p >= a.nblk - row) { p -= a.nblk - row; ++row; }
+        int q = p, row = 0;
+        while (q >= a.nblk - row) { q -= a.nblk - row; ++row; }
         I = row;
-        J = row + p;
+        J = row + q;
     }
+    double acc[4][4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int l = 0; l < 4; ++l) acc[k][l] = 0.0;
+    for (int e = tid; e < 2 * BUF; e += nt) fam_smem[e] = 0.0;   // padding rows stay 0
     const T* U = static_cast<const T*>(a.u);
-    const int64_t ntiles = int64_t(a.rows) * a.tiles_per_row;
-    for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
-        const int64_t r = a.row0 + tile_id / a.tiles_per_row;
-        const int64_t c0 = (tile_id % a.tiles_per_row) * FAM_TN;
-        __syncthreads();
-        for (int e = threadIdx.x; e < a.B * FAM_TN; e += blockDim.x) {
+    const int64_t t0 = int64_t(blockIdx.x) * a.tiles_per_cta;
+    const int64_t t1 = min(t0 + a.tiles_per_cta, a.ntiles);
+    const int nel = a.B * FAM_TN;
+    // fp64: the next tile goes straight to shared memory (cp.async, zero-filled past the row end:
+    // no prefetch registers, more CTAs per SM); fp32: through registers (converted on the store)
+    constexpr bool ASYNC = sizeof(T) == 8;
+    auto fetch_async = [&](int64_t t, int buf) {
+        const int64_t r = a.row0 + t / a.tiles_per_row;
+        const int64_t c0 = (t % a.tiles_per_row) * FAM_TN;
+        const T* base = U + r * a.pitch + c0;
+        const int64_t lim = a.nx - c0;
+        double* tb = fam_smem + buf * BUF;
+        for (int e = tid; e < nel; e += nt) {
             const int m = e / FAM_TN, cc = e % FAM_TN;
-            const int64_t col = c0 + cc;
-            tile[m * (FAM_TN + 1) + cc] = (col < a.nx) ? (double)U[m * a.mstride + r * a.pitch + col] : 0.0;
+            const bool in = cc < lim;
+            const uint32_t dst = smem_u32(tb + m * FAM_TP + (m >> 2) + cc);
+            const T* src = in ? base + m * a.mstride + cc : base;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(in ? 8 : 0)
+                         : "memory");
         }
-        __syncthreads();
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    T pf[ASYNC ? 1 : FAM_EPT];
+    auto fetch = [&](int64_t t) {
+        const int64_t r = a.row0 + t / a.tiles_per_row;
+        const int64_t c0 = (t % a.tiles_per_row) * FAM_TN;
+        const T* base = U + r * a.pitch + c0;
+        const int64_t lim = a.nx - c0;
+#pragma unroll
+        for (int q = 0; q < (ASYNC ? 1 : FAM_EPT); ++q) {
+            const int e = tid + q * nt;
+            pf[q] = (T)0;
+            if (e < nel) {
+                const int m = e / FAM_TN, cc = e % FAM_TN;
+                if (cc < lim) pf[q] = __ldg(base + m * a.mstride + cc);
+            }
+        }
+    };
+    auto stash = [&](int buf) {
+        double* tb = fam_smem + buf * BUF;
+#pragma unroll
+        for (int q = 0; q < (ASYNC ? 1 : FAM_EPT); ++q) {
+            const int e = tid + q * nt;
+            if (e < nel) {
+                const int m = e / FAM_TN, cc = e % FAM_TN;
+                tb[m * FAM_TP + (m >> 2) + cc] = (double)pf[q];
+            }
+        }
+    };
+    __syncthreads();   // the zero fill precedes the first stash
+    if (t0 < t1) {
+        if constexpr (ASYNC) {
+            fetch_async(t0, 0);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        } else {
+            fetch(t0);
+            stash(0);
+        }
+    }
+    __syncthreads();
+    for (int64_t t = t0; t < t1; ++t) {
+        const int buf = int(t - t0) & 1;
+        if (t + 1 < t1) {   // in flight during the arithmetic below (buffer buf ^ 1 was last read
+                            // before the previous barrier)
+            if constexpr (ASYNC) fetch_async(t + 1, buf ^ 1);
+            else fetch(t + 1);
+        }
         if (owner) {
+            const double* tb = fam_smem + buf * BUF;
+            const double* xr = tb + 4 * I * FAM_TP + I;
+            const double* yr = tb + 4 * J * FAM_TP + J;
+#pragma unroll 4
             for (int n = 0; n < FAM_TN; ++n) {
                 double x[4], y[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const int i = 4 * I + k, j = 4 * J + k;
-                    x[k] = (i < a.B) ? tile[i * (FAM_TN + 1) + n] : 0.0;
-                    y[k] = (j < a.B) ? tile[j * (FAM_TN + 1) + n] : 0.0;
+                    x[k] = xr[k * FAM_TP + n];
+                    y[k] = yr[k * FAM_TP + n];
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
 #pragma unroll
                     for (int l = 0; l < 4; ++l) {
                         const double d = x[k] - y[l];
-                        acc[k][l] += d * d;
+                        acc[k][l] = __fma_rn(d, d, acc[k][l]);
                     }
             }
         }
+        if (t + 1 < t1) {
+            if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
+            else stash(buf ^ 1);
+        }
+        __syncthreads();
     }
     if (owner) {
         double* out = partial + size_t(blockIdx.x) * a.B * a.B;

@@ -756,7 +756,7 @@ bool peer_mode(const tsw_ctx* c) { return c->g.nranks > 1 && c->g.dim == 2 && c-
 template <typename T, int K, int NC>
 tsw_status launch_tb_nc(tsw_ctx* c, int fk, int fkm1, int32_t s_lo, int32_t s_hi, int32_t s_lo2, int32_t s_hi2) {
     using G = TbGeom<T, K, NC>;
-    const int depth = c->tb_depth ? c->tb_depth : (TSW_TB_MINB(T, NC) == 1 ? 8 : 4);
+    const int depth = c->tb_depth ? c->tb_depth : (tb_minb<T, K, NC>() == 1 ? 8 : 4);
     const size_t smem = tb_smem_bytes<T, K, NC>(depth);
     const bool peer = peer_mode(c);
     int& occ = c->tb_occ[is_f64(c) ? 1 : 0][K][NC == 4 ? 0 : 1];
@@ -2429,11 +2429,27 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
     a.row0 = (c->g.dim == 1) ? 0 : 1;
     a.B = B;
     a.nblk = (B + 3) / 4;
+    // one thread per block of 4 × 4 member pairs (and ≥ B / 16 · FAM_TN threads for the prefetch),
+    // at most FAM_MAXT per CTA: groups of blocks on blockIdx.y
+    const int npairs = a.nblk * (a.nblk + 1) / 2;
+    const int need_t = std::max(npairs, (B * FAM_TN + FAM_EPT - 1) / FAM_EPT);
+    const int nthr = std::min(FAM_MAXT, (need_t + 31) / 32 * 32);
+    const int groups = (npairs + nthr - 1) / nthr;
     a.tiles_per_row = (c->g.nx + FAM_TN - 1) / FAM_TN;
-    if (a.nblk * (a.nblk + 1) / 2 > 256) return fail(TSW_ERR_ARG, "too many members for one CTA of pair blocks");
-    const int64_t ntiles = int64_t(a.rows) * a.tiles_per_row;
-    const int ncta = int(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * c->sm_count)));
-    // partials [ncta][B][B], then the per-pair sums [B][B] (one allocation, grown once)
+    a.ntiles = int64_t(a.rows) * a.tiles_per_row;
+    const size_t smem = size_t(2) * fam_rows_elems(a.nblk) * sizeof(double);
+    if (smem > 48 * 1024) {
+        if (is_f64(c)) CK(cudaFuncSetAttribute(k_family_l2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        else CK(cudaFuncSetAttribute(k_family_l2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    }
+    // one wave: exactly the resident CTAs (all groups), each a contiguous, balanced range of tiles
+    int occ = 1;
+    if (is_f64(c)) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_family_l2<double>, nthr, smem));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_family_l2<float>, nthr, smem));
+    const int64_t want = std::min<int64_t>(a.ntiles, std::max<int64_t>(1, int64_t(std::max(occ, 1)) * c->sm_count / groups));
+    a.tiles_per_cta = (a.ntiles + want - 1) / want;
+    const int ncta = int((a.ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta);
+    // partials [ncta][B][B] (each group writes its own pairs), then the per-pair sums [B][B]
     const size_t need = size_t(ncta + 1) * B * B;
     if (c->fam_cap < need) {
         if (c->d_fam) cudaFree(c->d_fam);
@@ -2444,15 +2460,11 @@ tsw_status tsw_family_l2(tsw_ctx* c, double* out_BB) {
     }
     double* d_sum = c->d_fam + size_t(ncta) * B * B;
     CK(cudaMemsetAsync(c->d_fam, 0, size_t(ncta) * B * B * sizeof(double), c->stream));
-    const size_t smem = size_t(B) * (FAM_TN + 1) * sizeof(double);
-    if (smem > 48 * 1024) {
-        if (is_f64(c)) CK(cudaFuncSetAttribute(k_family_l2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        else CK(cudaFuncSetAttribute(k_family_l2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    }
+    const dim3 grid{unsigned(ncta), unsigned(groups), 1u};
     if (is_f64(c))
-        k_family_l2<double><<<ncta, 256, smem, c->stream>>>(a, c->d_fam);
+        k_family_l2<double><<<grid, nthr, smem, c->stream>>>(a, c->d_fam);
     else
-        k_family_l2<float><<<ncta, 256, smem, c->stream>>>(a, c->d_fam);
+        k_family_l2<float><<<grid, nthr, smem, c->stream>>>(a, c->d_fam);
     CKL();
     k_family_final<<<std::max(1, (B * B + 255) / 256), 256, 0, c->stream>>>(c->d_fam, ncta, B, d_sum);
     CKL();

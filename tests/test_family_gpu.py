@@ -46,6 +46,29 @@ def test_family_l2_and_norms_small(dtype, dim):
     s.close()
 
 
+@pytest.mark.parametrize("dim,B,dtype", [(2, 65, "f64"), (1, 200, "f64"), (2, 37, "f32"), (1, 88, "f32")])
+def test_family_l2_many_members(dim, B, dtype):
+    """All pairs against the oracle for the member counts that select the pair-block groups and
+    node phases of k_family_l2 (B = 65: 3 groups × 51 blocks, H = 5; B = 200: 5 groups, H = 1),
+    on grids whose rows end in a ragged tile."""
+    eps = [0.03 + 0.2 * k / B for k in range(B)]
+    amp = [1.0 + 0.01 * k for k in range(B - 1)] + [0.0]
+    if dim == 1:
+        cfg = inputs.config(1, nx=3001, eps=eps, amp=amp, dt=5e-4)
+    else:
+        cfg = inputs.config(3, nx=203, ny=97, dx=0.02, dy=0.02, eps=eps, amp=amp, dt=2e-3)
+    s = tsw.Solver.from_config(cfg, dtype)
+    s.set_initial(cfg.initial().astype(NP[dtype]), None, cfg.dt, flags=tsw.TSW_INIT_SHARED)
+    s.step(60)
+    un = s.read(0)
+    w = cfg.dx if dim == 1 else cfg.dx * cfg.dy
+    D = s.family_l2()
+    Do = oracle.family_l2(un, w)
+    assert np.all(D == D.T) and np.all(np.diag(D) == 0.0)
+    np.testing.assert_allclose(D, Do, rtol=1e-12, atol=1e-300)
+    s.close()
+
+
 def test_family_l2_config5_full_size():
     cfg = inputs.config(5)
     s = tsw.Solver.from_config(cfg, "f64")

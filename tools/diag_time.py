@@ -50,6 +50,12 @@ def main():
             ms = med_ms(s.family_l2, reps=3)
             out["family_l2_ms"] = round(ms, 4)
             out["family_l2_GBs"] = round(field / (ms * 1e-3) / 1e9, 1)     # each member's field once
+            # the roof that binds: fp64 instructions (a subtraction and a fused multiply-add per
+            # member pair and node) against the measured fp64 add/multiply rate
+            ops = cfg.batch * (cfg.batch - 1) / 2 * cfg.nx * cfg.ny * 2
+            out["family_l2_TOPs"] = round(ops / (ms * 1e-3) / 1e12, 2)
+            roof = tsw.tsw_alu_probe(0, tsw.TSW_F64)
+            out["family_l2_alu_frac"] = round(ops / (ms * 1e-3) / roof, 3)
         s.close()
         print(json.dumps(out), flush=True)
 

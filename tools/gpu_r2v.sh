@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests/test_tblock_gpu.py tests/test_energy_fused_gpu.py tests/test_peer_gpu.py -q -x -p no:cacheprovider > gpurun_out/pytest_k10.log 2>&1; echo "pytest=$? $(tail -1 gpurun_out/pytest_k10.log)"
-bash tools/abdepth.sh "k10" "f64:8 f64:9 f64:10 f32:8 f32:9 f32:10" 2 "0"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_family_l2 -c 1 -f -o gpurun_out/prof_fam_f64 python tools/fam_one.py f64 > gpurun_out/ncu_fam.log 2>&1; echo "ncu rc=$?"
