@@ -1,8 +1,10 @@
 """S5 fused into S3 (TSW_OPT_ENERGY_FUSE): the last temporally blocked pass of a
 stepping call reduces the discrete energy E^{n−½} (R17, the discrete CL-01 of PAPER.md P:209–213)
-of the two levels it writes — item partials for the faces inside each item, a seam kernel for the
-faces across strip and chunk seams.  It must equal the oracle's energy of the same fields (fp64
-accumulation in a different order: ≤ 1e−12 relative) and leave the fields bitwise unchanged."""
+of the two levels it writes, in the node form of reading R30 (−Σ u^{n+1}·L(u^n) + Σ (u^{n+1} −
+u^n)², the stencil's own L at the pass's last level; per-item fp64 partials summed in a fixed
+order by k_tb_energy_final).  It must equal the oracle's (face-form) energy of the same fields
+(fp64 accumulation in a different order: ≤ 1e−12 relative) and leave the fields bitwise
+unchanged."""
 import numpy as np
 import pytest
 
