@@ -254,9 +254,10 @@ int64_t tsw_launch_count(const tsw_ctx* ctx);
                               the wide CTA */
 #define TSW_OPT_ENERGY_FUSE 14 /* 1 (default): on a single-rank 2D temporally blocked run, the last pass of
                               every tsw_step call also reduces the discrete energy of the two levels it
-                              writes (S5 fused into S3: per-item fp64 partials, plus the faces across its
-                              strip / chunk seams from a small kernel); tsw_energy at that level then
-                              only reads the result.  0: tsw_energy always runs the standalone kernel */
+                              writes (S5 fused into S3 in the node form of reading R30: per-item fp64
+                              partials, summed in a fixed order by one small kernel); tsw_energy at that
+                              level then only reads the result.  0: tsw_energy always runs the
+                              standalone kernel */
 #define TSW_OPT_ENERGY_DRIFT 15 /* blow-up detection in tsw_energy: k (default 2) — TSW_ERR_UNSTABLE
                               when the energy is non-finite or has drifted from the first energy measured
                               after tsw_set_initial / tsw_set_state by more than 10^−k relative (R17: the

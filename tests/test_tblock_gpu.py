@@ -83,10 +83,10 @@ def test_tblock_profile_isotropic_and_auto_chunks(K):
     ref.close()
 
 
-@pytest.mark.parametrize("K", [4, 8])
+@pytest.mark.parametrize("K", [4, 8, 10])
 def test_tblock_bench_shape_sampled(K):
-    """The bench workload (32768 × 4096 δ-line slab) with K = 4 and the bench's K = 8 (the start-up
-    level, passes and a remainder pass): the whole field ≡ the K = 1 run."""
+    """The bench workload (32768 × 4096 δ-line slab) with K = 4, 8 and the bench's K = 10 (the
+    start-up level, passes and a remainder pass): the whole field ≡ the K = 1 run."""
     cfg = inputs.weak_unit(1)
     u0 = inputs.uniform_dense_rows(cfg.nx, cfg.ny, 0, cfg.ny)
     a = _run(cfg, "f64", K, 41 + K // 2, u0)
