@@ -636,6 +636,9 @@ __device__ __forceinline__ void tb_jitter(int R, int warp, int where) {
 // (the others see the stage through that barrier).  Measured 5 % slower than every warp waiting
 // after the barrier (f64 K = 4: 655 vs 693 Gpt/s; f32 K = 8: 1234 vs 1293): the waits of the 8
 // warps overlap, a single waiter's ≈ 90-cycle try_wait is serialised in front of the barrier.
+#ifndef TSW_TB_STARTUP
+#define TSW_TB_STARTUP 1
+#endif
 #ifndef TSW_TB_WAIT1
 #define TSW_TB_WAIT1 0
 #endif
@@ -684,11 +687,14 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // One input row of the wavefront.  `cr` / `cw`: this thread's element in the centre-row buffers
 // of the previous / current row parity (level m at offset m·2·WEP).  MASKED: force the Dirichlet
 // rows/columns to +0 (only items whose dependency cone touches them need it).
-template <typename T, int K, int PH, bool MASKED, int NC, bool EN = false>
+// SU (start-up rows of an item, TSW_TB_STARTUP): only levels m ≤ mcount are computed — at input row
+// i of an unclamped item, level m yields row s0 − K + i − m, which a level-K output needs only when
+// i ≥ 2m, so mcount = ⌊i/2⌋ skips the K(K+1) level-rows per item that no output depends on.
+template <typename T, int K, int PH, bool MASKED, int NC, bool EN = false, bool SU = false>
 __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
                                        int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
                                        T* __restrict__ yc, const T (&lr1)[2], int lane, bool en_on = false,
-                                       double* en_acc = nullptr) {
+                                       double* en_acc = nullptr, int mcount = K) {
     constexpr int V = 2;
     constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
     constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
@@ -701,6 +707,12 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
     T left = lr1[0], right = lr1[1];
 #pragma unroll
     for (int m = 1; m <= K; ++m) {
+        if constexpr (SU) {
+            if (m > mcount) {   // this and every higher level: rows no output depends on
+                if (m == 1) sts_v2(cw, nw);   // level 0's centre row is still read by the next row
+                break;
+            }
+        }
         // level m−1 after its update: rows (r−1, r, r+1) in slots (C, N, O); level m−2: row r in C
         T nleft = (T)0, nright = (T)0;
         if (m < K) {
@@ -729,7 +741,9 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
             guv[k] = gu;
             T gd;
             if (TbYCache<T>::on) {
-                gd = S.gup[m][k];
+                // SU rows: the cached flux of a level computed for the first time is not there yet —
+                // recomputed from the same operands (the cache's gu of the previous row), bit for bit
+                gd = SU ? r_mul(S.c2v[k], r_sub(cu, S.w[m - 1][C][k])) : S.gup[m][k];
                 S.gup[m][k] = gu;
             } else if (TbYCache<T>::smem) {
                 gd = gdv[k];
@@ -919,9 +933,10 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
         }
 
         // one input row: barrier, refill, stage read, wavefront (phase PH), output
-        auto row = [&](auto ph, auto msk, int i) {
+        auto row = [&](auto ph, auto msk, auto su, int i) {
             constexpr int PH = decltype(ph)::value;
             constexpr bool MASKED = decltype(msk)::value;
+            constexpr bool SU = decltype(su)::value;
             const int R = in_lo + i;
             if (TSW_TB_WAIT1 && tid == 0 && i < nload) mbar_wait(&full[gs & dmask], uint32_t(gs >> dlog) & 1u);
             if (TSW_TB_JITTER) tb_jitter(R, warp, 0);
@@ -962,8 +977,8 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
             }
             T lastk[V];
             const bool en_on = EN && out_cols && (R - K >= s0) && (R - K < s1);
-            tb_row<T, K, PH, MASKED, NC, EN>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1, lane, en_on,
-                                            &en_acc);
+            tb_row<T, K, PH, MASKED, NC, EN, SU>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1, lane,
+                                                en_on, &en_acc, i >> 1);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
                 // level K−1 after this row: rows (ro−1, ro, ro+1) in slots (C, N, O) of phase PH
@@ -989,16 +1004,17 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
             okp += a.pitch;
         };
         // rows [i0, i1) of the item; i0 is a multiple of 3 (the window phase is i mod 3)
-        auto run_rows = [&](auto msk, int i0, int i1) {
+        auto run_rows = [&](auto msk, auto su, int i0, int i1) {
             int i = i0;
             for (; i + 3 <= i1; i += 3) {
-                row(std::integral_constant<int, 0>{}, msk, i);
-                row(std::integral_constant<int, 1>{}, msk, i + 1);
-                row(std::integral_constant<int, 2>{}, msk, i + 2);
+                row(std::integral_constant<int, 0>{}, msk, su, i);
+                row(std::integral_constant<int, 1>{}, msk, su, i + 1);
+                row(std::integral_constant<int, 2>{}, msk, su, i + 2);
             }
-            if (i < i1) row(std::integral_constant<int, 0>{}, msk, i++);
-            if (i < i1) row(std::integral_constant<int, 1>{}, msk, i++);
+            if (i < i1) row(std::integral_constant<int, 0>{}, msk, su, i++);
+            if (i < i1) row(std::integral_constant<int, 1>{}, msk, su, i++);
         };
+        constexpr std::integral_constant<bool, false> no_su{};
         // Input row i computes levels m = 1..K at rows R − m (R = in_lo + i); it needs the
         // boundary selects only while one of those rows lies outside [rowlo, rowhi].  In a strip
         // clear of the boundary columns the item runs masked only at its ends (segment limits
@@ -1020,10 +1036,21 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
             const int lo = (sg == 0) ? 0 : (sg == 1 ? ua : ub);
             const int hi = (sg == 0) ? ua : (sg == 1 ? ub : L);
             if (lo >= hi) continue;
-            if (sg == 1)
-                run_rows(std::integral_constant<bool, false>{}, lo, hi);
-            else
-                run_rows(std::integral_constant<bool, true>{}, lo, hi);
+            if (sg == 1) {
+                // an unclamped item's first ⌊2K/3⌋·3 rows compute only the levels its outputs need
+                // (a multiple of 3: the window phase) with the y-flux cache, up to a row at which
+                // every level was computed, so that the rows after it (plain or masked) find every
+                // cached flux
+                constexpr int SU_ROWS = TbYCache<T>::on ? (2 * K + 3) / 3 * 3 : (2 * K / 3) * 3;
+                int mid = lo;
+                if (TSW_TB_STARTUP && lo == 0 && in_lo == s0 - K && hi >= SU_ROWS) {
+                    mid = SU_ROWS;
+                    run_rows(std::integral_constant<bool, false>{}, std::integral_constant<bool, true>{}, 0, mid);
+                }
+                run_rows(std::integral_constant<bool, false>{}, no_su, mid, hi);
+            } else {
+                run_rows(std::integral_constant<bool, true>{}, no_su, lo, hi);
+            }
         }
         if constexpr (EN) {
             const double v = warp_sum_d(en_acc);
