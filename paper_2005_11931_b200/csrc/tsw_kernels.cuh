@@ -567,23 +567,14 @@ struct TbPad {
 };
 
 // Caching the upper y-flux for the next row saves 2 fp ops per update (identical operands, so the
-// tree is unchanged bit for bit).  fp32 keeps it in registers (2V per level); fp64 has no spare
-// registers and keeps it in shared memory (one 16-byte load + store per level and thread, each
-// thread touching only its own slots — no barrier).
-// fp64 y-flux cache in shared memory: measured 15 % slower on B200 (K = 4: 569 vs 657 Gpt/s,
-// interleaved A/B on one box) — the load sits in the dependency chain — so it is off by default.
-// Round 2: the same cache with the load issued one level ahead (with the next level's neighbours):
-// K = 6 630 vs 812 Gpt/s, K = 8 613 vs 903 — its (K+1)·NT·V words of shared memory (37 KB at K = 8)
-// leave room for one CTA per SM instead of two; rejected again.
-#ifndef TSW_TB_YCACHE_SMEM
-#define TSW_TB_YCACHE_SMEM 0
-#endif
+// tree is unchanged bit for bit).  fp32 keeps it in registers (2V per level).  fp64 recomputes it:
+// in registers (TSW_TB_YCACHE_F64 = 1) it measured +3 % at K = 7, −2 % at K = 8, −27 % at K = 10
+// (spills); in shared or tensor memory it was slower still (measured and rejected).
 #ifndef TSW_TB_YCACHE_F64
 #define TSW_TB_YCACHE_F64 0
 #endif
 template <typename T> struct TbYCache {
     static constexpr bool on = sizeof(T) == 4 || TSW_TB_YCACHE_F64;      // registers
-    static constexpr bool smem = sizeof(T) == 8 && TSW_TB_YCACHE_SMEM;     // shared memory
 };
 
 // Register budget and CTA width.  A CTA of NC warps is sized for 16 / NC CTAs per SM (at least
@@ -632,15 +623,11 @@ __device__ __forceinline__ void tb_jitter(int R, int warp, int where) {
     if ((h & 7u) == 0u) __nanosleep(h % 2048u);   // one row in eight, per warp
 }
 
-// TSW_TB_WAIT1=1: only thread 0 waits on a stage's "full" mbarrier, before the per-row CTA barrier
-// (the others see the stage through that barrier).  Measured 5 % slower than every warp waiting
-// after the barrier (f64 K = 4: 655 vs 693 Gpt/s; f32 K = 8: 1234 vs 1293): the waits of the 8
-// warps overlap, a single waiter's ≈ 90-cycle try_wait is serialised in front of the barrier.
+// Every warp waits on a stage's "full" mbarrier after the per-row CTA barrier: a single waiter
+// before the barrier measured 5 % slower (its ≈ 90-cycle try_wait is serialised).
+// TSW_TB_STARTUP = 0 runs an item's start-up rows with every level (no level cut, see tb_row).
 #ifndef TSW_TB_STARTUP
 #define TSW_TB_STARTUP 1
-#endif
-#ifndef TSW_TB_WAIT1
-#define TSW_TB_WAIT1 0
 #endif
 
 // Measured and rejected (round 2): the left/right neighbours of every level from the
@@ -652,8 +639,7 @@ template <typename T, int K, int NC = TB_NC>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
     return size_t(depth) * 2 * TbGeom<T, K, NC>::WE * sizeof(T) +
            size_t(K) * 2 * (TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P) * sizeof(T) +
-           (size_t(depth) * sizeof(uint64_t) + 15) / 16 * 16 +
-           (TbYCache<T>::smem ? size_t(K + 1) * TbGeom<T, K, NC>::NT * TbGeom<T, K, NC>::V * sizeof(T) : 0);
+           (size_t(depth) * sizeof(uint64_t) + 15) / 16 * 16;
 }
 
 // Per-thread state of one item's wavefront.  Window slots rotate with the row phase PH ∈ {0,1,2}:
@@ -693,7 +679,7 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 template <typename T, int K, int PH, bool MASKED, int NC, bool EN = false, bool SU = false>
 __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ cr, T* __restrict__ cw, int rowlo,
                                        int rowhi, int R, const T (&nw)[2], const T (&pv_new)[2], T (&lastk)[2],
-                                       T* __restrict__ yc, const T (&lr1)[2], int lane, bool en_on = false,
+                                       const T (&lr1)[2], int lane, bool en_on = false,
                                        double* en_acc = nullptr, int mcount = K) {
     constexpr int V = 2;
     constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
@@ -732,21 +718,16 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
         T nv[V];
         bool rowok = true;
         if (MASKED) rowok = unsigned(R - m - rowlo) <= unsigned(rowhi - rowlo);
-        T gdv[V], guv[V];
-        if (TbYCache<T>::smem) lds_v2(yc + m * TbGeom<T, K, NC>::NT * V, gdv);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const T cu = S.w[m - 1][N][k];
             const T gu = r_mul(S.c2v[k], r_sub(S.w[m - 1][O][k], cu));
-            guv[k] = gu;
             T gd;
             if (TbYCache<T>::on) {
                 // SU rows: the cached flux of a level computed for the first time is not there yet —
                 // recomputed from the same operands (the cache's gu of the previous row), bit for bit
                 gd = SU ? r_mul(S.c2v[k], r_sub(cu, S.w[m - 1][C][k])) : S.gup[m][k];
                 S.gup[m][k] = gu;
-            } else if (TbYCache<T>::smem) {
-                gd = gdv[k];
             } else {
                 gd = r_mul(S.c2v[k], r_sub(cu, S.w[m - 1][C][k]));
             }
@@ -781,7 +762,6 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
                 }
             }
         }
-        if (TbYCache<T>::smem) sts_v2(yc + m * TbGeom<T, K, NC>::NT * V, guv);
         if (m < K) {
 #pragma unroll
             for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
@@ -813,10 +793,6 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
     T* cen = cenp + PAD;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    // y-flux cache (fp64): [K+1][NT][V] after the mbarriers (16-byte aligned: depth is even or the
-    // barrier block is padded below)
-    T* ycache = reinterpret_cast<T*>(reinterpret_cast<char*>(full) + ((size_t(depth) * sizeof(uint64_t) + 15) / 16) * 16) +
-                tid * V;
     for (int e = tid; e < int(CEN_ELEMS); e += blockDim.x) cenp[e] = (T)0;  // pads stay 0
     __shared__ double en_red[EN ? NC : 1];   // EN: per-item warp sums
     if (tid == 0) {
@@ -917,11 +893,6 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
             for (int m = 0; m <= (TbYCache<T>::on ? K : 0); ++m)
 #pragma unroll
                 for (int k = 0; k < V; ++k) S.gup[m][k] = (T)0;
-        if (TbYCache<T>::smem) {
-            const T z2[V] = {(T)0, (T)0};
-#pragma unroll
-            for (int m = 0; m <= K; ++m) sts_v2(ycache + m * G::NT * V, z2);
-        }
         const int nload = in_hi - in_lo;
         const int L = s1 + K - in_lo;
         // this item's stage stream: input row in_lo + j at element ibase + j·pitch; prefill
@@ -938,7 +909,6 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
             constexpr bool MASKED = decltype(msk)::value;
             constexpr bool SU = decltype(su)::value;
             const int R = in_lo + i;
-            if (TSW_TB_WAIT1 && tid == 0 && i < nload) mbar_wait(&full[gs & dmask], uint32_t(gs >> dlog) & 1u);
             if (TSW_TB_JITTER) tb_jitter(R, warp, 0);
             __syncthreads();  // the previous rows' stages and centre rows are consumed / published
             if (TSW_TB_JITTER) tb_jitter(R, warp, 1);
@@ -966,7 +936,7 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
             const bool refill = (i < nload);
             if (refill) {
                 const int cslot = gs & dmask;
-                if (!TSW_TB_WAIT1) mbar_wait(&full[cslot], uint32_t(gs >> dlog) & 1u);
+                mbar_wait(&full[cslot], uint32_t(gs >> dlog) & 1u);
                 const T* st = ring + size_t(cslot) * 2 * WE;
                 lds_v2(st + e0, nw);
                 lds_v2(st + WE + e0, pv_new);
@@ -977,7 +947,7 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
             }
             T lastk[V];
             const bool en_on = EN && out_cols && (R - K >= s0) && (R - K < s1);
-            tb_row<T, K, PH, MASKED, NC, EN, SU>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, ycache, lr1, lane,
+            tb_row<T, K, PH, MASKED, NC, EN, SU>(S, cr, cw, rowlo, rowhi, R, nw, pv_new, lastk, lr1, lane,
                                                 en_on, &en_acc, i >> 1);
             const int ro = R - K;
             if (out_cols && ro >= s0 && ro < s1) {
