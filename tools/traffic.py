@@ -1,5 +1,6 @@
 """Add a traffic.json entry from an `ncu --set full` report of one stencil launch on the bench
-workload:  python tools/traffic.py REPORT.ncu-rep KEY LEVELS [raw_csv_out]"""
+workload:  python tools/traffic.py REPORT.ncu-rep|RAW.csv KEY LEVELS [raw_csv_out]
+(RAW.csv: the report's `ncu -i REPORT --page raw --csv` export)"""
 import csv
 import io
 import json
@@ -8,7 +9,8 @@ import subprocess
 import sys
 
 rep, key, levels = sys.argv[1], sys.argv[2], int(sys.argv[3])
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = (open(rep).read() if rep.endswith(".csv") else
+       subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
 if len(sys.argv) > 4:
     open(sys.argv[4], "w").write(raw)
 r = list(csv.reader(io.StringIO(raw)))
