@@ -570,11 +570,20 @@ struct TbPad {
 // tree is unchanged bit for bit).  fp32 keeps it in registers (2V per level).  fp64 recomputes it:
 // in registers (TSW_TB_YCACHE_F64 = 1) it measured +3 % at K = 7, −2 % at K = 8, −27 % at K = 10
 // (spills); in shared or tensor memory it was slower still (measured and rejected).
+// TSW_TB_YCACHE_F64_LEVELS = L caches it for the first L levels only (the registers left under
+// the 170-register budget).
 #ifndef TSW_TB_YCACHE_F64
 #define TSW_TB_YCACHE_F64 0
 #endif
+#ifndef TSW_TB_YCACHE_F64_LEVELS
+#define TSW_TB_YCACHE_F64_LEVELS 0
+#endif
 template <typename T> struct TbYCache {
-    static constexpr bool on = sizeof(T) == 4 || TSW_TB_YCACHE_F64;      // registers
+    // levels 1..levels<K>() keep the flux in registers
+    template <int K> __host__ __device__ static constexpr int levels() {
+        return (sizeof(T) == 4 || TSW_TB_YCACHE_F64) ? K
+                                                      : (TSW_TB_YCACHE_F64_LEVELS < K ? TSW_TB_YCACHE_F64_LEVELS : K);
+    }
 };
 
 // Register budget and CTA width.  A CTA of NC warps is sized for 16 / NC CTAs per SM (at least
@@ -651,7 +660,7 @@ template <typename T, int K>
 struct TbState {
     static constexpr int V = 2;
     T w[K][3][V];
-    T gup[TbYCache<T>::on ? K + 1 : 1][V];  // level m's y-flux c2·(u_{r+1} − u_r) of level m−1 at its last row r: the next
+    T gup[TbYCache<T>::template levels<K>() + 1][V];  // level m's y-flux c2·(u_{r+1} − u_r) of level m−1 at its last row r: the next
                       // row's lower flux (identical operands, so the tree is unchanged bit for bit)
     T pm1[V];
     T c1l[V], c1r[V], c2v[V];
@@ -723,7 +732,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
             const T cu = S.w[m - 1][N][k];
             const T gu = r_mul(S.c2v[k], r_sub(S.w[m - 1][O][k], cu));
             T gd;
-            if (TbYCache<T>::on) {
+            if (m <= TbYCache<T>::template levels<K>()) {
                 // SU rows: the cached flux of a level computed for the first time is not there yet —
                 // recomputed from the same operands (the cache's gu of the previous row), bit for bit
                 gd = SU ? r_mul(S.c2v[k], r_sub(cu, S.w[m - 1][C][k])) : S.gup[m][k];
@@ -888,9 +897,8 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
                 for (int k = 0; k < V; ++k) S.w[m][q][k] = (T)0;
 #pragma unroll
         for (int k = 0; k < V; ++k) S.pm1[k] = (T)0;
-        if (TbYCache<T>::on)
 #pragma unroll
-            for (int m = 0; m <= (TbYCache<T>::on ? K : 0); ++m)
+            for (int m = 0; m <= TbYCache<T>::template levels<K>(); ++m)
 #pragma unroll
                 for (int k = 0; k < V; ++k) S.gup[m][k] = (T)0;
         const int nload = in_hi - in_lo;
@@ -1011,7 +1019,8 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
                 // (a multiple of 3: the window phase) with the y-flux cache, up to a row at which
                 // every level was computed, so that the rows after it (plain or masked) find every
                 // cached flux
-                constexpr int SU_ROWS = TbYCache<T>::on ? (2 * K + 3) / 3 * 3 : (2 * K / 3) * 3;
+                constexpr int YCL = TbYCache<T>::template levels<K>();
+                constexpr int SU_ROWS = (2 * K / 3) * 3 >= 2 * YCL + 1 ? (2 * K / 3) * 3 : (2 * YCL + 3) / 3 * 3;
                 int mid = lo;
                 if (TSW_TB_STARTUP && lo == 0 && in_lo == s0 - K && hi >= SU_ROWS) {
                     mid = SU_ROWS;

@@ -21,20 +21,24 @@ def needed_rows(K, s0, s1):
     return need
 
 
-def su_rows(K, cache):
-    return (2 * K + 3) // 3 * 3 if cache else (2 * K // 3) * 3
+def su_rows(K, ycl):
+    """The kernel's SU_ROWS for a y-flux cache on levels 1..ycl (fp32: ycl = K; fp64: 0, or
+    TSW_TB_YCACHE_F64_LEVELS)."""
+    return (2 * K // 3) * 3 if (2 * K // 3) * 3 >= 2 * ycl + 1 else (2 * ycl + 3) // 3 * 3
 
 
 @pytest.mark.parametrize("K", [2, 3, 4, 5, 7, 8, 9, 10])
-@pytest.mark.parametrize("cache", [False, True])
-def test_startup_cut_is_exact(K, cache):
+@pytest.mark.parametrize("ycl", [0, 2, 4, "K"])
+def test_startup_cut_is_exact(K, ycl):
+    ycl = K if ycl == "K" else min(ycl, K)
+    cache = ycl > 0
     s0, s1 = 100, 137
     in_lo = s0 - K
     L = s1 + K - in_lo
     need = needed_rows(K, s0, s1)
-    SU = su_rows(K, cache)
+    SU = su_rows(K, ycl)
     assert SU % 3 == 0                                 # the window phase of the next row is 0
-    if cache:                                          # the shortest such cut after row 2K
+    if ycl == K:                                       # the shortest such cut after row 2K
         assert SU == -(-(2 * K + 1) // 3) * 3
     for i in range(L):
         for m in range(1, K + 1):
@@ -47,8 +51,8 @@ def test_startup_cut_is_exact(K, cache):
     # the plain rows after the cut read each level's cached flux from the previous row: every level
     # must have been computed at row SU − 1 (the cache variant) — and every needed row before the
     # cut is computed in both variants (checked above)
-    if cache:
-        assert (SU - 1) // 2 >= K
+    if cache:   # every cached level ran at row SU − 1 (its first needed row is 2m ≤ SU − 1)
+        assert (SU - 1) // 2 >= ycl
 
 
 @pytest.mark.parametrize("K", [2, 5, 10])
