@@ -644,10 +644,38 @@ __device__ __forceinline__ void tb_jitter(int R, int warp, int where) {
 // fp64 909 → 815 Gpt/s, fp32 1531 → 1355 (the baseline's MIO throttle is ≈ 0; the shuffles and
 // edge selects add issue slots).
 
+// Centre-row buffers (one row per level and parity).  Default: columns in order, a thread's two
+// columns as one 16-byte store, its left / right neighbours as two 8-byte loads at a 16-byte stride
+// (4 wavefronts each).  TSW_TB_SPLIT_CEN = 1: even columns then odd columns (with a zero pad
+// between), so both neighbour loads are consecutive across the warp (2 wavefronts each) and the
+// store becomes two consecutive 8-byte stores.
+#ifndef TSW_TB_SPLIT_CEN
+#define TSW_TB_SPLIT_CEN 0
+#endif
+template <typename T, int K, int NC>
+struct TbCen {
+    static constexpr int P = TbPad<T>::P, NT = TbGeom<T, K, NC>::NT, WE = TbGeom<T, K, NC>::WE;
+    static constexpr bool split = TSW_TB_SPLIT_CEN;
+    static constexpr int WEP = split ? WE + 3 * P : WE + 2 * P;   // one row, pads included
+    static constexpr int OOFF = NT + P;                           // split: odd region − even region
+    static constexpr int LOFF = split ? OOFF - 1 : -1;            // column 2t − 1 (odd of t − 1)
+    static constexpr int ROFF = split ? 1 : 2;                    // column 2t + 2 (even of t + 1)
+    __host__ __device__ static constexpr int base(int tid) { return split ? tid : 2 * tid; }
+};
+template <typename T, int K, int NC>
+__device__ __forceinline__ void cen_store(T* p, const T (&v)[2]) {
+    if constexpr (TbCen<T, K, NC>::split) {
+        p[0] = v[0];
+        p[TbCen<T, K, NC>::OOFF] = v[1];
+    } else {
+        sts_v2(p, v);
+    }
+}
+
 template <typename T, int K, int NC = TB_NC>
 __host__ __device__ constexpr size_t tb_smem_bytes(int depth) {
     return size_t(depth) * 2 * TbGeom<T, K, NC>::WE * sizeof(T) +
-           size_t(K) * 2 * (TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P) * sizeof(T) +
+           size_t(K) * 2 * TbCen<T, K, NC>::WEP * sizeof(T) +
            (size_t(depth) * sizeof(uint64_t) + 15) / 16 * 16;
 }
 
@@ -691,7 +719,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
                                        const T (&lr1)[2], int lane, bool en_on = false,
                                        double* en_acc = nullptr, int mcount = K) {
     constexpr int V = 2;
-    constexpr int WEP = TbGeom<T, K, NC>::WE + 2 * TbPad<T>::P;
+    constexpr int WEP = TbCen<T, K, NC>::WEP;
     constexpr int O = PH % 3, C = (PH + 1) % 3, N = (PH + 2) % 3;  // pre-update roles
     // level 0
 #pragma unroll
@@ -704,7 +732,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
     for (int m = 1; m <= K; ++m) {
         if constexpr (SU) {
             if (m > mcount) {   // this and every higher level: rows no output depends on
-                if (m == 1) sts_v2(cw, nw);   // level 0's centre row is still read by the next row
+                if (m == 1) cen_store<T, K, NC>(cw, nw);   // level 0's centre row is still read by the next row
                 break;
             }
         }
@@ -712,10 +740,10 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
         T nleft = (T)0, nright = (T)0;
         if (m < K) {
             const T* cn = cr + m * 2 * WEP;
-            nleft = cn[-1];
-            nright = cn[V];
+            nleft = cn[TbCen<T, K, NC>::LOFF];
+            nright = cn[TbCen<T, K, NC>::ROFF];
         }
-        if (m == 1) sts_v2(cw, nw);
+        if (m == 1) cen_store<T, K, NC>(cw, nw);
         // canonical tree with shared face fluxes:
         //   F_{i+1/2} = c1_{i+1/2}·(u_{i+1} − u_i) is node i's right and node i+1's left x-flux,
         //   G_{j+1/2} = c2·(u_{j+1} − u_j) is row j's upper and row j+1's lower y-flux
@@ -774,7 +802,7 @@ __device__ __forceinline__ void tb_row(TbState<T, K>& S, const T* __restrict__ c
         if (m < K) {
 #pragma unroll
             for (int k = 0; k < V; ++k) S.w[m][O][k] = nv[k];
-            sts_v2(cw + m * 2 * WEP, nv);
+            cen_store<T, K, NC>(cw + m * 2 * WEP, nv);
         } else {
 #pragma unroll
             for (int k = 0; k < V; ++k) lastk[k] = nv[k];
@@ -793,7 +821,7 @@ template <typename T, int K, bool PEER = false, int NC = TB_NC, bool EN = false>
 __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(const TbArgs<T> a, int depth) {
     using G = TbGeom<T, K, NC>;
     constexpr int V = G::V, H = G::H, WE = G::WE, WO = G::WO;
-    constexpr int PAD = TbPad<T>::P, WEP = WE + 2 * PAD;
+    constexpr int PAD = TbPad<T>::P, WEP = TbCen<T, K, NC>::WEP;
     extern __shared__ __align__(128) unsigned char smem[];
     T* ring = reinterpret_cast<T*>(smem);                    // [depth][2][WE]
     T* cenp = ring + size_t(depth) * 2 * WE;                 // [K][2][WEP], row data at +PAD
@@ -845,8 +873,9 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
     const int dlog = __ffs(depth) - 1;
 
     const int e0 = tid * V;  // my first column of the extended strip
-    T* const cen0 = cen + e0;          // my element in the centre-row buffers of parity 0 / 1
-    T* const cen1 = cen + WEP + e0;
+    const int ce0 = TbCen<T, K, NC>::base(tid);
+    T* const cen0 = cen + ce0;         // my element in the centre-row buffers of parity 0 / 1
+    T* const cen1 = cen + WEP + ce0;
     // interior storage rows of the global grid: g ∈ [1, ny−2] ⇔ storage s ∈ [rowlo, rowhi]
     const int rowlo = int(1 - a.r0 + 1), rowhi = int(a.ny - 2 - a.r0 + 1);
     int gs = 0;         // rows loaded from the ring so far: slot gs & dmask, phase parity (gs >> dlog) & 1
@@ -935,11 +964,11 @@ __global__ void __launch_bounds__(NC * 32, tb_minb<T, K, NC>()) k_step2d_tb(cons
                 cw = par ? cen1 : cen0;
                 cr = par ? cen0 : cen1;
             } else {                            // fp64 (no spare registers): recomputed per row
-                cw = cen + par * WEP + e0;
-                cr = cen + (par ^ 1) * WEP + e0;
+                cw = cen + par * WEP + ce0;
+                cr = cen + (par ^ 1) * WEP + ce0;
             }
-            lr1[0] = cr[-1];
-            lr1[1] = cr[V];
+            lr1[0] = cr[TbCen<T, K, NC>::LOFF];
+            lr1[1] = cr[TbCen<T, K, NC>::ROFF];
             T nw[V], pv_new[V];
             const bool refill = (i < nload);
             if (refill) {
